@@ -1,0 +1,234 @@
+"""ctypes front-end of the CPU fp64 oracle (oracle/pot3d_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this package.  The product path
+(paper_1709_01126_b200/) never imports it and shares no code with it.
+
+Array conventions follow synth/: faces 1-D; br0 shape (np, nt); Phi and every
+cell array shape (np, nt, nr) in C order (r fastest, m = i + nr*(j + nt*k),
+the Fortran x(i,j,k) of PAPER.md P:222-224).
+
+Parity status of each function:
+  assemble/apply   pinned: symmetry, null space, closed-form dipole/multipole,
+                   hand-evaluated coefficients, dense brute force.
+  rhs              pinned: closed form, S:234 hand evaluation, Σb = 0 (CW).
+  solve (PC1/PC2)  pinned: dense brute force, SPEC 2x2, closed form,
+                   monotone PC2 degradation, decomposition invariance.
+  ilu0             pinned: defining property (LU)_ij = a_ij on the pattern,
+                   tridiagonal exact LU.
+  field            pinned: Br(r0) = Br0, Phi=r -> Br=1, V div B = b - A Phi,
+                   closed-form dipole field.
+  polar_average    pinned: constant ring, cos(phi) ring.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_SRC = _HERE / "pot3d_oracle.c"
+_LIB = _HERE / "liboracle.so"
+
+SOURCE_SURFACE = 0
+CLOSED_WALL = 1
+
+STATUS = {0: "converged", 1: "not_converged", 2: "pc2_fell_back_to_pc1",
+          -1: "invalid_argument", -4: "indefinite"}
+
+
+def build(force: bool = False) -> Path:
+    """Compile the oracle with gcc (plain IEEE fp64: no FMA contraction)."""
+    if force or not _LIB.exists() or _LIB.stat().st_mtime < _SRC.stat().st_mtime:
+        tmp = _LIB.with_suffix(f".so.tmp{os.getpid()}")
+        cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-shared",
+               "-fPIC", "-std=c11", "-o", str(tmp), str(_SRC), "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(str(_LIB))
+        P = ctypes.POINTER
+        d = P(ctypes.c_double)
+        i64 = P(ctypes.c_int64)
+        ci = ctypes.c_int
+        L.orc_assemble.argtypes = [ci, ci, ci, d, d, d, ci, d, d]
+        L.orc_apply.argtypes = [ci, ci, ci, d, d, d, d]
+        L.orc_apply.restype = None
+        L.orc_rhs.argtypes = [ci, ci, ci, d, d, d, ci, d, d, d]
+        L.orc_solve.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, d, ctypes.c_double,
+                                ctypes.c_int64, d, i64, d, d, d]
+        L.orc_precond.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, d, d]
+        L.orc_block_ilu0.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, i64, i64, d, d]
+        L.orc_ilu0_csr.argtypes = [ctypes.c_int64, i64, i64, d]
+        L.orc_polar_average.argtypes = [ci, ci, ci, d, d, ci, d]
+        L.orc_polar_average.restype = None
+        L.orc_field.argtypes = [ci, ci, ci, d, d, d, ci, d, d, d, d, d]
+        L.orc_volumes.argtypes = [ci, ci, ci, d, d, d, d]
+        L.orc_solve_fixed.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, d, ctypes.c_int64, d, d]
+        _lib = L
+    return _lib
+
+
+def _d(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _i(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+def _f(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class System:
+    """The discrete problem on one grid: DIA bands + wrap couplings."""
+
+    def __init__(self, rf, tf, pf, bc=SOURCE_SURFACE):
+        self.rf, self.tf, self.pf = _f(rf), _f(tf), _f(pf)
+        self.nr, self.nt, self.np = len(rf) - 1, len(tf) - 1, len(pf) - 1
+        self.bc = bc
+        self.N = self.nr * self.nt * self.np
+        self.bands = np.zeros((7, self.N))
+        self.wrap = np.zeros((2, self.nr * self.nt))
+        rc = lib().orc_assemble(self.nr, self.nt, self.np, _d(self.rf), _d(self.tf), _d(self.pf),
+                                bc, _d(self.bands), _d(self.wrap))
+        if rc:
+            raise ValueError("invalid grid")
+
+    @property
+    def shape(self):
+        return (self.np, self.nt, self.nr)
+
+    def apply(self, x):
+        x = _f(x).reshape(-1)
+        y = np.empty_like(x)
+        lib().orc_apply(self.nr, self.nt, self.np, _d(self.bands), _d(self.wrap), _d(x), _d(y))
+        return y.reshape(self.shape)
+
+    def diag(self):
+        return self.bands[3].reshape(self.shape).copy()
+
+    def rhs(self, br0, return_adjusted=False):
+        br0 = _f(br0)
+        b = np.empty(self.N)
+        adj = np.empty(self.nt * self.np)
+        lib().orc_rhs(self.nr, self.nt, self.np, _d(self.rf), _d(self.tf), _d(self.pf), self.bc,
+                      _d(br0), _d(b), _d(adj))
+        if return_adjusted:
+            return b.reshape(self.shape), adj.reshape(self.np, self.nt)
+        return b.reshape(self.shape)
+
+    def volumes(self):
+        v = np.empty(self.N)
+        lib().orc_volumes(self.nr, self.nt, self.np, _d(self.rf), _d(self.tf), _d(self.pf), _d(v))
+        return v.reshape(self.shape)
+
+    def dense(self):
+        """Materialise A by applying it to unit vectors (small grids only)."""
+        if self.N > 4096:
+            raise ValueError("dense_of refuses n > 4096 (S:148)")
+        A = np.empty((self.N, self.N))
+        e = np.zeros(self.N)
+        for c in range(self.N):
+            e[c] = 1.0
+            A[:, c] = self.apply(e).reshape(-1)
+            e[c] = 0.0
+        return A
+
+
+def solve(rf, tf, pf, br0, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1, rtol=1e-9, maxit=100000,
+          history=False):
+    """Oracle PCG solve.  Returns dict(x, iters, rel_res, true_rel_res, status[, hist])."""
+    rf, tf, pf, br0 = _f(rf), _f(tf), _f(pf), _f(br0)
+    nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
+    x = np.zeros(nr * nt * np_)
+    it = np.zeros(1, dtype=np.int64)
+    rr = np.zeros(1)
+    tr = np.zeros(1)
+    hist = np.zeros(int(maxit) + 1) if history else None
+    st = lib().orc_solve(nr, nt, np_, _d(rf), _d(tf), _d(pf), bc, pc, pc2_blocks, _d(br0),
+                         float(rtol), int(maxit), _d(x), _i(it), _d(rr), _d(tr),
+                         _d(hist) if history else None)
+    out = dict(x=x.reshape(np_, nt, nr), iters=int(it[0]), rel_res=float(rr[0]),
+               true_rel_res=float(tr[0]), status=st)
+    if history:
+        out["hist"] = hist[: out["iters"] + 1]
+    return out
+
+
+def precond(rf, tf, pf, r, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1):
+    rf, tf, pf, r = _f(rf), _f(tf), _f(pf), _f(r).reshape(-1)
+    nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
+    z = np.empty_like(r)
+    rc = lib().orc_precond(nr, nt, np_, _d(rf), _d(tf), _d(pf), bc, pc, pc2_blocks, _d(r), _d(z))
+    if rc:
+        raise RuntimeError(f"preconditioner build failed ({rc})")
+    return z.reshape(np_, nt, nr)
+
+
+def block_ilu0(rf, tf, pf, i0, i1, bc=SOURCE_SURFACE):
+    """CSR pattern, A values and ILU0 values of the r-slab block [i0, i1)."""
+    rf, tf, pf = _f(rf), _f(tf), _f(pf)
+    nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
+    n = (i1 - i0) * nt * np_
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    col = np.zeros(7 * n, dtype=np.int64)
+    aval = np.zeros(7 * n)
+    lu = np.zeros(7 * n)
+    rc = lib().orc_block_ilu0(nr, nt, np_, _d(rf), _d(tf), _d(pf), bc, i0, i1, _i(rowptr),
+                              _i(col), _d(aval), _d(lu))
+    nnz = int(rowptr[-1])
+    return rowptr, col[:nnz], aval[:nnz], lu[:nnz], rc
+
+
+def ilu0_csr(rowptr, col, val):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int64)
+    v = _f(val).copy()
+    rc = lib().orc_ilu0_csr(len(rowptr) - 1, _i(rowptr), _i(col), _d(v))
+    return v, rc
+
+
+def polar_average(pf, x, south=False):
+    x = _f(x)
+    np_, nt, nr = x.shape
+    avg = np.empty(nr)
+    lib().orc_polar_average(nr, nt, np_, _d(_f(pf)), _d(x), int(south), _d(avg))
+    return avg
+
+
+def field(rf, tf, pf, br0, x, bc=SOURCE_SURFACE):
+    rf, tf, pf, br0, x = _f(rf), _f(tf), _f(pf), _f(br0), _f(x)
+    nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
+    br = np.empty((np_, nt, nr + 1))
+    bt = np.empty((np_, nt + 1, nr))
+    bp = np.empty((np_, nt, nr))
+    rc = lib().orc_field(nr, nt, np_, _d(rf), _d(tf), _d(pf), bc, _d(br0), _d(x), _d(br), _d(bt),
+                         _d(bp))
+    if rc:
+        raise ValueError("invalid grid")
+    return br, bt, bp
+
+
+def solve_fixed(rf, tf, pf, br0, iters, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1):
+    """Exactly `iters` PCG iterations (rtol = 0): the timed cpu_baseline sample."""
+    rf, tf, pf, br0 = _f(rf), _f(tf), _f(pf), _f(br0)
+    nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
+    x = np.zeros(nr * nt * np_)
+    rr = np.zeros(1)
+    st = lib().orc_solve_fixed(nr, nt, np_, _d(rf), _d(tf), _d(pf), bc, pc, pc2_blocks, _d(br0),
+                               int(iters), _d(x), _d(rr))
+    return x.reshape(np_, nt, nr), float(rr[0]), st
