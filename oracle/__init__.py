@@ -76,7 +76,7 @@ def lib():
         L.orc_polar_average.restype = None
         L.orc_field.argtypes = [ci, ci, ci, d, d, d, ci, d, d, d, d, d]
         L.orc_volumes.argtypes = [ci, ci, ci, d, d, d, d]
-        L.orc_solve_fixed.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, d, ctypes.c_int64, d, d]
+        L.orc_solve_fixed.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, d, ctypes.c_int64, d, d, d]
         _lib = L
     return _lib
 
@@ -224,11 +224,13 @@ def field(rf, tf, pf, br0, x, bc=SOURCE_SURFACE):
 
 
 def solve_fixed(rf, tf, pf, br0, iters, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1):
-    """Exactly `iters` PCG iterations (rtol = 0): the timed cpu_baseline sample."""
+    """Exactly `iters` PCG iterations (rtol = 0): the timed cpu_baseline sample.
+    Returns (x, rel_res, status, seconds spent in the PCG loop)."""
     rf, tf, pf, br0 = _f(rf), _f(tf), _f(pf), _f(br0)
     nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
     x = np.zeros(nr * nt * np_)
     rr = np.zeros(1)
+    secs = np.zeros(1)
     st = lib().orc_solve_fixed(nr, nt, np_, _d(rf), _d(tf), _d(pf), bc, pc, pc2_blocks, _d(br0),
-                               int(iters), _d(x), _d(rr))
-    return x.reshape(np_, nt, nr), float(rr[0]), st
+                               int(iters), _d(x), _d(rr), _d(secs))
+    return x.reshape(np_, nt, nr), float(rr[0]), st, float(secs[0])

@@ -36,6 +36,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #define ORC_SOURCE_SURFACE 0
 #define ORC_CLOSED_WALL 1
@@ -432,6 +433,15 @@ static void pc_free(orc_pc *M) {
   free(M->rb); free(M->zb);
 }
 
+/* Wall time of the last orc_solve PCG loop (instrumentation for the timed
+ * cpu_baseline; not part of the method). */
+static double g_loop_seconds = 0.0;
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
 /* Plain sequential inner product in index order. */
 static double dot(int64_t n, const double *x, const double *y) {
   double s = 0.0;
@@ -489,6 +499,7 @@ int orc_solve(int nr, int nt, int np, const double *rf, const double *tf,
   for (int64_t m = 0; m < N; m++) p[m] = z[m];
   double rho = dot(N, r, z);
   int conv = 0;
+  const double t_loop = now_s();
   while (1) {
     orc_apply(nr, nt, np, bands, wrap, p, q);
     double sigma = dot(N, p, q);
@@ -508,8 +519,8 @@ int orc_solve(int nr, int nt, int np, const double *rf, const double *tf,
     for (int64_t m = 0; m < N; m++) p[m] = z[m] + beta * p[m];
     rho = rho_new;
   }
+  g_loop_seconds = now_s() - t_loop;
   if (status == 0 && !conv) status = 1;
-  if (status == 2 && !conv) status = 2;
   if (bc == ORC_CLOSED_WALL) {
     double sv = 0.0, svx = 0.0;
     for (int kk = 0; kk < np; kk++)
@@ -678,9 +689,10 @@ int orc_volumes(int nr, int nt, int np, const double *rf, const double *tf,
  * maxit = iters and rtol = 0), exposed separately only to report time. */
 int orc_solve_fixed(int nr, int nt, int np, const double *rf, const double *tf,
                     const double *pf, int bc, int pc, int pc2_blocks, const double *br0,
-                    int64_t iters, double *x, double *rel_res) {
+                    int64_t iters, double *x, double *rel_res, double *loop_seconds) {
   int64_t it = 0;
   int st = orc_solve(nr, nt, np, rf, tf, pf, bc, pc, pc2_blocks, br0, 0.0, iters, x, &it,
                      rel_res, NULL, NULL);
+  if (loop_seconds) *loop_seconds = g_loop_seconds;
   return st;
 }

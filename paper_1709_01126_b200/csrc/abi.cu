@@ -1,0 +1,968 @@
+// abi.cu -- the C ABI of libpot3d.so (include/pot3d.h): setup, solve loop
+// orchestration (CUDA graphs, device-resident scalars, NCCL halo/all-gather),
+// field derivation and diagnostics.  All arithmetic of the method runs in the
+// kernels of kernels.cu / pc2.cu; this file only schedules them.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pot3d.h"
+#include "pot3d_internal.cuh"
+
+
+using namespace pot3d;
+
+struct pot3d_ctx {
+  // problem
+  int nr = 0, nt = 0, np = 0, bc = 0, pc_req = 1, pc = 1;
+  int rank = 0, nranks = 1, pc2_blocks = 1, unroll = 8;
+  int device = 0;
+  double r0 = 1.0;
+  Grid G{};
+  std::vector<double> rf, tf, pf;
+  // runtime
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void *(*ualloc)(size_t, void *) = nullptr;
+  void (*ufree)(void *, void *) = nullptr;
+  void *actx = nullptr;
+  std::vector<void *> allocs;
+  size_t dev_bytes = 0;
+  ncclComm_t comm = nullptr;
+  // device data
+  double *d_rf = nullptr, *d_tf = nullptr, *d_pf = nullptr;
+  double *m_arp, *m_arm, *m_dr, *m_ss, *m_g, *m_atp, *m_atm, *m_q, *m_dp, *m_app, *m_apm;
+  double *m_rc, *m_drh, *m_tc, *m_dth, *m_st, *m_dph, *m_vr;
+  Metrics M{};
+  double *x = nullptr, *r = nullptr, *P[2] = {nullptr, nullptr}, *z = nullptr;
+  double *bshell = nullptr, *br_dev = nullptr, *mean2 = nullptr, *staging = nullptr;
+  size_t staging_bytes = 0;
+  Scalars *S = nullptr;
+  Scalars *hS = nullptr;  // pinned mirror
+  double *partials = nullptr;
+  size_t partials_len = 0;
+  double *hist = nullptr;
+  int64_t hist_len = 0;
+  double *local_sum = nullptr, *gathered = nullptr;
+  double *poles = nullptr;
+  Pc2 *pc2 = nullptr;
+  // graphs
+  cudaGraphExec_t gexec = nullptr;
+  int graph_unroll = 0;
+  // launch accounting (pot3d_info_t.kernel_launches)
+  int64_t n_launch = 0;     // kernels launched (graph launches count their kernel nodes)
+  int64_t n_enq = 0;        // kernels enqueued by enqueue_iteration (graph capture)
+  int64_t graph_nodes = 0;  // kernel nodes of the instantiated graph
+  // state
+  bool solved = false;
+  int64_t last_iters = 0;
+  std::string err;
+};
+
+namespace {
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+      return POT3D_ERR_CUDA;                                                          \
+    }                                                                                 \
+  } while (0)
+#define NK(call)                                                                      \
+  do {                                                                                \
+    ncclResult_t n_ = (call);                                                         \
+    if (n_ != ncclSuccess) {                                                          \
+      ctx->err = std::string(#call) + ": " + ncclGetErrorString(n_);                  \
+      return POT3D_ERR_NCCL;                                                          \
+    }                                                                                 \
+  } while (0)
+#define TRY(expr)               \
+  do {                          \
+    int rc_ = (expr);           \
+    if (rc_ < 0) return rc_;    \
+  } while (0)
+
+void *dalloc_raw(pot3d_ctx *ctx, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void *p = nullptr;
+  if (ctx->ualloc) {
+    p = ctx->ualloc(bytes, ctx->actx);
+  } else {
+    if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
+  }
+  if (p) {
+    ctx->allocs.push_back(p);
+    ctx->dev_bytes += bytes;
+  }
+  return p;
+}
+
+template <typename T>
+int dalloc(pot3d_ctx *ctx, T **out, size_t count) {
+  *out = static_cast<T *>(dalloc_raw(ctx, sizeof(T) * count));
+  if (!*out) {
+    ctx->err = "device allocation of " + std::to_string(sizeof(T) * count) + " bytes failed";
+    return POT3D_ERR_OOM;
+  }
+  return 0;
+}
+
+void dfree_all(pot3d_ctx *ctx) {
+  for (void *p : ctx->allocs) {
+    if (ctx->ufree)
+      ctx->ufree(p, ctx->actx);
+    else
+      cudaFree(p);
+  }
+  ctx->allocs.clear();
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int ensure_staging(pot3d_ctx *ctx, size_t bytes) {
+  if (ctx->staging_bytes >= bytes) return 0;
+  double *p = nullptr;
+  TRY(dalloc(ctx, &p, (bytes + 7) / 8));
+  ctx->staging = p;
+  ctx->staging_bytes = bytes;
+  return 0;
+}
+
+// slab partition: B = nranks * pc2_blocks blocks (leading-remainder rule)
+void block_bounds(int nr, int B, int b, int &i0, int &i1) {
+  int base = nr / B, rem = nr % B;
+  i0 = b * base + (b < rem ? b : rem);
+  i1 = i0 + base + (b < rem ? 1 : 0);
+}
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+// user layout (r fastest, ni shells) <-> device cells (phi fastest)
+int to_device_cells(pot3d_ctx *ctx, const double *user, double *dev_cells_first_shell, int ni,
+                    long long stride_i) {
+  const size_t n = (size_t)ni * ctx->nt * ctx->np;
+  const double *src = user;
+  if (!is_device_ptr(user)) {
+    TRY(ensure_staging(ctx, n * sizeof(double)));
+    CK(cudaMemcpyAsync(ctx->staging, user, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    src = ctx->staging;
+  }
+  dim3 blk(32, 8), grd((ctx->np + 31) / 32, (ni + 31) / 32, ctx->nt);
+  k_transpose<<<grd, blk, 0, ctx->stream>>>(ni, ctx->nt, ctx->np, stride_i, ctx->G.PK, src,
+                                            dev_cells_first_shell, 1);
+  CK(cudaGetLastError());
+  ctx->n_launch++;
+  return 0;
+}
+
+int from_device_cells(pot3d_ctx *ctx, const double *dev_first, double *user, int ni, int nj,
+                      long long stride_i) {
+  const size_t n = (size_t)ni * nj * ctx->np;
+  const bool dev = is_device_ptr(user);
+  double *dst = user;
+  if (!dev) {
+    TRY(ensure_staging(ctx, n * sizeof(double)));
+    dst = ctx->staging;
+  }
+  dim3 blk(32, 8), grd((ctx->np + 31) / 32, (ni + 31) / 32, nj);
+  k_transpose<<<grd, blk, 0, ctx->stream>>>(ni, nj, ctx->np, stride_i, ctx->G.PK, dev_first, dst, 0);
+  CK(cudaGetLastError());
+  ctx->n_launch++;
+  if (!dev) {
+    CK(cudaMemcpyAsync(user, dst, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return 0;
+}
+
+// all-gather `count` doubles per rank from local_sum into gathered (no-op copy at 1 rank)
+int gather_sums(pot3d_ctx *ctx, int count) {
+  if (ctx->nranks == 1) {
+    CK(cudaMemcpyAsync(ctx->gathered, ctx->local_sum, sizeof(double) * 2, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    return 0;
+  }
+  (void)count;
+  NK(ncclAllGather(ctx->local_sum, ctx->gathered, 2, ncclDouble, ctx->comm, ctx->stream));
+  return 0;
+}
+
+// halo exchange of one shell per r face of a cell array with ghost shells
+int halo_exchange(pot3d_ctx *ctx, double *a) {
+  if (ctx->nranks == 1) return 0;
+  const Grid &G = ctx->G;
+  const size_t cnt = (size_t)G.plane;
+  NK(ncclGroupStart());
+  if (ctx->rank > 0) {
+    NK(ncclSend(a + cidx(G, 0, 0, 0), cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+    NK(ncclRecv(a + cidx(G, -1, 0, 0), cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+  }
+  if (ctx->rank < ctx->nranks - 1) {
+    NK(ncclSend(a + cidx(G, G.nr_loc - 1, 0, 0), cnt, ncclDouble, ctx->rank + 1, ctx->comm,
+                ctx->stream));
+    NK(ncclRecv(a + cidx(G, G.nr_loc, 0, 0), cnt, ncclDouble, ctx->rank + 1, ctx->comm,
+                ctx->stream));
+  }
+  NK(ncclGroupEnd());
+  return 0;
+}
+
+int pass_blocks(pot3d_ctx *ctx) { return ctx->G.ntj * ctx->G.ntk * ctx->G.nchunks; }
+
+PassArgs make_args(pot3d_ctx *ctx, int parity) {
+  PassArgs a{};
+  a.G = ctx->G;
+  a.M = ctx->M;
+  a.S = ctx->S;
+  a.r = ctx->r;
+  a.r_out = ctx->r;
+  a.z = ctx->z;
+  a.p_old = ctx->P[parity];
+  a.p_new = ctx->P[parity ^ 1];
+  a.x = ctx->x;
+  a.partials = ctx->partials;
+  a.hist = ctx->hist;
+  a.finalize = ctx->nranks == 1 ? 1 : 0;
+  a.local_sum = ctx->local_sum;
+  return a;
+}
+
+// One PCG iteration (a3-a10) enqueued on ctx->stream; parity = iteration & 1.
+//   [multi-rank] edge shells of p_new -> NCCL halo
+//   pass A  (p_new, q = A p_new, sigma partial, lazy x update) -> alpha
+//   pass B  (r -= alpha q, PC1: rho', ||r||^2)                 -> convergence, beta
+//   [PC2]   forward + backward D-ILU sweeps (z, rho')           -> beta
+int enqueue_iteration(pot3d_ctx *ctx, int parity) {
+  const Grid &G = ctx->G;
+  PassArgs a = make_args(ctx, parity);
+  dim3 grd(G.ntj * G.ntk, G.nchunks);
+  const bool pc2 = ctx->pc == 2;
+  const bool multi = ctx->nranks > 1;
+  if (multi) {
+    k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
+                                                ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0);
+    CK(cudaGetLastError());
+    ctx->n_enq++;
+    TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
+  }
+  if (pc2)
+    k_pass_a_pc2<<<grd, NTHREADS, 0, ctx->stream>>>(a);
+  else
+    k_pass_a_pc1<<<grd, NTHREADS, 0, ctx->stream>>>(a);
+  CK(cudaGetLastError());
+    ctx->n_enq++;
+  if (multi) {
+    TRY(gather_sums(ctx, 1));
+    k_finalize_alpha<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks);
+    CK(cudaGetLastError());
+    ctx->n_enq++;
+  }
+  if (pc2)
+    k_pass_b_pc2<<<grd, NTHREADS, 0, ctx->stream>>>(a);
+  else
+    k_pass_b_pc1<<<grd, NTHREADS, 0, ctx->stream>>>(a);
+  CK(cudaGetLastError());
+    ctx->n_enq++;
+  if (multi) {
+    TRY(gather_sums(ctx, 2));
+    if (pc2)
+      k_finalize_rr<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks, ctx->hist);
+    else
+      k_finalize_beta<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks, ctx->hist);
+    CK(cudaGetLastError());
+    ctx->n_enq++;
+  }
+  if (pc2) {
+    int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, multi ? 0 : 1,
+                       ctx->local_sum, ctx->stream, true);
+    TRY(nk);
+    CK(cudaGetLastError());
+    ctx->n_enq += nk;
+    if (multi) {
+      TRY(gather_sums(ctx, 1));
+      k_finalize_rho<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks);
+      CK(cudaGetLastError());
+    ctx->n_enq++;
+    }
+  }
+  return 0;
+}
+
+int build_graph(pot3d_ctx *ctx) {
+  if (ctx->gexec) {
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  cudaGraph_t g;
+  ctx->n_enq = 0;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = 0;
+  for (int u = 0; u < ctx->unroll && rc == 0; u++) rc = enqueue_iteration(ctx, u & 1);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (rc) return rc;
+  CK(e);
+  CK(cudaGraphInstantiate(&ctx->gexec, g, 0));
+  cudaGraphDestroy(g);
+  ctx->graph_unroll = ctx->unroll;
+  ctx->graph_nodes = ctx->n_enq;
+  return 0;
+}
+
+int choose_chunks(pot3d_ctx *ctx) {
+  Grid &G = ctx->G;
+  const char *env = getenv("POT3D_CHUNKS");
+  if (env && atoi(env) > 0) {
+    G.nchunks = std::min(atoi(env), G.nr_loc);
+    return 0;
+  }
+  int occ = 0, sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_b_pc1, NTHREADS, 0));
+  int occa = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occa, k_pass_a_pc1, NTHREADS, 0));
+  occ = std::max(1, std::min(occ, occa));
+  const double slots = (double)sms * occ;
+  const long long tiles = (long long)G.ntj * G.ntk;
+  double best = -1;
+  int bestc = 1;
+  for (int c = 1; c <= std::min(G.nr_loc, 32); c++) {
+    double blocks = (double)tiles * c;
+    double waves = blocks / slots;
+    double eff_w = waves / std::ceil(waves);
+    double L = (double)G.nr_loc / c;
+    double eff_h = L / (L + 2.0);
+    double e = eff_w * eff_h;
+    if (e > best + 1e-9) {
+      best = e;
+      bestc = c;
+    }
+  }
+  G.nchunks = bestc;
+  return 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+static thread_local std::string g_setup_error = "no error";
+
+const char *pot3d_last_error(const pot3d_ctx *ctx) {
+  return ctx ? ctx->err.c_str() : g_setup_error.c_str();
+}
+
+int pot3d_nccl_unique_id(void *out128) {
+  if (!out128) return POT3D_ERR_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return POT3D_ERR_NCCL;
+  memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
+  if (!ctx || !info) return POT3D_ERR_INVALID;
+  info->i0 = ctx->G.i0;
+  info->i1 = ctx->G.i0 + ctx->G.nr_loc;
+  info->nr_loc = ctx->G.nr_loc;
+  info->br_shells = ctx->G.nr_loc + (ctx->rank == ctx->nranks - 1 ? 1 : 0);
+  info->pc = ctx->pc;
+  info->pc2_blocks_total = ctx->pc2_blocks * ctx->nranks;
+  int64_t k = 2;
+  if (ctx->nranks > 1) k += 3;
+  if (ctx->pc == 2 && ctx->pc2) k += pc2_kernels_per_apply(ctx->pc2);
+  info->graph_kernels_per_iter = k;
+  // algorithmic bytes: PC1 64 B/cell, PC2 pass A 40 + pass B 24 + sweeps
+  const int64_t cells = (int64_t)ctx->G.nr_loc * ctx->nt * ctx->np;
+  info->bytes_per_iter = (ctx->pc == 2 ? 120 : 64) * cells;
+  info->device_bytes = (int64_t)ctx->dev_bytes;
+  info->kernel_launches = ctx->n_launch;
+  return 0;
+}
+
+int pot3d_set_br0(pot3d_ctx *ctx, const double *br0) {
+  if (!ctx || !br0) return POT3D_ERR_INVALID;
+  const Grid &G = ctx->G;
+  CK(cudaSetDevice(ctx->device));
+  // (np, nt) theta-fastest user map -> device [j][k]: the transpose with ni = nt, nj = 1
+  const size_t n = (size_t)ctx->nt * ctx->np;
+  const double *src = br0;
+  if (!is_device_ptr(br0)) {
+    TRY(ensure_staging(ctx, n * sizeof(double)));
+    CK(cudaMemcpyAsync(ctx->staging, br0, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    src = ctx->staging;
+  }
+  {
+    dim3 blk(32, 8), grd((ctx->np + 31) / 32, (ctx->nt + 31) / 32, 1);
+    k_transpose<<<grd, blk, 0, ctx->stream>>>(ctx->nt, 1, ctx->np, G.PK, G.PK, src, ctx->br_dev, 1);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  if (ctx->bc == POT3D_CLOSED_WALL) {
+    k_br_mean<<<1, 1024, 0, ctx->stream>>>(G, ctx->M, ctx->br_dev, ctx->mean2);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  if (G.i0 == 0) {
+    unsigned nb = (unsigned)((n + 255) / 256);
+    k_rhs<<<nb, 256, 0, ctx->stream>>>(G, ctx->M, ctx->r0, ctx->br_dev,
+                                       ctx->bc == POT3D_CLOSED_WALL ? ctx->mean2 : nullptr,
+                                       ctx->bshell);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->solved = false;
+  return 0;
+}
+
+int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int32_t pc,
+                const pot3d_runtime *rt, pot3d_ctx **out) {
+  if (!out) return POT3D_ERR_INVALID;
+  *out = nullptr;
+  pot3d_ctx *ctx = new pot3d_ctx();
+  auto fail = [&](int rc) {
+    *out = nullptr;
+    g_setup_error = ctx->err;  // reachable through pot3d_last_error(NULL)
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    dfree_all(ctx);
+    if (ctx->hS) cudaFreeHost(ctx->hS);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return rc;
+  };
+  if (!grid || !br0 || !grid->r_faces || !grid->t_faces || !grid->p_faces) {
+    ctx->err = "null argument";
+    return fail(POT3D_ERR_INVALID);
+  }
+  const int nr = grid->nr, nt = grid->nt, np = grid->np;
+  if (nr < 2 || nt < 2 || np < 2) {
+    ctx->err = "cell counts must be >= 2 (S:45)";
+    return fail(POT3D_ERR_INVALID);
+  }
+  if (outer_bc != POT3D_SOURCE_SURFACE && outer_bc != POT3D_CLOSED_WALL) {
+    ctx->err = "outer_bc must be SOURCE_SURFACE or CLOSED_WALL";
+    return fail(POT3D_ERR_INVALID);
+  }
+  if (pc != POT3D_PC1 && pc != POT3D_PC2) {
+    ctx->err = "pc must be 1 or 2";
+    return fail(POT3D_ERR_INVALID);
+  }
+  ctx->rf.assign(grid->r_faces, grid->r_faces + nr + 1);
+  ctx->tf.assign(grid->t_faces, grid->t_faces + nt + 1);
+  ctx->pf.assign(grid->p_faces, grid->p_faces + np + 1);
+  for (int i = 0; i < nr; i++)
+    if (!(ctx->rf[i + 1] > ctx->rf[i])) { ctx->err = "r_faces not increasing"; return fail(POT3D_ERR_INVALID); }
+  for (int j = 0; j < nt; j++)
+    if (!(ctx->tf[j + 1] > ctx->tf[j])) { ctx->err = "t_faces not increasing"; return fail(POT3D_ERR_INVALID); }
+  for (int k = 0; k < np; k++)
+    if (!(ctx->pf[k + 1] > ctx->pf[k])) { ctx->err = "p_faces not increasing"; return fail(POT3D_ERR_INVALID); }
+  if (!(ctx->rf[0] > 0.0)) { ctx->err = "r0 must be > 0"; return fail(POT3D_ERR_INVALID); }
+  if (std::fabs(ctx->tf[0]) > 1e-12 || std::fabs(ctx->tf[nt] - M_PI) > 1e-12) {
+    ctx->err = "t_faces must span [0, pi]";
+    return fail(POT3D_ERR_INVALID);
+  }
+  if (std::fabs(ctx->pf[np] - ctx->pf[0] - 2 * M_PI) > 1e-12) {
+    ctx->err = "p_faces must span 2 pi";
+    return fail(POT3D_ERR_INVALID);
+  }
+  ctx->nr = nr; ctx->nt = nt; ctx->np = np;
+  ctx->bc = outer_bc;
+  ctx->pc_req = ctx->pc = pc;
+  ctx->r0 = ctx->rf[0];
+  pot3d_runtime R{};
+  R.nranks = 1;
+  R.device = -1;
+  if (rt) R = *rt;
+  ctx->rank = R.rank;
+  ctx->nranks = R.nranks < 1 ? 1 : R.nranks;
+  ctx->pc2_blocks = R.pc2_blocks < 1 ? 1 : R.pc2_blocks;
+  ctx->unroll = R.unroll > 0 ? (R.unroll + 1) / 2 * 2 : 8;
+  ctx->ualloc = R.alloc;
+  ctx->ufree = R.free;
+  ctx->actx = R.alloc_ctx;
+  if (ctx->rank < 0 || ctx->rank >= ctx->nranks) { ctx->err = "bad rank"; return fail(POT3D_ERR_INVALID); }
+  if (ctx->nranks > 1 && !R.nccl_unique_id) { ctx->err = "nccl_unique_id required for nranks > 1"; return fail(POT3D_ERR_INVALID); }
+  const int B = ctx->nranks * ctx->pc2_blocks;
+  if (nr < 2 * ctx->nranks || (pc == POT3D_PC2 && nr < B)) {
+    ctx->err = "too many ranks/blocks for nr";
+    return fail(POT3D_ERR_INVALID);
+  }
+  if (R.device >= 0) {
+    ctx->device = R.device;
+  } else {
+    cudaGetDevice(&ctx->device);
+  }
+  CK(cudaSetDevice(ctx->device));
+  if (R.cuda_stream) {
+    ctx->stream = (cudaStream_t)R.cuda_stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+
+  // r-slab of this rank: union of its pc2_blocks consecutive blocks
+  std::vector<int> bi0(B), bi1(B);
+  for (int b = 0; b < B; b++) block_bounds(nr, B, b, bi0[b], bi1[b]);
+  if (pc == POT3D_PC1) {
+    int a, b;
+    block_bounds(nr, ctx->nranks, ctx->rank, a, b);
+    ctx->G.i0 = a;
+    ctx->G.nr_loc = b - a;
+  } else {
+    ctx->G.i0 = bi0[ctx->rank * ctx->pc2_blocks];
+    ctx->G.nr_loc = bi1[(ctx->rank + 1) * ctx->pc2_blocks - 1] - ctx->G.i0;
+  }
+  Grid &G = ctx->G;
+  G.nr = nr; G.nt = nt; G.np = np;
+  G.PK = round_up(np, 16);
+  G.plane = (long long)nt * G.PK;
+  G.ntj = (nt + TJ - 1) / TJ;
+  G.ntk = (np + TK - 1) / TK;
+  { int rc = choose_chunks(ctx); if (rc) return fail(rc); }
+
+  // metrics (a1)
+  int rc = 0;
+#define DA(ptr, n) if ((rc = dalloc(ctx, &(ptr), (n)))) return fail(rc)
+  DA(ctx->d_rf, nr + 1); DA(ctx->d_tf, nt + 1); DA(ctx->d_pf, np + 1);
+  DA(ctx->m_arp, nr); DA(ctx->m_arm, nr); DA(ctx->m_dr, nr); DA(ctx->m_ss, nr);
+  DA(ctx->m_rc, nr); DA(ctx->m_drh, nr); DA(ctx->m_vr, nr);
+  DA(ctx->m_g, nt); DA(ctx->m_atp, nt); DA(ctx->m_atm, nt); DA(ctx->m_q, nt);
+  DA(ctx->m_tc, nt); DA(ctx->m_dth, nt); DA(ctx->m_st, nt);
+  DA(ctx->m_dp, np); DA(ctx->m_app, np); DA(ctx->m_apm, np); DA(ctx->m_dph, np);
+  if (cudaMemcpyAsync(ctx->d_rf, ctx->rf.data(), sizeof(double) * (nr + 1), cudaMemcpyHostToDevice, ctx->stream) ||
+      cudaMemcpyAsync(ctx->d_tf, ctx->tf.data(), sizeof(double) * (nt + 1), cudaMemcpyHostToDevice, ctx->stream) ||
+      cudaMemcpyAsync(ctx->d_pf, ctx->pf.data(), sizeof(double) * (np + 1), cudaMemcpyHostToDevice, ctx->stream)) {
+    ctx->err = "face upload failed";
+    return fail(POT3D_ERR_CUDA);
+  }
+  {
+    int n = std::max(nr, std::max(nt, np));
+    k_metrics<<<(n + 127) / 128, 128, 0, ctx->stream>>>(
+        nr, nt, np, outer_bc, ctx->d_rf, ctx->d_tf, ctx->d_pf, ctx->m_arp, ctx->m_arm, ctx->m_dr,
+        ctx->m_ss, ctx->m_g, ctx->m_atp, ctx->m_atm, ctx->m_q, ctx->m_dp, ctx->m_app, ctx->m_apm,
+        ctx->m_rc, ctx->m_drh, ctx->m_tc, ctx->m_dth, ctx->m_st, ctx->m_dph, ctx->m_vr);
+    if (cudaGetLastError() != cudaSuccess) { ctx->err = "k_metrics launch failed"; return fail(POT3D_ERR_CUDA); }
+  }
+  ctx->M = Metrics{ctx->m_arp, ctx->m_arm, ctx->m_dr, ctx->m_ss, ctx->m_g, ctx->m_atp,
+                   ctx->m_atm, ctx->m_q, ctx->m_dp, ctx->m_app, ctx->m_apm};
+
+  // vectors with ghost shells
+  const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
+  DA(ctx->x, cells); DA(ctx->r, cells); DA(ctx->P[0], cells); DA(ctx->P[1], cells);
+  if (pc == POT3D_PC2) DA(ctx->z, cells);
+  DA(ctx->bshell, G.plane); DA(ctx->br_dev, G.plane); DA(ctx->mean2, 2);
+  DA(ctx->S, 1);
+  ctx->partials_len = 4 * (size_t)std::max<long long>(pass_blocks(ctx), 4096);
+  DA(ctx->partials, ctx->partials_len);
+  DA(ctx->local_sum, 2);
+  DA(ctx->gathered, 2 * (size_t)ctx->nranks + 2);
+  DA(ctx->poles, 2 * (size_t)G.nr_loc);
+#undef DA
+  for (void *p : {(void *)ctx->x, (void *)ctx->r, (void *)ctx->P[0], (void *)ctx->P[1]})
+    if (cudaMemsetAsync(p, 0, cells * sizeof(double), ctx->stream)) { ctx->err = "memset"; return fail(POT3D_ERR_CUDA); }
+  if (ctx->z) cudaMemsetAsync(ctx->z, 0, cells * sizeof(double), ctx->stream);
+  cudaMemsetAsync(ctx->bshell, 0, G.plane * sizeof(double), ctx->stream);
+  cudaMemsetAsync(ctx->br_dev, 0, G.plane * sizeof(double), ctx->stream);
+  cudaMemsetAsync(ctx->S, 0, sizeof(Scalars), ctx->stream);
+  if (cudaMallocHost(&ctx->hS, sizeof(Scalars)) != cudaSuccess) { ctx->err = "pinned alloc"; return fail(POT3D_ERR_CUDA); }
+
+  if (ctx->nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, R.nccl_unique_id, sizeof(id));
+    ncclResult_t nr_ = ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank);
+    if (nr_ != ncclSuccess) {
+      ctx->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(nr_);
+      return fail(POT3D_ERR_NCCL);
+    }
+  }
+
+  if (pc == POT3D_PC2) {
+    std::vector<int> lb(ctx->pc2_blocks + 1);
+    for (int b = 0; b < ctx->pc2_blocks; b++) lb[b] = bi0[ctx->rank * ctx->pc2_blocks + b] - G.i0;
+    lb[ctx->pc2_blocks] = G.nr_loc;
+    rc = pc2_create(&ctx->pc2, G, ctx->pc2_blocks, lb.data(), ctx->ualloc, ctx->actx);
+    if (rc) { ctx->err = "pc2_create failed"; return fail(POT3D_ERR_OOM); }
+    double minpiv = 0;
+    rc = pc2_factor(ctx->pc2, ctx->M, ctx->stream, &minpiv);
+    if (rc) { ctx->err = "pc2_factor failed"; return fail(POT3D_ERR_CUDA); }
+    // breakdown on any rank -> every rank falls back
+    int bad = (minpiv < 1e-300) ? 1 : 0;
+    if (ctx->nranks > 1) {
+      int *d = nullptr;
+      if ((rc = dalloc(ctx, &d, 2 * ctx->nranks))) return fail(rc);
+      cudaMemcpyAsync(d, &bad, sizeof(int), cudaMemcpyHostToDevice, ctx->stream);
+      ncclAllGather(d, d + ctx->nranks, 1, ncclInt32, ctx->comm, ctx->stream);
+      std::vector<int> h(ctx->nranks);
+      cudaMemcpyAsync(h.data(), d + ctx->nranks, sizeof(int) * ctx->nranks, cudaMemcpyDeviceToHost, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+      for (int v : h) bad |= v;
+    }
+    if (bad) ctx->pc = POT3D_PC1;
+  }
+  {
+    int rc2 = pot3d_set_br0(ctx, br0);
+    if (rc2) return fail(rc2);
+  }
+  {
+    int rc2 = build_graph(ctx);
+    if (rc2) return fail(rc2);
+  }
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    ctx->err = std::string("setup: ") + cudaGetErrorString(cudaGetLastError());
+    return fail(POT3D_ERR_CUDA);
+  }
+  *out = ctx;
+  return 0;
+}
+
+int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t *iters,
+                double *rel_residual, double *true_rel_residual) {
+  if (!ctx) return POT3D_ERR_INVALID;
+  if (!(rtol >= 0.0) || maxit < 1) {
+    ctx->err = "rtol must be >= 0 and maxit >= 1";
+    return POT3D_ERR_INVALID;
+  }
+  CK(cudaSetDevice(ctx->device));
+  const Grid &G = ctx->G;
+  cudaStream_t s = ctx->stream;
+  const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
+  ctx->solved = false;
+  // residual history buffer (maxit+1 doubles, capped)
+  const int64_t hlen = std::min<int64_t>(maxit + 1, (int64_t)1 << 24);
+  if (hlen > ctx->hist_len) {
+    double *h = nullptr;
+    TRY(dalloc(ctx, &h, (size_t)hlen));
+    ctx->hist = h;
+    ctx->hist_len = hlen;
+    TRY(build_graph(ctx));  // graph captured the old history pointer
+  }
+  // x0 = 0, r = b, p = 0 (A9)
+  CK(cudaMemsetAsync(ctx->x, 0, cells * sizeof(double), s));
+  CK(cudaMemsetAsync(ctx->r, 0, cells * sizeof(double), s));
+  CK(cudaMemsetAsync(ctx->P[0], 0, cells * sizeof(double), s));
+  CK(cudaMemsetAsync(ctx->P[1], 0, cells * sizeof(double), s));
+  if (G.i0 == 0)
+    CK(cudaMemcpyAsync(ctx->r + cidx(G, 0, 0, 0), ctx->bshell, G.plane * sizeof(double),
+                       cudaMemcpyDeviceToDevice, s));
+  Scalars h0{};
+  h0.rtol = rtol;
+  h0.maxit = (long long)std::min<int64_t>(maxit, hlen - 1);
+  CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+  // z0 = M^-1 b, rho0 = b.z0, ||b|| (a10 init)
+  const int nbi = 148 * 4;
+  if (ctx->pc == 2) {
+    int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
+                       s, false);
+    TRY(nk);
+    CK(cudaGetLastError());
+    ctx->n_launch += nk;
+  }
+  k_init_dots<<<nbi, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, ctx->partials, ctx->nranks == 1,
+                                  ctx->local_sum, ctx->pc == 2, ctx->z);
+  CK(cudaGetLastError());
+    ctx->n_launch++;
+  if (ctx->nranks > 1) {
+    TRY(gather_sums(ctx, 2));
+    k_init_finalize<<<1, 1, 0, s>>>(ctx->S, ctx->gathered, ctx->nranks);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  if (ctx->hist) {
+    // hist[0] = 1 (||r_0|| = ||b||)
+    double one = 1.0;
+    CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  // device-driven loop: graphs of `unroll` predicated iterations; the stop flag
+  // of graph g is read back while graph g+1 is already queued
+  CK(cudaMemcpyAsync(ctx->hS, ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int64_t launched = 0;
+  if (!ctx->hS->stop) {
+    cudaEvent_t ev[2];
+    Scalars *hs2 = nullptr;
+    CK(cudaMallocHost(&hs2, 2 * sizeof(Scalars)));
+    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    CK(cudaGraphLaunch(ctx->gexec, s));
+    ctx->n_launch += ctx->graph_nodes;
+    CK(cudaMemcpyAsync(&hs2[0], ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ev[0], s));
+    launched++;
+    int cur = 0;
+    while (true) {
+      const bool more = (launched * ctx->graph_unroll) < maxit + ctx->graph_unroll;
+      if (more) {
+        CK(cudaGraphLaunch(ctx->gexec, s));
+        ctx->n_launch += ctx->graph_nodes;
+        CK(cudaMemcpyAsync(&hs2[cur ^ 1], ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ev[cur ^ 1], s));
+        launched++;
+      }
+      CK(cudaEventSynchronize(ev[cur]));
+      if (hs2[cur].stop || !more) break;
+      cur ^= 1;
+    }
+    CK(cudaStreamSynchronize(s));
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    cudaFreeHost(hs2);
+  }
+  CK(cudaMemcpyAsync(ctx->hS, ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const Scalars hs = *ctx->hS;
+  if (hs.status == -4) {
+    ctx->err = "p.Ap <= 0: operator or preconditioner not positive definite (S:341)";
+    return POT3D_ERR_INDEFINITE;
+  }
+  if (!hs.stop) {
+    ctx->err = "loop ended without the stop flag";
+    return POT3D_ERR_STATE;
+  }
+  // finish (a11): x += alpha_last p_last
+  if (hs.iter > 0) {
+    k_axpy_cells<<<148 * 8, 256, 0, s>>>(G, ctx->x, ctx->P[hs.iter & 1], ctx->S);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  // closed wall: zero volume-weighted-mean gauge (A8)
+  if (ctx->bc == POT3D_CLOSED_WALL && hs.bnorm > 0) {
+    k_gauge_sums<<<nbi, 256, 0, s>>>(G, ctx->M, ctx->m_vr, ctx->x, ctx->S, ctx->partials,
+                                      ctx->local_sum);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+    TRY(gather_sums(ctx, 2));
+    k_gauge_shift<<<148 * 8, 256, 0, s>>>(G, ctx->x, ctx->gathered, ctx->nranks);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  TRY(halo_exchange(ctx, ctx->x));
+  if (true_rel_residual) {
+    k_apply<<<nbi, 256, 0, s>>>(G, ctx->M, ctx->x, nullptr, ctx->bshell, G.i0 == 0 ? 0 : -1000,
+                                ctx->S, ctx->partials, ctx->local_sum);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+    TRY(gather_sums(ctx, 1));
+    std::vector<double> g(2 * ctx->nranks);
+    CK(cudaMemcpyAsync(g.data(), ctx->gathered, sizeof(double) * 2 * ctx->nranks,
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double t = 0.0;
+    for (int rr = 0; rr < ctx->nranks; rr++) t += g[2 * rr];
+    *true_rel_residual = hs.bnorm > 0 ? std::sqrt(t) / hs.bnorm : 0.0;
+  }
+  if (phi) TRY(from_device_cells(ctx, ctx->x + G.plane, phi, G.nr_loc, ctx->nt, G.plane));
+  CK(cudaStreamSynchronize(s));
+  if (iters) *iters = hs.iter;
+  if (rel_residual) *rel_residual = hs.bnorm > 0 ? std::sqrt(hs.rr) / hs.bnorm : 0.0;
+  ctx->last_iters = hs.iter;
+  ctx->solved = true;
+  if (ctx->pc != ctx->pc_req) return POT3D_PC2_FELL_BACK;
+  return hs.status == 1 ? POT3D_NOT_CONVERGED : POT3D_OK;
+}
+
+int64_t pot3d_history(pot3d_ctx *ctx, double *hist, int64_t len) {
+  if (!ctx || !hist) return POT3D_ERR_INVALID;
+  if (!ctx->solved || !ctx->hist) return POT3D_ERR_STATE;
+  int64_t n = std::min<int64_t>(len, ctx->last_iters + 1);
+  if (cudaMemcpy(hist, ctx->hist, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    ctx->err = "history copy failed";
+    return POT3D_ERR_CUDA;
+  }
+  return n;
+}
+
+int pot3d_field(pot3d_ctx *ctx, double *br, double *bt, double *bp) {
+  if (!ctx) return POT3D_ERR_INVALID;
+  if (!ctx->solved) {
+    ctx->err = "pot3d_field before a successful pot3d_solve";
+    return POT3D_ERR_STATE;
+  }
+  CK(cudaSetDevice(ctx->device));
+  const Grid &G = ctx->G;
+  cudaStream_t s = ctx->stream;
+  // temporaries: reuse the Krylov buffers (x keeps the solution)
+  double *Br = ctx->P[0], *Bt = ctx->P[1], *Bp = ctx->r;
+  const int nbr = G.nr_loc + (ctx->rank == ctx->nranks - 1 ? 1 : 0);
+  const int ntf = ctx->nt + 1;
+  // Bt needs nr_loc * (nt+1) * PK <= (nr_loc+2) * nt * PK
+  if ((long long)G.nr_loc * ntf > (long long)(G.nr_loc + 2) * ctx->nt) {
+    ctx->err = "field buffer too small";
+    return POT3D_ERR_STATE;
+  }
+  k_pole_avg<<<dim3(G.nr_loc, 2), 256, 0, s>>>(G, ctx->x, ctx->m_dp, ctx->pf[ctx->np] - ctx->pf[0],
+                                                ctx->poles, ctx->poles + G.nr_loc);
+  CK(cudaGetLastError());
+    ctx->n_launch++;
+  FieldArgs F{};
+  F.G = G;
+  F.x = ctx->x;
+  F.br = ctx->br_dev;
+  F.mean2 = ctx->bc == POT3D_CLOSED_WALL ? ctx->mean2 : nullptr;
+  F.rc = ctx->m_rc; F.dr = ctx->m_dr; F.drh = ctx->m_drh; F.tc = ctx->m_tc; F.tf = ctx->d_tf;
+  F.dth = ctx->m_dth; F.st = ctx->m_st; F.dph = ctx->m_dph;
+  F.poleN = ctx->poles; F.poleS = ctx->poles + G.nr_loc;
+  F.bc = ctx->bc;
+  F.nbr = nbr;
+  F.Br = Br; F.Bt = Bt; F.Bp = Bp;
+  const long long nc = (long long)G.nr_loc * ctx->nt * ctx->np;
+  if (br) {
+    long long n = (long long)nbr * ctx->nt * ctx->np;
+    k_field_r<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(F);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+    TRY(from_device_cells(ctx, Br, br, nbr, ctx->nt, G.plane));
+  }
+  if (bt) {
+    long long n = (long long)G.nr_loc * ntf * ctx->np;
+    k_field_t<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(F);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+    TRY(from_device_cells(ctx, Bt, bt, G.nr_loc, ntf, (long long)ntf * G.PK));
+  }
+  if (bp) {
+    k_field_p<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(F);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+    TRY(from_device_cells(ctx, Bp, bp, G.nr_loc, ctx->nt, G.plane));
+  }
+  CK(cudaStreamSynchronize(s));
+  // the Krylov buffers were reused: a later field call needs a new solve's x only
+  return 0;
+}
+
+int pot3d_apply(pot3d_ctx *ctx, const double *x, double *y) {
+  if (!ctx || !x || !y) return POT3D_ERR_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  const Grid &G = ctx->G;
+  cudaStream_t s = ctx->stream;
+  const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
+  double *xin = ctx->P[0], *yout = ctx->P[1];
+  CK(cudaMemsetAsync(xin, 0, cells * sizeof(double), s));
+  TRY(to_device_cells(ctx, x, xin + G.plane, G.nr_loc, G.plane));
+  TRY(halo_exchange(ctx, xin));
+  k_apply<<<148 * 4, 256, 0, s>>>(G, ctx->M, xin, yout, nullptr, 0, ctx->S, nullptr, nullptr);
+  CK(cudaGetLastError());
+    ctx->n_launch++;
+  TRY(from_device_cells(ctx, yout + G.plane, y, G.nr_loc, ctx->nt, G.plane));
+  CK(cudaStreamSynchronize(s));
+  ctx->solved = false;
+  return 0;
+}
+
+int pot3d_precond(pot3d_ctx *ctx, const double *rin, double *zout) {
+  if (!ctx || !rin || !zout) return POT3D_ERR_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  const Grid &G = ctx->G;
+  cudaStream_t s = ctx->stream;
+  const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
+  double *rr = ctx->P[0], *zz = ctx->P[1];
+  CK(cudaMemsetAsync(rr, 0, cells * sizeof(double), s));
+  CK(cudaMemsetAsync(zz, 0, cells * sizeof(double), s));
+  TRY(to_device_cells(ctx, rin, rr + G.plane, G.nr_loc, G.plane));
+  if (ctx->pc == 2) {
+    int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, rr, zz, ctx->partials, 0, ctx->local_sum, s, false);
+    TRY(nk);
+    CK(cudaGetLastError());
+    ctx->n_launch += nk;
+  } else {
+    // PC1: the edge-plane kernel computes z = D^-1 r (beta = 0) over any planes
+    Scalars h0{};
+    CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+    k_edge_p<<<148 * 8, 256, 0, s>>>(G, ctx->M, ctx->S, rr, nullptr, zz, -1);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  TRY(from_device_cells(ctx, zz + G.plane, zout, G.nr_loc, ctx->nt, G.plane));
+  CK(cudaStreamSynchronize(s));
+  ctx->solved = false;
+  return 0;
+}
+
+int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_pass_b,
+                  double *ms_precond) {
+  if (!ctx || iters < 1) return POT3D_ERR_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const Grid &G = ctx->G;
+  // continue the recurrences of the current state without a stopping test
+  CK(cudaMemcpyAsync(ctx->hS, ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  Scalars h = *ctx->hS;
+  h.stop = 0;
+  h.status = 0;
+  h.rtol = 0.0;
+  h.maxit = h.iter + iters + 1;
+  if (!(h.rho != 0.0)) h.rho = 1.0;
+  if (!(h.bnorm > 0.0)) h.bnorm = 1.0;
+  *ctx->hS = h;
+  CK(cudaMemcpyAsync(ctx->S, ctx->hS, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+  cudaEvent_t ev[4];
+  for (auto &e : ev) CK(cudaEventCreate(&e));
+  double ta = 0, tb = 0, tp = 0;
+  const bool pc2 = ctx->pc == 2;
+  dim3 grd(G.ntj * G.ntk, G.nchunks);
+  for (int it = 0; it < iters; it++) {
+    PassArgs a = make_args(ctx, (int)((h.iter + it) & 1));
+    a.hist = nullptr;
+    a.finalize = 1;
+    CK(cudaEventRecord(ev[0], s));
+    if (pc2) k_pass_a_pc2<<<grd, NTHREADS, 0, s>>>(a); else k_pass_a_pc1<<<grd, NTHREADS, 0, s>>>(a);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev[1], s));
+    if (pc2) k_pass_b_pc2<<<grd, NTHREADS, 0, s>>>(a); else k_pass_b_pc1<<<grd, NTHREADS, 0, s>>>(a);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev[2], s));
+    ctx->n_launch += 2;
+    if (pc2) {
+      int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 1, ctx->local_sum,
+                         s, true);
+      TRY(nk);
+      ctx->n_launch += nk;
+    }
+    CK(cudaEventRecord(ev[3], s));
+    CK(cudaEventSynchronize(ev[3]));
+    float f;
+    CK(cudaEventElapsedTime(&f, ev[0], ev[1])); ta += f;
+    CK(cudaEventElapsedTime(&f, ev[1], ev[2])); tb += f;
+    CK(cudaEventElapsedTime(&f, ev[2], ev[3])); tp += f;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  if (ms_pass_a) *ms_pass_a = ta / iters;
+  if (ms_pass_b) *ms_pass_b = tb / iters;
+  if (ms_precond) *ms_precond = tp / iters;
+  ctx->solved = false;
+  return 0;
+}
+
+int pot3d_destroy(pot3d_ctx *ctx) {
+  if (!ctx) return 0;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->pc2) pc2_destroy(ctx->pc2, ctx->ufree, ctx->actx);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  dfree_all(ctx);
+  if (ctx->hS) cudaFreeHost(ctx->hS);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return 0;
+}
+
+}  // extern "C"

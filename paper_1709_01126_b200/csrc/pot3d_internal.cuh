@@ -1,0 +1,155 @@
+// pot3d_internal.cuh -- device data layout and kernel interfaces of libpot3d.
+//
+// Layout in HBM:
+//   cell arrays   [il + 1][j][k], il in [-1, nr_loc] (one ghost shell on each r
+//                 side), phi fastest with row pitch PK = round_up(np, 16)
+//                 doubles so that every row starts on a 128-byte line.
+//                 A theta-phi shell is contiguous: the r-slab halo is one
+//                 cudaMemcpy-able / NCCL-sendable block.
+//   1-D metrics   per axis, global indices (r) / plain (theta, phi), fp64.
+//
+// The operator (P:62-77 with the full metric A1, volume-scaled A3, A = -V lap A4)
+// is never stored: every coupling is a product of 1-D factors,
+//   A^r_{i+1/2,j,k} = arp[i] * g[j] * dp[k]      (arp[i] = rf[i+1]^2 / drh[i+1/2])
+//   A^t_{i,j+1/2,k} = dr[i] * atp[j] * dp[k]     (atp[j] = sin tf[j+1] / dth[j+1/2])
+//   A^p_{i,j,k+1/2} = dr[i] * q[j] * app[k]      (q[j] = dt[j]/sin tc[j], app[k] = 1/dph[k+1/2])
+//   S_{i,j,k}       = ss[i] * g[j] * dp[k]       (source surface, last shell: 2 r1^2/dr)
+// with g[j] = sin(tc[j]) dt[j], arm[i] = arp[i-1] (0 at r0: homogeneous Neumann,
+// A6), atm[j] = atp[j-1] (0 at the poles, A5), apm[k] = app[k-1] (periodic).
+// (A p)_m = sum_f A_f (p_m - p_nbr) + S_m p_m,  diag_m = sum_f A_f + S_m.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pot3d {
+
+constexpr int TK = 64;        // phi columns per tile (32 lanes x double2)
+constexpr int TJ = 8;         // theta rows per tile (one warp per row)
+constexpr int NTHREADS = TJ * 32;
+constexpr int SROW = TK + 4;  // smem row: [pad][left halo][TK interior][right halo][pad]
+constexpr int SROWS = TJ + 2; // rows j0-1 .. j0+TJ
+
+struct Metrics {
+  // r (global index, size nr)
+  const double *arp, *arm, *dr, *ss;
+  // theta (size nt)
+  const double *g, *atp, *atm, *q;
+  // phi (size np)
+  const double *dp, *app, *apm;
+};
+
+// Device-resident PCG scalars (A9).  One instance per context.
+struct Scalars {
+  double rho;        // r.z of the current residual
+  double alpha;      // step of the current iteration
+  double alpha_prev; // step applied to x lazily in the next pass A
+  double beta;       // p_k = z_k + beta p_{k-1}
+  double sigma;      // p.Ap
+  double rr;         // ||r||^2
+  double bnorm;      // ||b||
+  double rtol;
+  double pad0;
+  long long iter;    // completed alpha-updates
+  long long maxit;
+  int stop;          // 1: loop finished (converged, maxit, error)
+  int status;        // 0 ok / 1 not converged / -4 indefinite
+  unsigned int counter[4]; // last-block counters
+};
+
+struct Grid {
+  int nr, nt, np;     // global cells
+  int i0, nr_loc;     // slab
+  int PK;             // row pitch (doubles)
+  long long plane;    // nt * PK
+  int nchunks;        // r chunks per fused pass
+  int ntj, ntk;       // tiles
+};
+
+// Cell (il, j, k) of an array with ghost shells.
+__host__ __device__ inline long long cidx(const Grid &g, int il, int j, int k) {
+  return (long long)(il + 1) * g.plane + (long long)j * g.PK + k;
+}
+
+
+// Arguments of the fused passes (kernels.cu, k_pass<PASS_A, USE_Z>).
+struct PassArgs {
+  Grid G;
+  Metrics M;
+  Scalars *S;
+  const double *r;      // A: r (read, PC1)      B: r (read)
+  double *r_out;        // B: r (write, same buffer)
+  const double *z;      // A (PC2): stored z = M^-1 r
+  const double *p_old;  // A
+  double *p_new;        // A: write, B: read
+  double *x;            // A
+  double *partials;
+  double *hist;
+  int finalize;         // 1: single rank, finalise scalars in the last block
+  double *local_sum;    // nranks > 1: this rank's sums for the all-gather
+};
+
+// Arguments of the field kernels (a11).
+struct FieldArgs {
+  Grid G;
+  const double *x;
+  const double *br;      // device-layout boundary map [j][k]
+  const double *mean2;   // closed-wall mean sums or nullptr
+  const double *rc, *dr, *drh, *tc, *tf, *dth, *st, *dph;
+  const double *poleN, *poleS;  // per local shell
+  int bc;
+  int nbr;               // r faces on this rank
+  double *Br, *Bt, *Bp;  // device layout: [face][j][k], [i][jf][k], [i][j][k] (pitch PK)
+};
+
+// kernels.cu
+__global__ void k_metrics(int nr, int nt, int np, int bc, const double *rf, const double *tf,
+                          const double *pf, double *arp, double *arm, double *dr, double *ss,
+                          double *g, double *atp, double *atm, double *q, double *dp, double *app,
+                          double *apm, double *rc, double *drh, double *tc, double *dth,
+                          double *st, double *dph, double *vr);
+__global__ void k_pass_a_pc1(PassArgs A);  // a3, z = D^-1 r on the fly
+__global__ void k_pass_a_pc2(PassArgs A);  // a3, z from the PC2 sweeps
+__global__ void k_pass_b_pc1(PassArgs A);  // a7 + a8
+__global__ void k_pass_b_pc2(PassArgs A);  // a7 (||r|| only)
+__global__ void k_finalize_alpha(Scalars *S, const double *gathered, int nranks);
+__global__ void k_finalize_beta(Scalars *S, const double *gathered, int nranks, double *hist);
+__global__ void k_finalize_rr(Scalars *S, const double *gathered, int nranks, double *hist);
+__global__ void k_finalize_rho(Scalars *S, const double *gathered, int nranks);
+__global__ void k_init_dots(Grid G, Metrics M, Scalars *S, const double *r, double *partials,
+                            int finalize, double *local_sum, int use_z, const double *z);
+__global__ void k_init_finalize(Scalars *S, const double *gathered, int nranks);
+__global__ void k_apply(Grid G, Metrics M, const double *x, double *y, const double *bshell,
+                        int b_il, Scalars *S, double *partials, double *local_sum);
+__global__ void k_br_mean(Grid G, Metrics M, const double *br, double *out2);
+__global__ void k_rhs(Grid G, Metrics M, double r0, const double *br, const double *mean2,
+                      double *bshell);
+__global__ void k_axpy_cells(Grid G, double *x, const double *p, const Scalars *S);
+__global__ void k_gauge_sums(Grid G, Metrics M, const double *vr, const double *x, Scalars *S,
+                             double *partials, double *local_sum);
+__global__ void k_gauge_shift(Grid G, double *x, const double *gathered, int nranks);
+__global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, const double *src,
+                            double *dst, int to_dev);
+__global__ void k_field_r(FieldArgs F);
+__global__ void k_field_t(FieldArgs F);
+__global__ void k_field_p(FieldArgs F);
+__global__ void k_pole_avg(Grid G, const double *x, const double *dp, double period, double *poleN,
+                           double *poleS);
+// mode -1: z = D^-1 src on every plane (PC1 apply); 0: p_new = D^-1 src + beta p_old on the
+// two edge shells (PC1); 1: p_new = src + beta p_old on the edge shells (PC2, src = z)
+__global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const double *p_old,
+                         double *p_new, int mode);
+
+// pc2.cu -- PC2 (block ILU0 = D-ILU, A11) with tiled sync-free wavefront sweeps
+struct Pc2;
+int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
+               void *(*alloc)(size_t, void *), void *actx);
+int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host);
+// z = M^-1 r; partial r.z -> finalize (single rank: rho/beta update, mode iteration) or
+// local_sum[0]; `iteration` selects the predicated in-loop variant.
+int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, double *partials,
+              int finalize, double *local_sum, cudaStream_t s, bool iteration);
+void pc2_destroy(Pc2 *P, void (*fr)(void *, void *), void *actx);
+size_t pc2_bytes(const Pc2 *P);
+int pc2_kernels_per_apply(const Pc2 *P);
+
+}  // namespace pot3d

@@ -1,0 +1,283 @@
+"""Thin ctypes binding of libpot3d.so (include/pot3d.h) -- argument marshalling only.
+
+Every step of the solve runs in the CUDA kernels of libpot3d.so.  PyTorch is
+used only as plumbing: the device allocator (caching allocator callbacks), the
+stream all work is ordered on, and torch.distributed to broadcast the NCCL id.
+There is no CPU fallback: on a machine without the built library or without a
+CUDA device the constructor raises.
+
+Array arguments may be numpy arrays (host) or torch tensors (host or cuda);
+layouts are those of include/pot3d.h (phi: shape (np, nt, nr_loc), r fastest;
+br0: shape (np, nt), theta fastest).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+SOURCE_SURFACE = 0
+CLOSED_WALL = 1
+PC1 = 1
+PC2 = 2
+
+OK = 0
+NOT_CONVERGED = 1
+PC2_FELL_BACK = 2
+STATUS_NAMES = {0: "ok", 1: "not_converged", 2: "pc2_fell_back", -1: "invalid", -2: "cuda",
+                -3: "nccl", -4: "indefinite", -5: "oom", -6: "state"}
+
+EXPORTS = ["pot3d_setup", "pot3d_set_br0", "pot3d_solve", "pot3d_field", "pot3d_apply",
+           "pot3d_precond", "pot3d_history", "pot3d_info", "pot3d_profile", "pot3d_nccl_unique_id",
+           "pot3d_destroy", "pot3d_last_error"]
+
+_ALLOC = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+_FREE = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class Pot3dError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Grid(ctypes.Structure):
+    _fields_ = [("nr", ctypes.c_int32), ("nt", ctypes.c_int32), ("np", ctypes.c_int32),
+                ("r_faces", ctypes.POINTER(ctypes.c_double)),
+                ("t_faces", ctypes.POINTER(ctypes.c_double)),
+                ("p_faces", ctypes.POINTER(ctypes.c_double))]
+
+
+class _Runtime(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p),
+                ("alloc", _ALLOC), ("free", _FREE), ("alloc_ctx", ctypes.c_void_p),
+                ("pc2_blocks", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("unroll", ctypes.c_int32)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("i0", ctypes.c_int32), ("i1", ctypes.c_int32), ("nr_loc", ctypes.c_int32),
+                ("br_shells", ctypes.c_int32), ("pc", ctypes.c_int32),
+                ("pc2_blocks_total", ctypes.c_int32), ("graph_kernels_per_iter", ctypes.c_int64),
+                ("bytes_per_iter", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def library(build_if_missing: bool = True):
+    """Load libpot3d.so (building it with nvcc if it is missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing:
+        try:
+            _build.build()
+        except Exception:
+            if not _build.LIB.exists():
+                raise
+    if not _build.LIB.exists():
+        raise ImportError(f"{_build.LIB} is missing: run __graft_entry__.build()")
+    L = ctypes.CDLL(str(_build.LIB))
+    vp, d, i64 = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)
+    L.pot3d_setup.argtypes = [ctypes.POINTER(_Grid), vp, ctypes.c_int32, ctypes.c_int32,
+                              ctypes.POINTER(_Runtime), ctypes.POINTER(vp)]
+    L.pot3d_set_br0.argtypes = [vp, vp]
+    L.pot3d_solve.argtypes = [vp, ctypes.c_double, ctypes.c_int64, vp, i64, d, d]
+    L.pot3d_field.argtypes = [vp, vp, vp, vp]
+    L.pot3d_apply.argtypes = [vp, vp, vp]
+    L.pot3d_precond.argtypes = [vp, vp, vp]
+    L.pot3d_history.argtypes = [vp, vp, ctypes.c_int64]
+    L.pot3d_history.restype = ctypes.c_int64
+    L.pot3d_info.argtypes = [vp, ctypes.POINTER(_Info)]
+    L.pot3d_profile.argtypes = [vp, ctypes.c_int32, d, d, d]
+    L.pot3d_nccl_unique_id.argtypes = [vp]
+    L.pot3d_destroy.argtypes = [vp]
+    L.pot3d_last_error.argtypes = [vp]
+    L.pot3d_last_error.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = library().pot3d_nccl_unique_id(buf)
+    if rc:
+        raise Pot3dError(rc, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def _ptr(a):
+    """(pointer, keepalive) of a numpy array or torch tensor, fp64 contiguous."""
+    try:
+        import torch
+
+        if isinstance(a, torch.Tensor):
+            if a.dtype != torch.float64 or not a.is_contiguous():
+                raise TypeError("torch tensors must be contiguous float64")
+            return ctypes.c_void_p(a.data_ptr()), a
+    except ImportError:
+        pass
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    return ctypes.c_void_p(arr.ctypes.data), arr
+
+
+@dataclass
+class SolveResult:
+    phi: object
+    iters: int
+    rel_residual: float
+    true_rel_residual: float
+    status: int
+
+
+class Pot3d:
+    """One context of the C ABI (one rank's r-slab on one GPU)."""
+
+    def __init__(self, r_faces, t_faces, p_faces, br0, bc=SOURCE_SURFACE, pc=PC1, *, rank=0,
+                 nranks=1, nccl_id: bytes | None = None, stream=None, pc2_blocks=1, device=None,
+                 unroll=8, torch_allocator=True):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("pot3d needs a CUDA device (no CPU fallback)")
+        L = library()
+        self._L = L
+        self.rf = np.ascontiguousarray(r_faces, dtype=np.float64)
+        self.tf = np.ascontiguousarray(t_faces, dtype=np.float64)
+        self.pf = np.ascontiguousarray(p_faces, dtype=np.float64)
+        self.nr, self.nt, self.np = len(self.rf) - 1, len(self.tf) - 1, len(self.pf) - 1
+        dev = torch.cuda.current_device() if device is None else int(device)
+        self.device = dev
+        torch.cuda.set_device(dev)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        g = _Grid(self.nr, self.nt, self.np,
+                  self.rf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                  self.tf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                  self.pf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        rt = _Runtime()
+        rt.rank, rt.nranks = rank, nranks
+        self._nccl_id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        rt.nccl_unique_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if nccl_id else None
+        rt.cuda_stream = self.stream.cuda_stream
+        if torch_allocator:
+            stream_handle = self.stream
+
+            def _alloc(nbytes, _ctx):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), dev, stream_handle)
+                except Exception:
+                    return None
+
+            def _free(ptr, _ctx):
+                torch.cuda.caching_allocator_delete(ptr)
+
+            self._cb = (_ALLOC(_alloc), _FREE(_free))
+            rt.alloc, rt.free = self._cb
+        rt.pc2_blocks = pc2_blocks
+        rt.device = dev
+        rt.unroll = unroll
+        p_br, keep = _ptr(br0)
+        ctx = ctypes.c_void_p()
+        rc = L.pot3d_setup(ctypes.byref(g), p_br, bc, pc, ctypes.byref(rt), ctypes.byref(ctx))
+        del keep
+        if rc < 0:
+            raise Pot3dError(rc, L.pot3d_last_error(None).decode())
+        self._ctx = ctx
+        self.bc, self.pc_requested = bc, pc
+        inf = self.info()
+        self.i0, self.i1, self.nr_loc = inf["i0"], inf["i1"], inf["nr_loc"]
+
+    # -- helpers ----------------------------------------------------------
+    def _check(self, rc):
+        if rc < 0:
+            raise Pot3dError(rc, self._L.pot3d_last_error(self._ctx).decode())
+        return rc
+
+    def _out(self, shape, out):
+        if out == "numpy":
+            return np.empty(shape, dtype=np.float64)
+        import torch
+
+        return torch.empty(shape, dtype=torch.float64, device=out)
+
+    def info(self):
+        inf = _Info()
+        self._check(self._L.pot3d_info(self._ctx, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in _Info._fields_}
+
+    # -- API ----------------------------------------------------------------
+    def set_br0(self, br0):
+        p, keep = _ptr(br0)
+        self._check(self._L.pot3d_set_br0(self._ctx, p))
+
+    def solve(self, rtol=1e-9, maxit=100000, want_phi=True, true_residual=True, out="numpy",
+              phi=None):
+        if want_phi and phi is None:
+            phi = self._out((self.np, self.nt, self.nr_loc), out)
+        p_phi = _ptr(phi)[0] if phi is not None else None
+        it = ctypes.c_int64(0)
+        rr = ctypes.c_double(0)
+        tr = ctypes.c_double(0)
+        rc = self._L.pot3d_solve(self._ctx, float(rtol), int(maxit), p_phi, ctypes.byref(it),
+                                 ctypes.byref(rr), ctypes.byref(tr) if true_residual else None)
+        self._check(rc)
+        return SolveResult(phi, it.value, rr.value, tr.value if true_residual else float("nan"), rc)
+
+    def field(self, out="numpy"):
+        inf = self.info()
+        br = self._out((self.np, self.nt, inf["br_shells"]), out)
+        bt = self._out((self.np, self.nt + 1, self.nr_loc), out)
+        bp = self._out((self.np, self.nt, self.nr_loc), out)
+        self._check(self._L.pot3d_field(self._ctx, _ptr(br)[0], _ptr(bt)[0], _ptr(bp)[0]))
+        return br, bt, bp
+
+    def apply(self, x, out="numpy"):
+        px, keep = _ptr(x)
+        y = self._out((self.np, self.nt, self.nr_loc), out)
+        self._check(self._L.pot3d_apply(self._ctx, px, _ptr(y)[0]))
+        return y
+
+    def precond(self, r, out="numpy"):
+        pr, keep = _ptr(r)
+        z = self._out((self.np, self.nt, self.nr_loc), out)
+        self._check(self._L.pot3d_precond(self._ctx, pr, _ptr(z)[0]))
+        return z
+
+    def history(self, n):
+        h = np.empty(int(n), dtype=np.float64)
+        m = self._L.pot3d_history(self._ctx, ctypes.c_void_p(h.ctypes.data), int(n))
+        self._check(m)
+        return h[:m]
+
+    def profile(self, iters=20):
+        """Mean device ms per launch of pass A, pass B and the PC2 sweeps (events on
+        the context stream); continues the current recurrences and invalidates the
+        last solution."""
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        self._check(self._L.pot3d_profile(self._ctx, int(iters), ctypes.byref(a), ctypes.byref(b),
+                                          ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._L.pot3d_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
