@@ -261,9 +261,9 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
   }
   if (pc2)
-    k_pass_a_pc2<<<grd, NTHREADS, 0, ctx->stream>>>(a);
+    k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(a);
   else
-    k_pass_a_pc1<<<grd, NTHREADS, 0, ctx->stream>>>(a);
+    k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(a);
   CK(cudaGetLastError());
     ctx->n_enq++;
   if (multi) {
@@ -273,9 +273,9 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     ctx->n_enq++;
   }
   if (pc2)
-    k_pass_b_pc2<<<grd, NTHREADS, 0, ctx->stream>>>(a);
+    k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(a);
   else
-    k_pass_b_pc1<<<grd, NTHREADS, 0, ctx->stream>>>(a);
+    k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(a);
   CK(cudaGetLastError());
     ctx->n_enq++;
   if (multi) {
@@ -332,9 +332,9 @@ int choose_chunks(pot3d_ctx *ctx) {
   }
   int occ = 0, sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_b_pc1, NTHREADS, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_b_pc1, NTHREADS, SMEM_B));
   int occa = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occa, k_pass_a_pc1, NTHREADS, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occa, k_pass_a_pc1, NTHREADS, SMEM_A));
   occ = std::max(1, std::min(occ, occa));
   const double slots = (double)sms * occ;
   const long long tiles = (long long)G.ntj * G.ntk;
@@ -535,6 +535,17 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   G.plane = (long long)nt * G.PK;
   G.ntj = (nt + TJ - 1) / TJ;
   G.ntk = (np + TK - 1) / TK;
+  {
+    const void *fa[2] = {(const void *)k_pass_a_pc1, (const void *)k_pass_a_pc2};
+    const void *fb[2] = {(const void *)k_pass_b_pc1, (const void *)k_pass_b_pc2};
+    for (int q = 0; q < 2; q++) {
+      if (cudaFuncSetAttribute(fa[q], cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_A) ||
+          cudaFuncSetAttribute(fb[q], cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B)) {
+        ctx->err = "cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed";
+        return fail(POT3D_ERR_CUDA);
+      }
+    }
+  }
   { int rc = choose_chunks(ctx); if (rc) return fail(rc); }
 
   // metrics (a1)
@@ -923,10 +934,10 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
     a.hist = nullptr;
     a.finalize = 1;
     CK(cudaEventRecord(ev[0], s));
-    if (pc2) k_pass_a_pc2<<<grd, NTHREADS, 0, s>>>(a); else k_pass_a_pc1<<<grd, NTHREADS, 0, s>>>(a);
+    if (pc2) k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, s>>>(a); else k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, s>>>(a);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev[1], s));
-    if (pc2) k_pass_b_pc2<<<grd, NTHREADS, 0, s>>>(a); else k_pass_b_pc1<<<grd, NTHREADS, 0, s>>>(a);
+    if (pc2) k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, s>>>(a); else k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, s>>>(a);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev[2], s));
     ctx->n_launch += 2;

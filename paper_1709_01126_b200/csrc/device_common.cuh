@@ -1,0 +1,194 @@
+// device_common.cuh -- device helpers shared by kernels.cu, passes.cu, pc2.cu:
+// deterministic reductions (a6), device-side scalar updates (a10), metric
+// helpers, a Newton-corrected fp64 quotient and cp.async wrappers.
+#pragma once
+#include "pot3d_internal.cuh"
+
+namespace pot3d {
+
+// ---------------------------------------------------------------------------
+// Deterministic reductions (a6).  Level 1: warp shuffle tree + fixed-order
+// combine of the warps of a block.  Level 2: the last block to finish sums
+// the per-block partials in index order (threads stride, then a fixed tree),
+// so the result does not depend on which block finishes last.
+// ---------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ void warp_sum(double (&v)[N]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int n = 0; n < N; n++) v[n] += __shfl_xor_sync(0xffffffffu, v[n], o);
+}
+
+// Reduces v over the block; the result is valid in thread 0.
+template <int N>
+__device__ __forceinline__ void block_sum(double (&v)[N], double *sred) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  warp_sum<N>(v);
+  __syncthreads();  // sred may still be read by a previous use
+  if (lane == 0)
+#pragma unroll
+    for (int n = 0; n < N; n++) sred[w * N + n] = v[n];
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int n = 0; n < N; n++) v[n] = (lane < nw) ? sred[lane * N + n] : 0.0;
+    warp_sum<N>(v);
+  }
+}
+
+// Writes this block's partial, and returns true in the (single) last block,
+// where `tot` then holds the grid total in every thread 0.
+template <int N>
+__device__ __forceinline__ bool grid_sum(double (&v)[N], double *partials, unsigned int *counter, double *sred,
+                         double (&tot)[N]) {
+  __shared__ bool s_last;
+  const int nb = gridDim.x * gridDim.y;
+  const int bid = blockIdx.x + gridDim.x * blockIdx.y;
+  block_sum<N>(v, sred);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int n = 0; n < N; n++) partials[(size_t)n * nb + bid] = v[n];
+    __threadfence();
+    unsigned int t = atomicAdd(counter, 1u);
+    s_last = (t == (unsigned)nb - 1);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  double a[N];
+#pragma unroll
+  for (int n = 0; n < N; n++) a[n] = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+    for (int n = 0; n < N; n++) a[n] += __ldcg(partials + (size_t)n * nb + b);
+  block_sum<N>(a, sred);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int n = 0; n < N; n++) tot[n] = a[n];
+    *counter = 0u;
+  }
+  return true;
+}
+
+// After pass A: alpha = rho / p.Ap; p.Ap <= 0 -> indefinite.
+__device__ __forceinline__ void finalize_alpha(Scalars *S, double sigma) {
+  S->sigma = sigma;
+  if (!(sigma > 0.0)) {
+    S->status = -4;
+    S->stop = 1;
+    return;
+  }
+  S->alpha = S->rho / sigma;
+}
+
+// After pass B: iteration count, convergence test ||r|| <= rtol ||b|| on the
+// recurrence residual (A9), beta = rho'/rho.
+__device__ __forceinline__ void finalize_beta(Scalars *S, double rz, double rr, double *hist) {
+  long long it = S->iter + 1;
+  S->iter = it;
+  S->rr = rr;
+  double rn = sqrt(rr);
+  if (hist) hist[it] = rn / S->bnorm;
+  S->alpha_prev = S->alpha;
+  if (rn <= S->rtol * S->bnorm) {
+    S->stop = 1;
+    S->status = 0;
+    return;
+  }
+  if (it >= S->maxit) {
+    S->stop = 1;
+    S->status = 1;
+    return;
+  }
+  S->beta = rz / S->rho;
+  S->rho = rz;
+}
+
+// PC2 split of finalize_beta: ||r|| test after pass B, rho/beta after the sweeps.
+__device__ __forceinline__ void finalize_rr(Scalars *S, double rr, double *hist) {
+  long long it = S->iter + 1;
+  S->iter = it;
+  S->rr = rr;
+  double rn = sqrt(rr);
+  if (hist) hist[it] = rn / S->bnorm;
+  S->alpha_prev = S->alpha;
+  if (rn <= S->rtol * S->bnorm) {
+    S->stop = 1;
+    S->status = 0;
+  } else if (it >= S->maxit) {
+    S->stop = 1;
+    S->status = 1;
+  }
+}
+__device__ __forceinline__ void finalize_rho(Scalars *S, double rz) {
+  S->beta = rz / S->rho;
+  S->rho = rz;
+}
+// ---------------------------------------------------------------------------
+// Per-cell helpers.
+// ---------------------------------------------------------------------------
+struct RowC {  // theta factors of one row
+  double g, atp, atm, q;
+};
+struct PlaneC {  // r factors of one shell
+  double arp, arm, dr, ss;
+};
+
+__device__ __forceinline__ RowC row_c(const Metrics &M, int j) {
+  RowC c;
+  c.g = __ldg(M.g + j);
+  c.atp = __ldg(M.atp + j);
+  c.atm = __ldg(M.atm + j);
+  c.q = __ldg(M.q + j);
+  return c;
+}
+__device__ __forceinline__ PlaneC plane_c(const Metrics &M, int ig) {
+  PlaneC c;
+  c.arp = __ldg(M.arp + ig);
+  c.arm = __ldg(M.arm + ig);
+  c.dr = __ldg(M.dr + ig);
+  c.ss = __ldg(M.ss + ig);
+  return c;
+}
+// diag(A) = dp_k [g_j (arp_i + arm_i + ss_i) + dr_i (atp_j + atm_j)] + dr_i q_j (app_k + apm_k)
+struct DiagRow {  // diag = dp_k * a + b * sk
+  double a, b;
+};
+__device__ __forceinline__ DiagRow diag_row(const PlaneC &P, const RowC &R) {
+  DiagRow d;
+  d.a = R.g * (P.arp + P.arm + P.ss) + P.dr * (R.atp + R.atm);
+  d.b = P.dr * R.q;
+  return d;
+}
+
+
+// r / d for d > 0 (normal): approximate reciprocal (MUFU.RCP64H, ~2^-20), one
+// Newton step (~2^-40), product, then one remainder correction
+// q1 = q0 + y (r - d q0), which leaves the quotient within ~1 ulp of the
+// correctly rounded r/d at 6 fp64 operations instead of the DDIV sequence.
+__device__ __forceinline__ double fdiv(double r, double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  double q = r * y;
+  double rem = fma(-d, q, r);
+  return fma(y, rem, q);
+}
+
+// cp.async (LDGSTS) with zero-fill: copies src_bytes of 16 (8) and fills the
+// rest of the destination with zeros; src_bytes = 0 reads nothing.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+}  // namespace pot3d

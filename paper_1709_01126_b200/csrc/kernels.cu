@@ -20,7 +20,7 @@
 // 3-slot shared-memory ring for the theta/phi neighbours, the r neighbours
 // stay in registers, and the next plane is prefetched into registers while
 // the stencil of the current plane runs.
-#include "pot3d_internal.cuh"
+#include "device_common.cuh"
 
 namespace pot3d {
 #ifndef PASS_MINB
@@ -95,456 +95,6 @@ __global__ void k_metrics(int nr, int nt, int np, int bc, const double *rf, cons
     apm[k] = 1.0 / (pck - pcp);
   }
 }
-
-// ---------------------------------------------------------------------------
-// Deterministic reductions (a6).  Level 1: warp shuffle tree + fixed-order
-// combine of the warps of a block.  Level 2: the last block to finish sums
-// the per-block partials in index order (threads stride, then a fixed tree),
-// so the result does not depend on which block finishes last.
-// ---------------------------------------------------------------------------
-template <int N>
-__device__ __forceinline__ void warp_sum(double (&v)[N]) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int n = 0; n < N; n++) v[n] += __shfl_xor_sync(0xffffffffu, v[n], o);
-}
-
-// Reduces v over the block; the result is valid in thread 0.
-template <int N>
-__device__ __forceinline__ void block_sum(double (&v)[N], double *sred) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  warp_sum<N>(v);
-  __syncthreads();  // sred may still be read by a previous use
-  if (lane == 0)
-#pragma unroll
-    for (int n = 0; n < N; n++) sred[w * N + n] = v[n];
-  __syncthreads();
-  if (w == 0) {
-#pragma unroll
-    for (int n = 0; n < N; n++) v[n] = (lane < nw) ? sred[lane * N + n] : 0.0;
-    warp_sum<N>(v);
-  }
-}
-
-// Writes this block's partial, and returns true in the (single) last block,
-// where `tot` then holds the grid total in every thread 0.
-template <int N>
-__device__ bool grid_sum(double (&v)[N], double *partials, unsigned int *counter, double *sred,
-                         double (&tot)[N]) {
-  __shared__ bool s_last;
-  const int nb = gridDim.x * gridDim.y;
-  const int bid = blockIdx.x + gridDim.x * blockIdx.y;
-  block_sum<N>(v, sred);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int n = 0; n < N; n++) partials[(size_t)n * nb + bid] = v[n];
-    __threadfence();
-    unsigned int t = atomicAdd(counter, 1u);
-    s_last = (t == (unsigned)nb - 1);
-  }
-  __syncthreads();
-  if (!s_last) return false;
-  __threadfence();
-  double a[N];
-#pragma unroll
-  for (int n = 0; n < N; n++) a[n] = 0.0;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x)
-#pragma unroll
-    for (int n = 0; n < N; n++) a[n] += __ldcg(partials + (size_t)n * nb + b);
-  block_sum<N>(a, sred);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int n = 0; n < N; n++) tot[n] = a[n];
-    *counter = 0u;
-  }
-  return true;
-}
-
-// After pass A: alpha = rho / p.Ap; p.Ap <= 0 -> indefinite.
-__device__ void finalize_alpha(Scalars *S, double sigma) {
-  S->sigma = sigma;
-  if (!(sigma > 0.0)) {
-    S->status = -4;
-    S->stop = 1;
-    return;
-  }
-  S->alpha = S->rho / sigma;
-}
-
-// After pass B: iteration count, convergence test ||r|| <= rtol ||b|| on the
-// recurrence residual (A9), beta = rho'/rho.
-__device__ void finalize_beta(Scalars *S, double rz, double rr, double *hist) {
-  long long it = S->iter + 1;
-  S->iter = it;
-  S->rr = rr;
-  double rn = sqrt(rr);
-  if (hist) hist[it] = rn / S->bnorm;
-  S->alpha_prev = S->alpha;
-  if (rn <= S->rtol * S->bnorm) {
-    S->stop = 1;
-    S->status = 0;
-    return;
-  }
-  if (it >= S->maxit) {
-    S->stop = 1;
-    S->status = 1;
-    return;
-  }
-  S->beta = rz / S->rho;
-  S->rho = rz;
-}
-
-// PC2 split of finalize_beta: ||r|| test after pass B, rho/beta after the sweeps.
-__device__ void finalize_rr(Scalars *S, double rr, double *hist) {
-  long long it = S->iter + 1;
-  S->iter = it;
-  S->rr = rr;
-  double rn = sqrt(rr);
-  if (hist) hist[it] = rn / S->bnorm;
-  S->alpha_prev = S->alpha;
-  if (rn <= S->rtol * S->bnorm) {
-    S->stop = 1;
-    S->status = 0;
-  } else if (it >= S->maxit) {
-    S->stop = 1;
-    S->status = 1;
-  }
-}
-__device__ void finalize_rho(Scalars *S, double rz) {
-  S->beta = rz / S->rho;
-  S->rho = rz;
-}
-// ---------------------------------------------------------------------------
-// Per-cell helpers.
-// ---------------------------------------------------------------------------
-struct RowC {  // theta factors of one row
-  double g, atp, atm, q;
-};
-struct PlaneC {  // r factors of one shell
-  double arp, arm, dr, ss;
-};
-
-__device__ __forceinline__ RowC row_c(const Metrics &M, int j) {
-  RowC c;
-  c.g = __ldg(M.g + j);
-  c.atp = __ldg(M.atp + j);
-  c.atm = __ldg(M.atm + j);
-  c.q = __ldg(M.q + j);
-  return c;
-}
-__device__ __forceinline__ PlaneC plane_c(const Metrics &M, int ig) {
-  PlaneC c;
-  c.arp = __ldg(M.arp + ig);
-  c.arm = __ldg(M.arm + ig);
-  c.dr = __ldg(M.dr + ig);
-  c.ss = __ldg(M.ss + ig);
-  return c;
-}
-// diag(A) = dp_k [g_j (arp_i + arm_i + ss_i) + dr_i (atp_j + atm_j)] + dr_i q_j (app_k + apm_k)
-struct DiagRow {  // diag = dp_k * a + b * sk
-  double a, b;
-};
-__device__ __forceinline__ DiagRow diag_row(const PlaneC &P, const RowC &R) {
-  DiagRow d;
-  d.a = R.g * (P.arp + P.arm + P.ss) + P.dr * (R.atp + R.atm);
-  d.b = P.dr * R.q;
-  return d;
-}
-
-// ---------------------------------------------------------------------------
-// Fused pass kernels.
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ void chunk_bounds(const Grid &G, int c, int &c0, int &c1) {
-  int base = G.nr_loc / G.nchunks, rem = G.nr_loc % G.nchunks;
-  c0 = c * base + (c < rem ? c : rem);
-  c1 = c0 + base + (c < rem ? 1 : 0);
-}
-
-// Loaded data of one plane for one thread (own item + halo duties).
-struct LoadA {
-  double2 r, p, x;     // own item
-  double2 hr, hp;      // halo row item (warps 0 / TJ-1)
-  double cr, cp;       // halo column (lanes 0 / 31)
-};
-
-template <bool PASS_A, bool USE_Z>
-__device__ __forceinline__ void pass_body(const PassArgs &A) {
-  const Grid &G = A.G;
-  const Metrics &M = A.M;
-  Scalars *S = A.S;
-  if (S->stop) return;
-
-  __shared__ __align__(16) double sm[3][SROWS][SROW];
-  __shared__ double sred[(NTHREADS / 32) * 2];
-
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int tile = blockIdx.x;
-  const int tj = tile % G.ntj, tk = tile / G.ntj;
-  const int j0 = tj * TJ, k0 = tk * TK;
-  int c0, c1;
-  chunk_bounds(G, blockIdx.y, c0, c1);
-
-  const int j = j0 + w;                 // own row
-  const bool jv = j < G.nt;
-  const int k = k0 + 2 * lane;          // own columns k, k+1
-  const bool kv0 = k < G.np, kv1 = (k + 1) < G.np;
-  const bool lv = jv && kv0;            // own item loads/stores
-  // halo duties
-  const int hrow = (w == 0) ? j0 - 1 : ((w == TJ - 1) ? j0 + TJ : -2);  // -2: none
-  const bool hv = (hrow >= 0) && (hrow < G.nt) && (w == 0 || w == TJ - 1);
-  const int hslot = (w == 0) ? 0 : TJ + 1;
-  // halo columns: lane 0 -> left neighbour of k0, lane 31 -> right neighbour of the last column
-  const int kend = min(k0 + TK, G.np);
-  const int hcol = (lane == 0) ? (k0 == 0 ? G.np - 1 : k0 - 1) : (kend == G.np ? 0 : kend);
-  const int hs = (lane == 0) ? 1 : (kend - k0 + 2);
-  const bool cv = jv && (lane == 0 || lane == 31);
-
-  // per-column and per-row constant factors
-  const int ka = min(k, G.np - 1), kb = min(k + 1, G.np - 1);
-  const double dp0 = __ldg(M.dp + ka), dp1 = __ldg(M.dp + kb);
-  const double app0 = __ldg(M.app + ka), app1 = __ldg(M.app + kb);
-  const double apm0 = __ldg(M.apm + ka), apm1 = __ldg(M.apm + kb);
-  const double sk0 = app0 + apm0, sk1 = app1 + apm1;
-  const RowC rw = row_c(M, jv ? j : 0);
-  const double beta = PASS_A ? S->beta : 0.0;
-  const double alpha_prev = PASS_A ? S->alpha_prev : 0.0;
-  const double alpha = PASS_A ? 0.0 : S->alpha;
-
-  const double *src_r = PASS_A ? (USE_Z ? A.z : A.r) : nullptr;
-
-  // ---- load one plane (il in [c0-1, c1]) into registers ----
-  // PASS_A: own item r/z, p_old, x (x only for owned planes); halo row r/z, p_old; halo col r/z, p_old.
-  //         On ghost planes (il < 0 or il >= nr_loc) p_new is final (halo exchange): load p_new.
-  // PASS_B: own item p_new, plus r of plane il-1 (consumed by the stencil of il-1);
-  //         halo row / col p_new.
-  auto load = [&](int il, LoadA &L) {
-    const bool ghost = (il < 0) || (il >= G.nr_loc);
-    const long long rowbase = cidx(G, il, jv ? j : 0, 0);
-    const double2 Z2 = make_double2(0.0, 0.0);
-    if (PASS_A) {
-      if (ghost) {
-        L.r = lv ? *reinterpret_cast<const double2 *>(A.p_new + rowbase + k) : Z2;
-        L.p = Z2;
-      } else {
-        L.r = lv ? __ldcs(reinterpret_cast<const double2 *>(src_r + rowbase + k)) : Z2;
-        L.p = lv ? __ldcs(reinterpret_cast<const double2 *>(A.p_old + rowbase + k)) : Z2;
-      }
-      const bool own = (il >= c0) && (il < c1);
-      L.x = (lv && own) ? __ldcs(reinterpret_cast<const double2 *>(A.x + rowbase + k)) : Z2;
-      if (hv) {
-        const long long hb = cidx(G, il, hrow, 0);
-        if (ghost) {
-          L.hr = kv0 ? *reinterpret_cast<const double2 *>(A.p_new + hb + k) : Z2;
-          L.hp = Z2;
-        } else {
-          L.hr = kv0 ? *reinterpret_cast<const double2 *>(src_r + hb + k) : Z2;
-          L.hp = kv0 ? *reinterpret_cast<const double2 *>(A.p_old + hb + k) : Z2;
-        }
-      }
-      if (cv) {
-        const long long cb = rowbase + hcol;
-        if (ghost) {
-          L.cr = A.p_new[cb];
-          L.cp = 0.0;
-        } else {
-          L.cr = src_r[cb];
-          L.cp = A.p_old[cb];
-        }
-      }
-    } else {
-      L.p = lv ? *reinterpret_cast<const double2 *>(A.p_new + rowbase + k) : Z2;
-      const int ir = il - 1;
-      const bool own = (ir >= c0) && (ir < c1);
-      L.r = (lv && own) ? __ldcs(reinterpret_cast<const double2 *>(A.r + cidx(G, ir, j, k))) : Z2;
-      if (hv) L.hp = kv0 ? *reinterpret_cast<const double2 *>(A.p_new + cidx(G, il, hrow, k)) : Z2;
-      if (cv) L.cp = A.p_new[rowbase + hcol];
-    }
-  };
-
-  // ---- transform a loaded plane: p_new values to registers (own) and smem ----
-  // The own item is written to smem first; after __syncwarp the halo column
-  // may overwrite the padding slot that follows the last phi column (the
-  // periodic wrap neighbour lives there on the last tile).
-  auto transform = [&](int il, const LoadA &L, double2 &pn, int slot, bool to_smem) {
-    const bool ghost = (il < 0) || (il >= G.nr_loc);
-    const double2 Z2 = make_double2(0.0, 0.0);
-    double2 h = Z2;  // halo-row value
-    double cvv = 0.0; // halo-column value
-    if (PASS_A) {
-      if (ghost) {
-        pn = L.r;  // loaded p_new (already final on ghost shells)
-        h = L.hr;
-        cvv = L.cr;
-      } else {
-        const PlaneC pc = plane_c(M, G.i0 + il);
-        if (lv) {
-          if (USE_Z) {
-            pn.x = L.r.x + beta * L.p.x;
-            pn.y = L.r.y + beta * L.p.y;
-          } else {
-            const DiagRow d = diag_row(pc, rw);
-            pn.x = L.r.x / (dp0 * d.a + d.b * sk0) + beta * L.p.x;
-            pn.y = L.r.y / (dp1 * d.a + d.b * sk1) + beta * L.p.y;
-          }
-          if (!kv1) pn.y = 0.0;
-        } else {
-          pn = Z2;
-        }
-        const bool own = (il >= c0) && (il < c1);
-        if (own && lv) {
-          const long long o = cidx(G, il, j, k);
-          if (kv1) {
-            *reinterpret_cast<double2 *>(A.p_new + o) = pn;
-            double2 xv = L.x;
-            xv.x += alpha_prev * L.p.x;
-            xv.y += alpha_prev * L.p.y;
-            __stcs(reinterpret_cast<double2 *>(A.x + o), xv);
-          } else {
-            A.p_new[o] = pn.x;
-            A.x[o] = L.x.x + alpha_prev * L.p.x;
-          }
-        }
-        if (to_smem) {
-          if (hv && kv0) {
-            const RowC hrw = row_c(M, hrow);
-            if (USE_Z) {
-              h.x = L.hr.x + beta * L.hp.x;
-              h.y = L.hr.y + beta * L.hp.y;
-            } else {
-              const DiagRow d = diag_row(pc, hrw);
-              h.x = L.hr.x / (dp0 * d.a + d.b * sk0) + beta * L.hp.x;
-              h.y = L.hr.y / (dp1 * d.a + d.b * sk1) + beta * L.hp.y;
-            }
-            if (!kv1) h.y = 0.0;
-          }
-          if (cv) {
-            if (USE_Z) {
-              cvv = L.cr + beta * L.cp;
-            } else {
-              const DiagRow d = diag_row(pc, rw);
-              const double dpc = __ldg(M.dp + hcol);
-              const double skc = __ldg(M.app + hcol) + __ldg(M.apm + hcol);
-              cvv = L.cr / (dpc * d.a + d.b * skc) + beta * L.cp;
-            }
-          }
-        }
-      }
-    } else {
-      pn = L.p;
-      h = L.hp;
-      cvv = L.cp;
-    }
-    if (to_smem) {
-      *reinterpret_cast<double2 *>(&sm[slot][w + 1][2 + 2 * lane]) = pn;
-      // halo rows: neighbours above/below the tile; rows outside the grid
-      // (beyond a pole) read as 0 and carry zero coupling (A5)
-      if (w == 0 || w == TJ - 1)
-        *reinterpret_cast<double2 *>(&sm[slot][hslot][2 + 2 * lane]) = hv ? h : Z2;
-      __syncwarp();
-      if (cv) sm[slot][w + 1][hs] = cvv;
-    }
-  };
-
-  double acc0 = 0.0, acc1 = 0.0;  // A: p.q      B: r.z, r.r
-  double2 pm, pc, pn;
-  LoadA L;
-  // prologue: planes c0-1 and c0
-  load(c0 - 1, L);
-  transform(c0 - 1, L, pm, 2, false);
-  load(c0, L);
-  transform(c0, L, pc, c0 % 3, true);
-  if (c0 + 1 <= c1) load(c0 + 1, L);
-
-  for (int il = c0; il < c1; il++) {
-    const int slot_n = (il + 1) % 3, slot_c = il % 3;
-    transform(il + 1, L, pn, slot_n, il + 1 < c1);
-    // In pass B, r of plane il arrived with the load of plane il+1.
-    const double2 rcur = L.r;
-    if (il + 2 <= c1) load(il + 2, L);
-    __syncthreads();
-    if (jv) {
-      const PlaneC P = plane_c(M, G.i0 + il);
-      const double2 up = *reinterpret_cast<const double2 *>(&sm[slot_c][w][2 + 2 * lane]);
-      const double2 dn = *reinterpret_cast<const double2 *>(&sm[slot_c][w + 2][2 + 2 * lane]);
-      const double lf = sm[slot_c][w + 1][1 + 2 * lane];
-      const double rt = sm[slot_c][w + 1][4 + 2 * lane];
-      // element 0: left = lf, right = pc.y (or the wrap halo if element 1 is
-      // padding); element 1: left = pc.x, right = rt
-      const double c0v = pc.x, c1v = pc.y;
-      const double r0n = kv1 ? c1v : sm[slot_c][w + 1][3 + 2 * lane];
-      double q0 = dp0 * (rw.g * (P.arp * (c0v - pn.x) + P.arm * (c0v - pm.x) + P.ss * c0v) +
-                         P.dr * (rw.atp * (c0v - dn.x) + rw.atm * (c0v - up.x))) +
-                  P.dr * rw.q * (app0 * (c0v - r0n) + apm0 * (c0v - lf));
-      double q1 = dp1 * (rw.g * (P.arp * (c1v - pn.y) + P.arm * (c1v - pm.y) + P.ss * c1v) +
-                         P.dr * (rw.atp * (c1v - dn.y) + rw.atm * (c1v - up.y))) +
-                  P.dr * rw.q * (app1 * (c1v - rt) + apm1 * (c1v - c0v));
-      if (PASS_A) {
-        if (kv0) acc0 += c0v * q0;
-        if (kv1) acc0 += c1v * q1;
-      } else {
-        const long long o = cidx(G, il, j, k);
-        double2 rn;
-        rn.x = rcur.x - alpha * q0;
-        rn.y = rcur.y - alpha * q1;
-        if (USE_Z) {  // PC2: z is formed by the sweeps; only ||r||^2 here
-          if (kv0) acc1 += rn.x * rn.x;
-          if (kv1) acc1 += rn.y * rn.y;
-        } else {
-          const DiagRow d = diag_row(P, rw);
-          const double z0 = rn.x / (dp0 * d.a + d.b * sk0);
-          const double z1 = rn.y / (dp1 * d.a + d.b * sk1);
-          if (kv0) {
-            acc0 += rn.x * z0;
-            acc1 += rn.x * rn.x;
-          }
-          if (kv1) {
-            acc0 += rn.y * z1;
-            acc1 += rn.y * rn.y;
-          }
-        }
-        if (kv1) {
-          __stcs(reinterpret_cast<double2 *>(A.r_out + o), rn);
-        } else if (kv0) {
-          A.r_out[o] = rn.x;
-        }
-      }
-    }
-    pm = pc;
-    pc = pn;
-  }
-
-  // ---- reductions ----
-  if (PASS_A) {
-    double v[1] = {acc0}, tot[1];
-    if (grid_sum<1>(v, A.partials, &S->counter[0], sred, tot) && threadIdx.x == 0) {
-      if (A.finalize)
-        finalize_alpha(S, tot[0]);
-      else
-        A.local_sum[0] = tot[0];
-    }
-  } else {
-    double v[2] = {acc0, acc1}, tot[2];
-    if (grid_sum<2>(v, A.partials, &S->counter[1], sred, tot) && threadIdx.x == 0) {
-      if (A.finalize) {
-        if (USE_Z) {
-          finalize_rr(S, tot[1], A.hist);  // PC2: rho' comes from the sweeps
-        } else {
-          finalize_beta(S, tot[0], tot[1], A.hist);
-        }
-      } else {
-        A.local_sum[0] = tot[0];
-        A.local_sum[1] = tot[1];
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(NTHREADS, PASS_MINB) k_pass_a_pc1(PassArgs A) { pass_body<true, false>(A); }
-__global__ void __launch_bounds__(NTHREADS, PASS_MINB) k_pass_a_pc2(PassArgs A) { pass_body<true, true>(A); }
-__global__ void __launch_bounds__(NTHREADS, PASS_MINB) k_pass_b_pc1(PassArgs A) { pass_body<false, false>(A); }
-__global__ void __launch_bounds__(NTHREADS, PASS_MINB) k_pass_b_pc2(PassArgs A) { pass_body<false, true>(A); }
 
 // ---------------------------------------------------------------------------
 // Multi-rank scalar finalisation: sum the all-gathered per-rank sums in rank

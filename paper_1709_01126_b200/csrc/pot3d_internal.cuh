@@ -23,11 +23,20 @@
 
 namespace pot3d {
 
-constexpr int TK = 64;        // phi columns per tile (32 lanes x double2)
-constexpr int TJ = 8;         // theta rows per tile (one warp per row)
-constexpr int NTHREADS = TJ * 32;
-constexpr int SROW = TK + 4;  // smem row: [pad][left halo][TK interior][right halo][pad]
-constexpr int SROWS = TJ + 2; // rows j0-1 .. j0+TJ
+// Fused-pass tiling (passes.cu): a block owns TJ interior theta rows x TK phi
+// columns and marches along r; one warp per haloed row (TR = TJ + 2 rows:
+// the rows above/below the tile are loaded and transformed by warps 0 and
+// TR-1), each lane two phi-adjacent cells (128-bit fp64 accesses).
+constexpr int TK = 64;          // phi columns per tile (32 lanes x double2)
+constexpr int TJ = 14;          // interior theta rows per tile
+constexpr int TR = TJ + 2;      // haloed rows = warps per block
+constexpr int NTHREADS = TR * 32;
+constexpr int SROW = TK + 4;    // smem row: [pad][left halo][TK interior][right halo][pad]
+constexpr int NS_A = 4;         // cp.async stages of pass A (3 planes in flight)
+constexpr int NS_B = 5;         // cp.async stages of pass B (3 planes in flight)
+// dynamic shared memory of the passes (bytes)
+constexpr int SMEM_A = (2 * NS_A + 2) * TR * SROW * 8;
+constexpr int SMEM_B = NS_B * (TR * SROW + TJ * TK) * 8;
 
 struct Metrics {
   // r (global index, size nr)
