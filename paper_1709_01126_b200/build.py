@@ -39,16 +39,19 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Build libpot3d.so (or a tuning variant `out` with extra -D `defines`)."""
+    target = LIB if out is None else Path(out)
+    if out is None and not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     inc, libdir = nccl_dirs()
     objs = []
-    tmpdir = PKG / "build"
-    tmpdir.mkdir(exist_ok=True)
+    tmpdir = PKG / "build" / (target.stem if out is not None else "")
+    tmpdir.mkdir(parents=True, exist_ok=True)
     common = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *ARCH,
-              f"-I{inc}", f"-I{ROOT / 'include'}", "-Xptxas", "-v" if verbose else "-O3"]
+              f"-I{inc}", f"-I{ROOT / 'include'}", "-Xptxas", "-v" if verbose else "-O3",
+              *[f"-D{d}" for d in defines]]
     for s in SOURCES:
         o = tmpdir / (Path(s).stem + ".o")
         cmd = [nvcc, *common, "-c", str(CSRC / s), "-o", str(o)]
@@ -59,15 +62,15 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(str(o))
-    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
+    tmp = target.with_suffix(f".so.tmp{os.getpid()}")
     link = [nvcc, "-shared", *ARCH, "-o", str(tmp), *objs, f"-L{libdir}", "-lnccl",
             f"-Xlinker", f"-rpath={libdir}"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link of libpot3d.so failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

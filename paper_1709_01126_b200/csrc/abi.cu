@@ -2,6 +2,8 @@
 // orchestration (CUDA graphs, device-resident scalars, NCCL halo/all-gather),
 // field derivation and diagnostics.  All arithmetic of the method runs in the
 // kernels of kernels.cu / pc2.cu; this file only schedules them.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -53,6 +55,7 @@ struct pot3d_ctx {
   double *local_sum = nullptr, *gathered = nullptr;
   double *poles = nullptr;
   Pc2 *pc2 = nullptr;
+  TMaps tmaps{};
   // graphs
   cudaGraphExec_t gexec = nullptr;
   int graph_unroll = 0;
@@ -163,7 +166,7 @@ int to_device_cells(pot3d_ctx *ctx, const double *user, double *dev_cells_first_
     src = ctx->staging;
   }
   dim3 blk(32, 8), grd((ctx->np + 31) / 32, (ni + 31) / 32, ctx->nt);
-  k_transpose<<<grd, blk, 0, ctx->stream>>>(ni, ctx->nt, ctx->np, stride_i, ctx->G.PK, src,
+  k_transpose<<<grd, blk, 0, ctx->stream>>>(ni, ctx->nt, ctx->np, stride_i, ctx->G.PK, COFF, src,
                                             dev_cells_first_shell, 1);
   CK(cudaGetLastError());
   ctx->n_launch++;
@@ -171,7 +174,7 @@ int to_device_cells(pot3d_ctx *ctx, const double *user, double *dev_cells_first_
 }
 
 int from_device_cells(pot3d_ctx *ctx, const double *dev_first, double *user, int ni, int nj,
-                      long long stride_i) {
+                      long long stride_i, int coff = COFF) {
   const size_t n = (size_t)ni * nj * ctx->np;
   const bool dev = is_device_ptr(user);
   double *dst = user;
@@ -180,7 +183,8 @@ int from_device_cells(pot3d_ctx *ctx, const double *dev_first, double *user, int
     dst = ctx->staging;
   }
   dim3 blk(32, 8), grd((ctx->np + 31) / 32, (ni + 31) / 32, nj);
-  k_transpose<<<grd, blk, 0, ctx->stream>>>(ni, nj, ctx->np, stride_i, ctx->G.PK, dev_first, dst, 0);
+  k_transpose<<<grd, blk, 0, ctx->stream>>>(ni, nj, ctx->np, stride_i, ctx->G.PK, coff, dev_first, dst,
+                                            0);
   CK(cudaGetLastError());
   ctx->n_launch++;
   if (!dev) {
@@ -209,16 +213,57 @@ int halo_exchange(pot3d_ctx *ctx, double *a) {
   const size_t cnt = (size_t)G.plane;
   NK(ncclGroupStart());
   if (ctx->rank > 0) {
-    NK(ncclSend(a + cidx(G, 0, 0, 0), cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
-    NK(ncclRecv(a + cidx(G, -1, 0, 0), cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+    NK(ncclSend(a + sidx(G, 0), cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+    NK(ncclRecv(a + sidx(G, -1), cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
   }
   if (ctx->rank < ctx->nranks - 1) {
-    NK(ncclSend(a + cidx(G, G.nr_loc - 1, 0, 0), cnt, ncclDouble, ctx->rank + 1, ctx->comm,
-                ctx->stream));
-    NK(ncclRecv(a + cidx(G, G.nr_loc, 0, 0), cnt, ncclDouble, ctx->rank + 1, ctx->comm,
-                ctx->stream));
+    NK(ncclSend(a + sidx(G, G.nr_loc - 1), cnt, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
+    NK(ncclRecv(a + sidx(G, G.nr_loc), cnt, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
   }
   NK(ncclGroupEnd());
+  return 0;
+}
+
+// TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry point)
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 3-D view [nr_loc+2 shells][nt rows][PK columns] of a cell array; box {b0, b1, 1}
+int make_map(pot3d_ctx *ctx, CUtensorMap *m, double *base, unsigned b0, unsigned b1) {
+  auto enc = tma_encoder();
+  if (!enc) {
+    ctx->err = "cuTensorMapEncodeTiled unavailable";
+    return POT3D_ERR_CUDA;
+  }
+  const Grid &G = ctx->G;
+  cuuint64_t dims[3] = {(cuuint64_t)G.PK, (cuuint64_t)G.nt, (cuuint64_t)G.nr_loc + 2};
+  cuuint64_t strides[2] = {(cuuint64_t)G.PK * 8, (cuuint64_t)G.plane * 8};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    ctx->err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    return POT3D_ERR_CUDA;
+  }
+  return 0;
+}
+
+int make_maps(pot3d_ctx *ctx) {
+  TRY(make_map(ctx, &ctx->tmaps.src_h, ctx->pc == 2 ? ctx->z : ctx->r, SROW, TR));
+  TRY(make_map(ctx, &ctx->tmaps.p_h[0], ctx->P[0], SROW, TR));
+  TRY(make_map(ctx, &ctx->tmaps.p_h[1], ctx->P[1], SROW, TR));
+  TRY(make_map(ctx, &ctx->tmaps.r_i, ctx->r, TK, TJ));
   return 0;
 }
 
@@ -261,9 +306,9 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
   }
   if (pc2)
-    k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(a);
+    k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, a, parity);
   else
-    k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(a);
+    k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, a, parity);
   CK(cudaGetLastError());
     ctx->n_enq++;
   if (multi) {
@@ -273,9 +318,9 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     ctx->n_enq++;
   }
   if (pc2)
-    k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(a);
+    k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, a, parity);
   else
-    k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(a);
+    k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, a, parity);
   CK(cudaGetLastError());
     ctx->n_enq++;
   if (multi) {
@@ -409,7 +454,7 @@ int pot3d_set_br0(pot3d_ctx *ctx, const double *br0) {
   }
   {
     dim3 blk(32, 8), grd((ctx->np + 31) / 32, (ctx->nt + 31) / 32, 1);
-    k_transpose<<<grd, blk, 0, ctx->stream>>>(ctx->nt, 1, ctx->np, G.PK, G.PK, src, ctx->br_dev, 1);
+    k_transpose<<<grd, blk, 0, ctx->stream>>>(ctx->nt, 1, ctx->np, G.PK, G.PK, COFF, src, ctx->br_dev, 1);
     CK(cudaGetLastError());
     ctx->n_launch++;
   }
@@ -531,7 +576,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   }
   Grid &G = ctx->G;
   G.nr = nr; G.nt = nt; G.np = np;
-  G.PK = round_up(np, 16);
+  G.PK = round_up(np + COFF + 1, 16);  // physical columns: [pad][ghost np-1][0..np-1][ghost 0][pads]
   G.plane = (long long)nt * G.PK;
   G.ntj = (nt + TJ - 1) / TJ;
   G.ntk = (np + TK - 1) / TK;
@@ -552,7 +597,9 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   int rc = 0;
 #define DA(ptr, n) if ((rc = dalloc(ctx, &(ptr), (n)))) return fail(rc)
   DA(ctx->d_rf, nr + 1); DA(ctx->d_tf, nt + 1); DA(ctx->d_pf, np + 1);
-  DA(ctx->m_arp, nr); DA(ctx->m_arm, nr); DA(ctx->m_dr, nr); DA(ctx->m_ss, nr);
+  // r factors carry one padding entry on each side (read for ghost shells)
+  DA(ctx->m_arp, nr + 2); DA(ctx->m_arm, nr + 2); DA(ctx->m_dr, nr + 2); DA(ctx->m_ss, nr + 2);
+  ctx->m_arp += 1; ctx->m_arm += 1; ctx->m_dr += 1; ctx->m_ss += 1;
   DA(ctx->m_rc, nr); DA(ctx->m_drh, nr); DA(ctx->m_vr, nr);
   DA(ctx->m_g, nt); DA(ctx->m_atp, nt); DA(ctx->m_atm, nt); DA(ctx->m_q, nt);
   DA(ctx->m_tc, nt); DA(ctx->m_dth, nt); DA(ctx->m_st, nt);
@@ -578,7 +625,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
   DA(ctx->x, cells); DA(ctx->r, cells); DA(ctx->P[0], cells); DA(ctx->P[1], cells);
   if (pc == POT3D_PC2) DA(ctx->z, cells);
-  DA(ctx->bshell, G.plane); DA(ctx->br_dev, G.plane); DA(ctx->mean2, 2);
+  DA(ctx->bshell, G.plane + 16); DA(ctx->br_dev, G.plane + 16); DA(ctx->mean2, 2);
   DA(ctx->S, 1);
   ctx->partials_len = 4 * (size_t)std::max<long long>(pass_blocks(ctx), 4096);
   DA(ctx->partials, ctx->partials_len);
@@ -589,8 +636,8 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   for (void *p : {(void *)ctx->x, (void *)ctx->r, (void *)ctx->P[0], (void *)ctx->P[1]})
     if (cudaMemsetAsync(p, 0, cells * sizeof(double), ctx->stream)) { ctx->err = "memset"; return fail(POT3D_ERR_CUDA); }
   if (ctx->z) cudaMemsetAsync(ctx->z, 0, cells * sizeof(double), ctx->stream);
-  cudaMemsetAsync(ctx->bshell, 0, G.plane * sizeof(double), ctx->stream);
-  cudaMemsetAsync(ctx->br_dev, 0, G.plane * sizeof(double), ctx->stream);
+  cudaMemsetAsync(ctx->bshell, 0, (G.plane + 16) * sizeof(double), ctx->stream);
+  cudaMemsetAsync(ctx->br_dev, 0, (G.plane + 16) * sizeof(double), ctx->stream);
   cudaMemsetAsync(ctx->S, 0, sizeof(Scalars), ctx->stream);
   if (cudaMallocHost(&ctx->hS, sizeof(Scalars)) != cudaSuccess) { ctx->err = "pinned alloc"; return fail(POT3D_ERR_CUDA); }
 
@@ -632,7 +679,9 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
     if (rc2) return fail(rc2);
   }
   {
-    int rc2 = build_graph(ctx);
+    int rc2 = make_maps(ctx);
+    if (rc2) return fail(rc2);
+    rc2 = build_graph(ctx);
     if (rc2) return fail(rc2);
   }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
@@ -669,9 +718,13 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
   CK(cudaMemsetAsync(ctx->r, 0, cells * sizeof(double), s));
   CK(cudaMemsetAsync(ctx->P[0], 0, cells * sizeof(double), s));
   CK(cudaMemsetAsync(ctx->P[1], 0, cells * sizeof(double), s));
-  if (G.i0 == 0)
-    CK(cudaMemcpyAsync(ctx->r + cidx(G, 0, 0, 0), ctx->bshell, G.plane * sizeof(double),
+  if (G.i0 == 0) {
+    CK(cudaMemcpyAsync(ctx->r + sidx(G, 0), ctx->bshell, G.plane * sizeof(double),
                        cudaMemcpyDeviceToDevice, s));
+    k_fix_ghost_cols<<<(ctx->nt + 255) / 256, 256, 0, s>>>(G, ctx->r, 0, 1);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
   Scalars h0{};
   h0.rtol = rtol;
   h0.maxit = (long long)std::min<int64_t>(maxit, hlen - 1);
@@ -838,20 +891,20 @@ int pot3d_field(pot3d_ctx *ctx, double *br, double *bt, double *bp) {
     k_field_r<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(F);
     CK(cudaGetLastError());
     ctx->n_launch++;
-    TRY(from_device_cells(ctx, Br, br, nbr, ctx->nt, G.plane));
+    TRY(from_device_cells(ctx, Br, br, nbr, ctx->nt, G.plane, 0));
   }
   if (bt) {
     long long n = (long long)G.nr_loc * ntf * ctx->np;
     k_field_t<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(F);
     CK(cudaGetLastError());
     ctx->n_launch++;
-    TRY(from_device_cells(ctx, Bt, bt, G.nr_loc, ntf, (long long)ntf * G.PK));
+    TRY(from_device_cells(ctx, Bt, bt, G.nr_loc, ntf, (long long)ntf * G.PK, 0));
   }
   if (bp) {
     k_field_p<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(F);
     CK(cudaGetLastError());
     ctx->n_launch++;
-    TRY(from_device_cells(ctx, Bp, bp, G.nr_loc, ctx->nt, G.plane));
+    TRY(from_device_cells(ctx, Bp, bp, G.nr_loc, ctx->nt, G.plane, 0));
   }
   CK(cudaStreamSynchronize(s));
   // the Krylov buffers were reused: a later field call needs a new solve's x only
@@ -930,14 +983,15 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
   const bool pc2 = ctx->pc == 2;
   dim3 grd(G.ntj * G.ntk, G.nchunks);
   for (int it = 0; it < iters; it++) {
-    PassArgs a = make_args(ctx, (int)((h.iter + it) & 1));
+    const int par = (int)((h.iter + it) & 1);
+    PassArgs a = make_args(ctx, par);
     a.hist = nullptr;
     a.finalize = 1;
     CK(cudaEventRecord(ev[0], s));
-    if (pc2) k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, s>>>(a); else k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, s>>>(a);
+    if (pc2) k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, s>>>(ctx->tmaps, a, par); else k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, s>>>(ctx->tmaps, a, par);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev[1], s));
-    if (pc2) k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, s>>>(a); else k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, s>>>(a);
+    if (pc2) k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, s>>>(ctx->tmaps, a, par); else k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, s>>>(ctx->tmaps, a, par);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev[2], s));
     ctx->n_launch += 2;

@@ -23,9 +23,6 @@
 #include "device_common.cuh"
 
 namespace pot3d {
-#ifndef PASS_MINB
-#define PASS_MINB 2
-#endif
 
 // ---------------------------------------------------------------------------
 // a1: metric factors.  One thread per entry; faces are device arrays.
@@ -59,6 +56,15 @@ __global__ void k_metrics(int nr, int nt, int np, int bc, const double *rf, cons
     }
     // source surface: odd ghost through Phi=0 on the r1 face (A7)
     ss[i] = (i == nr - 1 && bc == 0) ? 2.0 * rf[nr] * rf[nr] / (rf[nr] - rf[nr - 1]) : 0.0;
+  }
+  if (t == 0) {
+    // padding entries read for ghost shells (results discarded): finite values
+    for (int i : {-1, nr}) {
+      arp[i] = 1.0;
+      arm[i] = 1.0;
+      dr[i] = 1.0;
+      ss[i] = 0.0;
+    }
   }
   if (t < nt) {
     int j = t;
@@ -154,7 +160,10 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
       const DiagRow d = diag_row(P, R);
       zv = src[o] / (__ldg(M.dp + k) * d.a + d.b * (__ldg(M.app + k) + __ldg(M.apm + k)));
     }
-    p_new[o] = (mode < 0) ? zv : zv + beta * p_old[o];
+    const double v = (mode < 0) ? zv : zv + beta * p_old[o];
+    p_new[o] = v;
+    if (k == 0) p_new[o + G.np] = v;           // periodic ghost columns
+    if (k == G.np - 1) p_new[o - G.np] = v;
   }
 }
 
@@ -254,7 +263,7 @@ __global__ void k_apply(Grid G, Metrics M, const double *x, double *y, const dou
                       P.dr * (R.atp * (c0 - xjp) + R.atm * (c0 - xjm))) +
                P.dr * R.q * (appk * (c0 - xkp) + apmk * (c0 - xkm));
     if (bshell) {
-      double bv = (il == b_il) ? bshell[(long long)j * G.PK + k] : 0.0;
+      double bv = (il == b_il) ? bshell[pidx(G, j, k)] : 0.0;
       q = bv - q;
       acc += q * q;
     }
@@ -279,7 +288,7 @@ __global__ void k_br_mean(Grid G, Metrics M, const double *br, double *out2) {
   for (long long c = threadIdx.x; c < (long long)G.nt * G.np; c += blockDim.x) {
     int k = (int)(c % G.np), j = (int)(c / G.np);
     double wgt = __ldg(M.g + j) * __ldg(M.dp + k);
-    a0 += wgt * br[(long long)j * G.PK + k];
+    a0 += wgt * br[pidx(G, j, k)];
     a1 += wgt;
   }
   double v[2] = {a0, a1};
@@ -296,7 +305,7 @@ __global__ void k_rhs(Grid G, Metrics M, double r0, const double *br, const doub
   if (c >= (long long)G.nt * G.np) return;
   int k = (int)(c % G.np), j = (int)(c / G.np);
   double mean = mean2 ? mean2[0] / mean2[1] : 0.0;
-  long long o = (long long)j * G.PK + k;
+  long long o = pidx(G, j, k);
   bshell[o] = -r0 * r0 * __ldg(M.g + j) * __ldg(M.dp + k) * (br[o] - mean);
 }
 
@@ -359,8 +368,8 @@ __global__ void k_gauge_shift(Grid G, double *x, const double *gathered, int nra
 // the device layout d[i*stride_i + j*PK + k] (phi fastest), tiled 32x32 over
 // (i, k) at fixed j.  to_dev: user -> device.
 // ---------------------------------------------------------------------------
-__global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, const double *src,
-                            double *dst, int to_dev) {
+__global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, int coff,
+                            const double *src, double *dst, int to_dev) {
   __shared__ double tile[32][33];
   const int j = blockIdx.z;
   const int i_b = blockIdx.y * 32, k_b = blockIdx.x * 32;
@@ -374,12 +383,12 @@ __global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, 
     __syncthreads();
     for (int ii = ty; ii < 32; ii += 8) {
       int i = i_b + ii, k = k_b + tx;
-      if (k < np && i < ni) dst[i * stride_i + (long long)j * PK + k] = tile[tx][ii];
+      if (k < np && i < ni) dst[i * stride_i + (long long)j * PK + k + coff] = tile[tx][ii];
     }
   } else {
     for (int ii = ty; ii < 32; ii += 8) {
       int i = i_b + ii, k = k_b + tx;
-      if (k < np && i < ni) tile[tx][ii] = src[i * stride_i + (long long)j * PK + k];
+      if (k < np && i < ni) tile[tx][ii] = src[i * stride_i + (long long)j * PK + k + coff];
     }
     __syncthreads();
     for (int kk = ty; kk < 32; kk += 8) {
@@ -408,7 +417,7 @@ __global__ void k_field_r(FieldArgs F) {
     // ghost x(1) = x(2) - vmask*br0*dr1, vmask = 1 (A6)
     double mean = F.mean2 ? F.mean2[0] / F.mean2[1] : 0.0;
     double x0 = F.x[cidx(G, 0, j, k)];
-    double ghost = x0 - (F.br[(long long)j * G.PK + k] - mean) * F.dr[0];
+    double ghost = x0 - (F.br[pidx(G, j, k)] - mean) * F.dr[0];
     v = (x0 - ghost) / F.dr[0];
   } else if (I == G.nr) {
     double xl = F.x[cidx(G, fl - 1, j, k)];
@@ -466,7 +475,7 @@ __global__ void k_field_p(FieldArgs F) {
   int kp = (k == G.np - 1) ? 0 : k + 1;
   double v = (F.x[cidx(G, il, j, kp)] - F.x[cidx(G, il, j, k)]) /
              (F.rc[G.i0 + il] * F.st[j] * F.dph[k]);
-  F.Bp[cidx(G, il, j, k) - G.plane] = v;
+  F.Bp[(long long)il * G.plane + (long long)j * G.PK + k] = v;
 }
 
 }  // namespace pot3d

@@ -18,6 +18,7 @@
 // A6), atm[j] = atp[j-1] (0 at the poles, A5), apm[k] = app[k-1] (periodic).
 // (A p)_m = sum_f A_f (p_m - p_nbr) + S_m p_m,  diag_m = sum_f A_f + S_m.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,16 +28,28 @@ namespace pot3d {
 // columns and marches along r; one warp per haloed row (TR = TJ + 2 rows:
 // the rows above/below the tile are loaded and transformed by warps 0 and
 // TR-1), each lane two phi-adjacent cells (128-bit fp64 accesses).
+#ifndef POT3D_NS_A
+#define POT3D_NS_A 3
+#endif
+#ifndef POT3D_NS_B
+#define POT3D_NS_B 4
+#endif
+#ifndef POT3D_MINB
+#define POT3D_MINB 3
+#endif
 constexpr int TK = 64;          // phi columns per tile (32 lanes x double2)
 constexpr int TJ = 14;          // interior theta rows per tile
-constexpr int TR = TJ + 2;      // haloed rows = warps per block
-constexpr int NTHREADS = TR * 32;
+constexpr int TR = TJ + 2;      // haloed rows
+constexpr int RPW = 2;          // haloed rows per warp (each lane: 2 rows x 2 phi cells)
+constexpr int NWARPS = TR / RPW;
+constexpr int NTHREADS = NWARPS * 32;
 constexpr int SROW = TK + 4;    // smem row: [pad][left halo][TK interior][right halo][pad]
-constexpr int NS_A = 4;         // cp.async stages of pass A (3 planes in flight)
-constexpr int NS_B = 5;         // cp.async stages of pass B (3 planes in flight)
+constexpr int NS_A = POT3D_NS_A; // cp.async stages of pass A (NS_A-1 planes in flight)
+constexpr int NS_B = POT3D_NS_B; // cp.async stages of pass B (NS_B-2 planes in flight)
+constexpr int PASS_MINB = POT3D_MINB;  // resident blocks per SM the passes are compiled for
 // dynamic shared memory of the passes (bytes)
-constexpr int SMEM_A = (2 * NS_A + 2) * TR * SROW * 8;
-constexpr int SMEM_B = NS_B * (TR * SROW + TJ * TK) * 8;
+constexpr int SMEM_A = (2 * NS_A + 2) * TR * SROW * 8 + 128;  // + mbarriers
+constexpr int SMEM_B = NS_B * (TR * SROW + TJ * TK) * 8 + 128;
 
 struct Metrics {
   // r (global index, size nr)
@@ -74,10 +87,28 @@ struct Grid {
   int ntj, ntk;       // tiles
 };
 
-// Cell (il, j, k) of an array with ghost shells.
+// Physical column of logical phi index k: two leading columns, the second of
+// which (physical 1) is the periodic ghost copy of k = np-1; physical np+2 is
+// the ghost copy of k = 0.  The ghost columns let a TMA box cover the
+// wrap neighbours of every tile; every writer of a stencil operand keeps them.
+constexpr int COFF = 2;
+// Cell (il, j, k) of an array with ghost shells (il in [-1, nr_loc]).
 __host__ __device__ inline long long cidx(const Grid &g, int il, int j, int k) {
-  return (long long)(il + 1) * g.plane + (long long)j * g.PK + k;
+  return (long long)(il + 1) * g.plane + (long long)j * g.PK + k + COFF;
 }
+// Start of shell il (whole theta-phi plane incl. pads and ghost columns).
+__host__ __device__ inline long long sidx(const Grid &g, int il) { return (long long)(il + 1) * g.plane; }
+// (j, k) of a single-plane buffer (bshell, br) with the same row layout.
+__host__ __device__ inline long long pidx(const Grid &g, int j, int k) {
+  return (long long)j * g.PK + k + COFF;
+}
+
+// TMA descriptors of the cell arrays (host-encoded, passed __grid_constant__).
+struct TMaps {
+  CUtensorMap src_h;    // pass A source: r (PC1) or z (PC2), haloed box {SROW, TR, 1}
+  CUtensorMap p_h[2];   // P[0], P[1], haloed box
+  CUtensorMap r_i;      // r, interior box {TK, TJ, 1}
+};
 
 
 // Arguments of the fused passes (kernels.cu, k_pass<PASS_A, USE_Z>).
@@ -116,10 +147,13 @@ __global__ void k_metrics(int nr, int nt, int np, int bc, const double *rf, cons
                           double *g, double *atp, double *atm, double *q, double *dp, double *app,
                           double *apm, double *rc, double *drh, double *tc, double *dth,
                           double *st, double *dph, double *vr);
-__global__ void k_pass_a_pc1(PassArgs A);  // a3, z = D^-1 r on the fly
-__global__ void k_pass_a_pc2(PassArgs A);  // a3, z from the PC2 sweeps
-__global__ void k_pass_b_pc1(PassArgs A);  // a7 + a8
-__global__ void k_pass_b_pc2(PassArgs A);  // a7 (||r|| only)
+// parity: P[parity] is p_{k-1}, P[parity^1] receives p_k
+__global__ void k_pass_a_pc1(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a3 (+a8)
+__global__ void k_pass_a_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a3
+__global__ void k_pass_b_pc1(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a7 + a8
+__global__ void k_pass_b_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a7
+// ghost columns (physical 1 and np+2) of shells [il0, il0 + n) from the interior
+__global__ void k_fix_ghost_cols(Grid G, double *a, int il0, int n);
 __global__ void k_finalize_alpha(Scalars *S, const double *gathered, int nranks);
 __global__ void k_finalize_beta(Scalars *S, const double *gathered, int nranks, double *hist);
 __global__ void k_finalize_rr(Scalars *S, const double *gathered, int nranks, double *hist);
@@ -136,8 +170,8 @@ __global__ void k_axpy_cells(Grid G, double *x, const double *p, const Scalars *
 __global__ void k_gauge_sums(Grid G, Metrics M, const double *vr, const double *x, Scalars *S,
                              double *partials, double *local_sum);
 __global__ void k_gauge_shift(Grid G, double *x, const double *gathered, int nranks);
-__global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, const double *src,
-                            double *dst, int to_dev);
+__global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, int coff,
+                            const double *src, double *dst, int to_dev);
 __global__ void k_field_r(FieldArgs F);
 __global__ void k_field_t(FieldArgs F);
 __global__ void k_field_p(FieldArgs F);

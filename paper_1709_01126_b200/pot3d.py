@@ -82,9 +82,10 @@ def library(build_if_missing: bool = True):
         except Exception:
             if not _build.LIB.exists():
                 raise
-    if not _build.LIB.exists():
-        raise ImportError(f"{_build.LIB} is missing: run __graft_entry__.build()")
-    L = ctypes.CDLL(str(_build.LIB))
+    path = os.environ.get("POT3D_LIB") or str(_build.LIB)  # POT3D_LIB: tuning variants only
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run __graft_entry__.build()")
+    L = ctypes.CDLL(path)
     vp, d, i64 = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)
     L.pot3d_setup.argtypes = [ctypes.POINTER(_Grid), vp, ctypes.c_int32, ctypes.c_int32,
                               ctypes.POINTER(_Runtime), ctypes.POINTER(vp)]
