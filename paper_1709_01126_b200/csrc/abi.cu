@@ -264,6 +264,7 @@ int make_maps(pot3d_ctx *ctx) {
   TRY(make_map(ctx, &ctx->tmaps.p_h[0], ctx->P[0], SROW, TR));
   TRY(make_map(ctx, &ctx->tmaps.p_h[1], ctx->P[1], SROW, TR));
   TRY(make_map(ctx, &ctx->tmaps.r_i, ctx->r, TK, TJ));
+  TRY(make_map(ctx, &ctx->tmaps.x_i, ctx->x, TK, TJ));
   return 0;
 }
 
@@ -432,7 +433,7 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   if (ctx->nranks > 1) k += 3;
   if (ctx->pc == 2 && ctx->pc2) k += pc2_kernels_per_apply(ctx->pc2);
   info->graph_kernels_per_iter = k;
-  // algorithmic bytes: PC1 64 B/cell, PC2 pass A 40 + pass B 24 + sweeps
+  // algorithmic bytes: PC1 64 B/cell (pass A 24 + pass B 40), PC2 + 56 B sweeps
   const int64_t cells = (int64_t)ctx->G.nr_loc * ctx->nt * ctx->np;
   info->bytes_per_iter = (ctx->pc == 2 ? 120 : 64) * cells;
   info->device_bytes = (int64_t)ctx->dev_bytes;
@@ -799,12 +800,7 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
     ctx->err = "loop ended without the stop flag";
     return POT3D_ERR_STATE;
   }
-  // finish (a11): x += alpha_last p_last
-  if (hs.iter > 0) {
-    k_axpy_cells<<<148 * 8, 256, 0, s>>>(G, ctx->x, ctx->P[hs.iter & 1], ctx->S);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
-  }
+  // (x is current: pass B applies x += alpha p_k in the same sweep as r -= alpha q)
   // closed wall: zero volume-weighted-mean gauge (A8)
   if (ctx->bc == POT3D_CLOSED_WALL && hs.bnorm > 0) {
     k_gauge_sums<<<nbi, 256, 0, s>>>(G, ctx->M, ctx->m_vr, ctx->x, ctx->S, ctx->partials,

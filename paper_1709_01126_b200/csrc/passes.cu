@@ -3,10 +3,10 @@
 //
 //   pass A (k_pass_a_*):  p_k = z + beta p_{k-1}  (PC1: z = D^-1 r on the fly)
 //                          q   = A p_k            (7-point flux form, A1-A7)
-//                          sigma_partial = p_k . q
-//                          x  += alpha_{k-1} p_{k-1}   (lazy x update)
+//                          sigma_partial = p_k . q                     [24 B/cell]
 //   pass B (k_pass_b_*):  q = A p_k (recomputed: cheaper than storing q)
-//                          r -= alpha q;  PC1: z = D^-1 r, partials r.z, r.r
+//                          x += alpha p_k;  r -= alpha q
+//                          PC1: z = D^-1 r, partials r.z, r.r  [40 B/cell]
 //
 // Both march along r through a TJ x TK theta-phi tile (2.5-D blocking).  For
 // every plane one elected thread loads the haloed box (TR rows x SROW columns,
@@ -31,6 +31,7 @@ struct SmemA {
 struct SmemB {
   double pn[NS_B][TR][SROW];  // staged p_k
   double r[NS_B][TJ][TK];     // staged r (interior rows)
+  double x[NS_B][TJ][TK];     // staged x (interior rows)
   uint64_t bar[NS_B];
 };
 static_assert(sizeof(SmemA) <= SMEM_A, "SMEM_A");
@@ -189,7 +190,6 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   load_tile_const(tcs, G, M, t.j0, t.k0);
   const int cs = 2 + 2 * t.lane;  // smem column slot of element 0
   const double beta = S->beta;
-  const double alpha_prev = S->alpha_prev;
   const long long PL = G.plane;
   const void *map_src = &T.src_h;
   const void *map_old = &T.p_h[parity];
@@ -219,14 +219,10 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     for (int s = 0; s < NS_A - 1; s++) issue();
 
   const double2 Z2 = make_double2(0.0, 0.0);
-  double2 pm[RPW], pc[RPW], pn[RPW], xnext[RPW];
+  double2 pm[RPW], pc[RPW], pn[RPW];
 #pragma unroll
-  for (int e = 0; e < RPW; e++) pm[e] = pc[e] = pn[e] = xnext[e] = Z2;
-  double *g_x = A.x + (long long)(t.c0 + 1) * PL;   // + rowoff[e]: x at plane c0
-  double *g_pn = A.p_new + (long long)(t.c0 + 1) * PL;
-#pragma unroll
-  for (int e = 0; e < RPW; e++)
-    if (t.stencil[e] && t.kv0 && L > 0) xnext[e] = *reinterpret_cast<const double2 *>(g_x + t.rowoff[e]);
+  for (int e = 0; e < RPW; e++) pm[e] = pc[e] = pn[e] = Z2;
+  double *g_pn = A.p_new + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: p_k at plane c0
   const double m0 = t.kv0 ? 1.0 : 0.0, m1 = t.kv1 ? 1.0 : 0.0;
   PlanePtr pp = plane_ptr(M, G.i0 + t.c0 - 1);  // metrics of the transformed plane
   PlanePtr ps = plane_ptr(M, G.i0 + t.c0);      // metrics of the stencil plane
@@ -278,17 +274,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
         sm.pn[sl][r][hs] = v;
       }
       *reinterpret_cast<double2 *>(&sm.pn[sl][r][cs]) = pn[e];
-      if (own && t.stencil[e]) {
-        double2 xv = xnext[e];
-        if (q < L && t.kv0) xnext[e] = *reinterpret_cast<const double2 *>(g_x + PL + t.rowoff[e]);
-        xv.x = fma(alpha_prev, pv.x, xv.x);
-        xv.y = fma(alpha_prev, pv.y, xv.y);
-        store_pair(g_pn + t.rowoff[e], t, G.np, pn[e], false);
-        if (t.kv1)
-          __stcs(reinterpret_cast<double2 *>(g_x + t.rowoff[e]), xv);
-        else if (t.kv0)
-          g_x[t.rowoff[e]] = xv.x;
-      }
+      if (own && t.stencil[e]) store_pair(g_pn + t.rowoff[e], t, G.np, pn[e], false);
     }
     // ---- stencil of plane il-1 (its slot was completed before this barrier) ----
     if (q >= 2) {
@@ -311,10 +297,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
       ps.next();
     }
     pp.next();
-    if (own) {
-      g_x += PL;
-      g_pn += PL;
-    }
+    if (own) g_pn += PL;
 #pragma unroll
     for (int e = 0; e < RPW; e++) {
       pm[e] = pc[e];
@@ -355,6 +338,7 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   const long long PL = G.plane;
   const void *map_p = &T.p_h[parity ^ 1];
   const void *map_r = &T.r_i;
+  const void *map_x = &T.x_i;
   constexpr unsigned PB = TR * SROW * 8u, RB = TJ * TK * 8u;
 
   int qi = 0, si = 0;
@@ -362,9 +346,12 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
     if (qi <= L + 1) {
       const int il = t.c0 - 1 + qi;
       const bool rown = (qi >= 1) && (qi <= L);
-      mbar_arrive_expect_tx(&sm.bar[si], rown ? PB + RB : PB);
+      mbar_arrive_expect_tx(&sm.bar[si], rown ? PB + 2 * RB : PB);
       tma_load_3d(&sm.pn[si][0][0], map_p, &sm.bar[si], t.k0, t.j0 - 1, il + 1);
-      if (rown) tma_load_3d(&sm.r[si][0][0], map_r, &sm.bar[si], t.k0 + COFF, t.j0, il + 1);
+      if (rown) {
+        tma_load_3d(&sm.r[si][0][0], map_r, &sm.bar[si], t.k0 + COFF, t.j0, il + 1);
+        tma_load_3d(&sm.x[si][0][0], map_x, &sm.bar[si], t.k0 + COFF, t.j0, il + 1);
+      }
     }
     ++qi;
     si = wrap_inc(si, NS_B);
@@ -384,6 +371,7 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   double acc_rz = 0.0, acc_rr = 0.0;
   const double m0 = t.kv0 ? 1.0 : 0.0, m1 = t.kv1 ? 1.0 : 0.0;
   double *g_w = A.r_out + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: r of plane c0
+  double *g_x = A.x + (long long)(t.c0 + 1) * PL;      // + rowoff[e]: x of plane c0
   PlanePtr ps = plane_ptr(M, G.i0 + t.c0);             // metrics of the stencil plane
   int st = 0, so = NS_B - 1;                           // stages of planes q and q-1
   unsigned ph = 0;
@@ -430,9 +418,16 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
           acc_rr = fma(m1 * rn.y, rn.y, acc_rr);
         }
         store_pair(g_w + t.rowoff[e], t, G.np, rn, true);
+        const double2 xv = *reinterpret_cast<const double2 *>(&sm.x[so][r - 1][2 * t.lane]);
+        const double2 xn = make_double2(fma(alpha, pc[e].x, xv.x), fma(alpha, pc[e].y, xv.y));
+        if (t.kv1)
+          __stcs(reinterpret_cast<double2 *>(g_x + t.rowoff[e]), xn);
+        else if (t.kv0)
+          g_x[t.rowoff[e]] = xn.x;
       }
       ps.next();
       g_w += PL;
+      g_x += PL;
     }
 #pragma unroll
     for (int e = 0; e < RPW; e++) {

@@ -35,7 +35,7 @@ namespace pot3d {
 #define POT3D_NS_B 4
 #endif
 #ifndef POT3D_MINB
-#define POT3D_MINB 3
+#define POT3D_MINB 2
 #endif
 constexpr int TK = 64;          // phi columns per tile (32 lanes x double2)
 constexpr int TJ = 14;          // interior theta rows per tile
@@ -49,7 +49,7 @@ constexpr int NS_B = POT3D_NS_B; // cp.async stages of pass B (NS_B-2 planes in 
 constexpr int PASS_MINB = POT3D_MINB;  // resident blocks per SM the passes are compiled for
 // dynamic shared memory of the passes (bytes)
 constexpr int SMEM_A = (2 * NS_A + 2) * TR * SROW * 8 + 128;  // + mbarriers
-constexpr int SMEM_B = NS_B * (TR * SROW + TJ * TK) * 8 + 128;
+constexpr int SMEM_B = NS_B * (TR * SROW + 2 * TJ * TK) * 8 + 128;
 
 struct Metrics {
   // r (global index, size nr)
@@ -108,6 +108,7 @@ struct TMaps {
   CUtensorMap src_h;    // pass A source: r (PC1) or z (PC2), haloed box {SROW, TR, 1}
   CUtensorMap p_h[2];   // P[0], P[1], haloed box
   CUtensorMap r_i;      // r, interior box {TK, TJ, 1}
+  CUtensorMap x_i;      // x, interior box {TK, TJ, 1}
 };
 
 

@@ -14,6 +14,6 @@ with Pot3d(rf, tf, pf, c.br0()) as s:
     s.solve(rtol=0.0, maxit=40, true_residual=False)
     a, b, p = s.profile(40)
     n = c.n
-    print(f"pass A {a*1e3:.1f} us {40*n/a/1e6:.0f} GB/s | pass B {b*1e3:.1f} us {24*n/b/1e6:.0f} GB/s | loop {64*n/(a+b)/1e6:.0f} GB/s chunks={s.info()}")
+    print(f"pass A {a*1e3:.1f} us {24*n/a/1e6:.0f} GB/s | pass B {b*1e3:.1f} us {40*n/b/1e6:.0f} GB/s | loop {64*n/(a+b)/1e6:.0f} GB/s chunks={s.info()}")
 PY
 done
