@@ -263,8 +263,8 @@ int make_maps(pot3d_ctx *ctx) {
   TRY(make_map(ctx, &ctx->tmaps.src_h, ctx->pc == 2 ? ctx->z : ctx->r, SROW, TR));
   TRY(make_map(ctx, &ctx->tmaps.p_h[0], ctx->P[0], SROW, TR));
   TRY(make_map(ctx, &ctx->tmaps.p_h[1], ctx->P[1], SROW, TR));
-  TRY(make_map(ctx, &ctx->tmaps.r_i, ctx->r, TK, TJ));
-  TRY(make_map(ctx, &ctx->tmaps.x_i, ctx->x, TK, TJ));
+  TRY(make_map(ctx, &ctx->tmaps.r_i, ctx->r, TKB, TJ));
+  TRY(make_map(ctx, &ctx->tmaps.x_i, ctx->x, TKB, TJ));
   return 0;
 }
 
@@ -577,7 +577,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   }
   Grid &G = ctx->G;
   G.nr = nr; G.nt = nt; G.np = np;
-  G.PK = round_up(np + COFF + 1, 16);  // physical columns: [pad][ghost np-1][0..np-1][ghost 0][pads]
+  G.PK = round_up(np + COFF + 1, 16);  // physical columns: [ghost np-1][0..np-1][ghost 0][pads]
   G.plane = (long long)nt * G.PK;
   G.ntj = (nt + TJ - 1) / TJ;
   G.ntk = (np + TK - 1) / TK;

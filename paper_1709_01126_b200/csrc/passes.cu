@@ -9,35 +9,41 @@
 //                          PC1: z = D^-1 r, partials r.z, r.r  [40 B/cell]
 //
 // Both march along r through a TJ x TK theta-phi tile (2.5-D blocking).  For
-// every plane one elected thread loads the haloed box (TR rows x SROW columns,
-// i.e. one halo row above/below and the halo columns left/right -- the
-// periodic wrap neighbours come with the physical ghost columns) with a TMA
-// tensor copy (cp.async.bulk.tensor) into an NS-stage shared ring completed on
-// an mbarrier; rows outside the grid are zero-filled by the TMA unit.  Each
-// lane owns RPW rows x 2 phi-adjacent cells.  Pass A turns each staged plane
-// into p_k in a 2-slot shared ring; the r neighbours of a cell stay in its
-// thread's registers.  One __syncthreads per plane (it also frees the stage
-// the producer refills).  Per-block partials are reduced deterministically.
+// every plane one elected thread loads the haloed box (TR rows x SROW columns:
+// one halo row above/below, the halo columns left/right -- the periodic wrap
+// neighbours come with the physical ghost columns) with a TMA tensor copy
+// (cp.async.bulk.tensor) into a shared ring completed on an mbarrier; rows
+// outside the grid are zero-filled by the TMA unit.  Lane l of a warp owns the
+// logical columns k0-1+2l and k0+2l of RPW rows, so the halo columns are
+// ordinary lane work (lanes 0 and 31) and every shared/global access is
+// 128-bit.  Pass A turns each staged plane into p_k in a 3-slot shared ring
+// and is unrolled by 3 so stage, slot and register roles are compile-time;
+// the r neighbours of a cell stay in its thread's registers.  One
+// __syncthreads per plane.  Per-block partials are reduced deterministically.
+#include <type_traits>
+
 #include "device_common.cuh"
 
 namespace pot3d {
 
+static_assert(NS_A == 3, "pass A is unrolled by its stage count");
+
 struct SmemA {
   double r[NS_A][TR][SROW];   // staged r (PC1) / z (PC2) / final p on ghost shells
   double p[NS_A][TR][SROW];   // staged p_{k-1}
-  double pn[2][TR][SROW];     // p_k of the current / next plane
+  double pn[3][TR][SROW];     // p_k ring
   uint64_t bar[NS_A];
 };
 struct SmemB {
   double pn[NS_B][TR][SROW];  // staged p_k
-  double r[NS_B][TJ][TK];     // staged r (interior rows)
-  double x[NS_B][TJ][TK];     // staged x (interior rows)
+  double r[NS_B][TJ][TKB];    // staged r (interior rows)
+  double x[NS_B][TJ][TKB];    // staged x (interior rows)
   uint64_t bar[NS_B];
 };
 static_assert(sizeof(SmemA) <= SMEM_A, "SMEM_A");
 static_assert(sizeof(SmemB) <= SMEM_B, "SMEM_B");
-static_assert((TR * SROW * 8) % 128 == 0 && (TJ * TK * 8) % 128 == 0, "TMA boxes 128-B aligned");
-static_assert(TR % RPW == 0, "rows per warp");
+static_assert((TR * SROW * 8) % 128 == 0 && (TJ * TKB * 8) % 128 == 0, "TMA boxes 128-B aligned");
+static_assert(TR % RPW == 0 && TKB == 2 * 32 && TK == TKB - 2, "tile geometry");
 
 __device__ __forceinline__ void chunk_bounds(const Grid &G, int c, int &c0, int &c1) {
   int base = G.nr_loc / G.nchunks, rem = G.nr_loc % G.nchunks;
@@ -45,40 +51,22 @@ __device__ __forceinline__ void chunk_bounds(const Grid &G, int c, int &c0, int 
   c1 = c0 + base + (c < rem ? 1 : 0);
 }
 
-// Metric factors of the tile staged once per block: per smem column slot s
-// (logical column k0-2+s, periodic) dp, app, apm, and per haloed row r
-// (theta row j0-1+r) g, atp, atm, q.
+// Column metric factors of the tile per smem index i (logical column k0-3+i,
+// periodic): dp, app, apm.
 struct TileConst {
   double dp[SROW], app[SROW], apm[SROW];
-  double g[TR], atp[TR], atm[TR], q[TR];
 };
 
 __device__ __forceinline__ void load_tile_const(TileConst &tc, const Grid &G, const Metrics &M,
-                                                int j0, int k0) {
-  for (int s = threadIdx.x; s < SROW; s += blockDim.x) {
-    int k = k0 - 2 + s;
+                                                int k0) {
+  for (int i = threadIdx.x; i < SROW; i += blockDim.x) {
+    int k = k0 - 3 + i;
     k = (k < 0) ? k + G.np : k;
     k = (k >= G.np) ? (k - G.np) % G.np : k;
-    tc.dp[s] = __ldg(M.dp + k);
-    tc.app[s] = __ldg(M.app + k);
-    tc.apm[s] = __ldg(M.apm + k);
+    tc.dp[i] = __ldg(M.dp + k);
+    tc.app[i] = __ldg(M.app + k);
+    tc.apm[i] = __ldg(M.apm + k);
   }
-  for (int r = threadIdx.x; r < TR; r += blockDim.x) {
-    int j = min(max(j0 - 1 + r, 0), G.nt - 1);
-    tc.g[r] = __ldg(M.g + j);
-    tc.atp[r] = __ldg(M.atp + j);
-    tc.atm[r] = __ldg(M.atm + j);
-    tc.q[r] = __ldg(M.q + j);
-  }
-}
-
-__device__ __forceinline__ RowC row_tc(const TileConst &tc, int r) {
-  RowC c;
-  c.g = tc.g[r];
-  c.atp = tc.atp[r];
-  c.atm = tc.atm[r];
-  c.q = tc.q[r];
-  return c;
 }
 
 // Per-plane r metric factors through pointers advanced one shell per plane
@@ -120,12 +108,11 @@ __device__ __forceinline__ double stencil7(double c, double ip, double im, doubl
 struct TileThread {
   int lane, w;
   int j0, k0, c0, c1;
-  int k;
-  bool kv0, kv1;
-  int row[RPW];          // haloed rows w*RPW + e
+  int row[RPW];          // haloed rows w*RPW + e (theta row j0-1+row)
   bool stencil[RPW];     // interior row inside the grid
-  long long rowoff[RPW]; // j*PK + k + COFF (clamped)
-  bool gl0, gr0, gr1;    // element holds logical k = np-1 (left ghost dup) / k = 0 (right ghost dup)
+  long long rowoff[RPW]; // j*PK + (k0-1+2*lane) + COFF, row clamped into the grid
+  bool st0, st1;         // element 0/1 is an interior column of this tile inside the grid
+  bool gr0, gr1, gl0, gl1;  // element 0/1 holds k = 0 (right-ghost dup) / k = np-1 (left ghost)
 };
 
 __device__ __forceinline__ TileThread tile_thread(const Grid &G) {
@@ -136,9 +123,7 @@ __device__ __forceinline__ TileThread tile_thread(const Grid &G) {
   t.j0 = (tile % G.ntj) * TJ;
   t.k0 = (tile / G.ntj) * TK;
   chunk_bounds(G, blockIdx.y, t.c0, t.c1);
-  t.k = t.k0 + 2 * t.lane;
-  t.kv0 = t.k < G.np;
-  t.kv1 = (t.k + 1) < G.np;
+  const int k = t.k0 - 1 + 2 * t.lane;  // logical column of element 0
 #pragma unroll
   for (int e = 0; e < RPW; e++) {
     const int r = RPW * t.w + e;
@@ -146,30 +131,38 @@ __device__ __forceinline__ TileThread tile_thread(const Grid &G) {
     const bool jv = (j >= 0) && (j < G.nt);
     t.row[e] = r;
     t.stencil[e] = (r >= 1) && (r <= TJ) && jv;
-    t.rowoff[e] = (long long)(jv ? j : 0) * G.PK + (t.kv0 ? t.k : 0) + COFF;
+    t.rowoff[e] = (long long)(jv ? j : t.j0) * G.PK + k + COFF;
   }
-  t.gr0 = (t.k == 0);            // element 0 is k = 0: also store at physical np+2
-  t.gl0 = (t.k == G.np - 1);     // element 0 is k = np-1: also store at physical 1
-  t.gr1 = (t.k + 1 == G.np - 1); // element 1 is k = np-1
+  t.st0 = (t.lane > 0) && (k < G.np);
+  t.st1 = (t.lane < 31) && (k + 1 < G.np);
+  t.gr0 = t.st0 && (k == 0);
+  t.gr1 = t.st1 && (k + 1 == 0);
+  t.gl0 = t.st0 && (k == G.np - 1);
+  t.gl1 = t.st1 && (k + 1 == G.np - 1);
   return t;
 }
 
-// stores of a p / r pair with the periodic ghost-column duplicates
+// Store of a lane's column pair (interior elements only) with the periodic
+// ghost-column duplicates; row_k points at the physical column of element 0.
 __device__ __forceinline__ void store_pair(double *row_k, const TileThread &t, int np, double2 v,
                                            bool streaming) {
-  // row_k points at physical column of logical k (element 0)
-  if (t.kv1) {
+  if (t.st0 && t.st1) {
     if (streaming)
       __stcs(reinterpret_cast<double2 *>(row_k), v);
     else
       *reinterpret_cast<double2 *>(row_k) = v;
-  } else if (t.kv0) {
-    row_k[0] = v.x;
+  } else {
+    if (t.st0) row_k[0] = v.x;
+    if (t.st1) row_k[1] = v.y;
   }
-  if (t.gr0) row_k[np] = v.x;                 // logical k=0 -> physical np+2
-  if (t.gl0) row_k[-np] = v.x;                // logical np-1 -> physical 1
-  if (t.gr1) row_k[1 - np] = v.y;             // logical np-1 (element 1) -> physical 1
+  if (t.gr0) row_k[np] = v.x;        // k = 0 (element 0)    -> physical np+1
+  if (t.gr1) row_k[np + 1] = v.y;    // k = 0 (element 1)    -> physical np+1
+  if (t.gl0) row_k[-np] = v.x;       // k = np-1 (element 0) -> physical 0
+  if (t.gl1) row_k[1 - np] = v.y;    // k = np-1 (element 1) -> physical 0
 }
+
+template <int V>
+using IC = std::integral_constant<int, V>;
 
 // ---------------------------------------------------------------------------
 // pass A
@@ -187,124 +180,119 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
 
   const TileThread t = tile_thread(G);
   const int L = t.c1 - t.c0;
-  load_tile_const(tcs, G, M, t.j0, t.k0);
-  const int cs = 2 + 2 * t.lane;  // smem column slot of element 0
+  load_tile_const(tcs, G, M, t.k0);
+  const int cs = 2 + 2 * t.lane;  // smem index of element 0
   const double beta = S->beta;
   const long long PL = G.plane;
   const void *map_src = &T.src_h;
   const void *map_old = &T.p_h[parity];
   const void *map_new = &T.p_h[parity ^ 1];
   constexpr unsigned STAGE_BYTES = 2u * TR * SROW * 8u;
+  RowC rw[RPW];
+#pragma unroll
+  for (int e = 0; e < RPW; e++) rw[e] = row_c(M, min(max(t.j0 - 1 + t.row[e], 0), G.nt - 1));
 
-  // producer (thread 0): plane q (il = c0-1+q) -> stage q % NS_A
-  int qi = 0, si = 0;
-  auto issue = [&]() {
-    if (qi <= L + 1) {
-      const int il = t.c0 - 1 + qi;
+  // producer (thread 0): plane q (il = c0-1+q) -> stage st
+  auto issue = [&](int q, int st) {
+    if (q <= L + 1) {
+      const int il = t.c0 - 1 + q;
       const bool ghost = (il < 0) || (il >= G.nr_loc);  // ghost shells hold the final p_k
-      mbar_arrive_expect_tx(&sm.bar[si], STAGE_BYTES);
-      tma_load_3d(&sm.r[si][0][0], ghost ? map_new : map_src, &sm.bar[si], t.k0, t.j0 - 1, il + 1);
+      mbar_arrive_expect_tx(&sm.bar[st], STAGE_BYTES);
+      tma_load_3d(&sm.r[st][0][0], ghost ? map_new : map_src, &sm.bar[st], t.k0 - 3 + COFF,
+                  t.j0 - 1, il + 1);
       // p_{k-1} on a ghost shell is not used: an out-of-range shell zero-fills the stage
-      tma_load_3d(&sm.p[si][0][0], map_old, &sm.bar[si], t.k0, t.j0 - 1, ghost ? G.nr_loc + 2 : il + 1);
+      tma_load_3d(&sm.p[st][0][0], map_old, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1,
+                  ghost ? G.nr_loc + 2 : il + 1);
     }
-    ++qi;
-    si = wrap_inc(si, NS_A);
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS_A; s++) mbar_init(&sm.bar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0)
-    for (int s = 0; s < NS_A - 1; s++) issue();
+  if (threadIdx.x == 0) {
+    issue(0, 0);
+    issue(1, 1);
+  }
 
   const double2 Z2 = make_double2(0.0, 0.0);
-  double2 pm[RPW], pc[RPW], pn[RPW];
+  double2 R[3][RPW];  // p_k of planes q (R[q%3]), q-1, q-2 of this lane's cells
 #pragma unroll
-  for (int e = 0; e < RPW; e++) pm[e] = pc[e] = pn[e] = Z2;
+  for (int u = 0; u < 3; u++)
+#pragma unroll
+    for (int e = 0; e < RPW; e++) R[u][e] = Z2;
   double *g_pn = A.p_new + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: p_k at plane c0
-  const double m0 = t.kv0 ? 1.0 : 0.0, m1 = t.kv1 ? 1.0 : 0.0;
+  const double m0 = t.st0 ? 1.0 : 0.0, m1 = t.st1 ? 1.0 : 0.0;
   PlanePtr pp = plane_ptr(M, G.i0 + t.c0 - 1);  // metrics of the transformed plane
   PlanePtr ps = plane_ptr(M, G.i0 + t.c0);      // metrics of the stencil plane
-  const bool hl = (t.lane == 0), hr = (t.lane == 31);  // halo-column duty (s = 1 / TK+2)
-  const int hs = hl ? 1 : TK + 2;
   double acc = 0.0;
-  int st = 0;
-  unsigned ph = 0;  // mbarrier parity of stage st
+  unsigned ph = 0;  // mbarrier parity of the current group of 3 planes
 
-#pragma unroll 1
-  for (int q = 0; q <= L + 1; q++) {
-    __syncthreads();  // stage (q-1)%NS_A and slot (q&1) are free
-    if (threadIdx.x == 0) issue();
+  auto step = [&](auto U, int q) {
+    constexpr int u = decltype(U)::value;       // stage, slot and register set of plane q
+    constexpr int um = (u + 2) % 3, umm = (u + 1) % 3;
+    __syncthreads();  // stage um and slot u are free
+    if (threadIdx.x == 0) issue(q + 2, um);
     const int il = t.c0 - 1 + q;
     const bool ghost = (il < 0) || (il >= G.nr_loc);
-    const bool own = (q >= 1) && (q <= L);
-    const int sl = q & 1;
     const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
     const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
     const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
-    const double dph = tcs.dp[hs], sph = tcs.app[hs] + tcs.apm[hs];
-    PlaneC P = pp.get();
-    mbar_wait(&sm.bar[st], ph);
+    const PlaneC P = pp.get();
+    pp.next();
+    mbar_wait(&sm.bar[u], ph);
     // ---- transform plane il -> p_k ----
 #pragma unroll
     for (int e = 0; e < RPW; e++) {
       const int r = t.row[e];
-      const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[st][r][cs]);
-      const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[st][r][cs]);
-      const RowC R = row_tc(tcs, r);
+      const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[u][r][cs]);
+      const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[u][r][cs]);
+      double2 pn;
       if (USE_Z) {
-        pn[e].x = fma(beta, pv.x, rv.x);  // ghost shells: pv = 0 -> pn = rv (final p_k)
-        pn[e].y = fma(beta, pv.y, rv.y);
+        pn.x = fma(beta, pv.x, rv.x);  // ghost shells: pv = 0 -> pn = rv (final p_k)
+        pn.y = fma(beta, pv.y, rv.y);
       } else {
-        const DiagRow d = diag_row(P, R);
-        const double2 t2 = make_double2(fdiv(rv.x, dp.x * d.a + d.b * (ap.x + am.x)) + beta * pv.x,
-                                        fdiv(rv.y, dp.y * d.a + d.b * (ap.y + am.y)) + beta * pv.y);
-        pn[e] = ghost ? rv : t2;
+        const DiagRow d = diag_row(P, rw[e]);
+        pn.x = ghost ? rv.x : fdiv(rv.x, dp.x * d.a + d.b * (ap.x + am.x)) + beta * pv.x;
+        pn.y = ghost ? rv.y : fdiv(rv.y, dp.y * d.a + d.b * (ap.y + am.y)) + beta * pv.y;
       }
-      if (hl || hr) {
-        const double hv = sm.r[st][r][hs], hp = sm.p[st][r][hs];
-        double v;
-        if (USE_Z) {
-          v = fma(beta, hp, hv);
-        } else {
-          const DiagRow d = diag_row(P, R);
-          v = ghost ? hv : fdiv(hv, dph * d.a + d.b * sph) + beta * hp;
-        }
-        sm.pn[sl][r][hs] = v;
-      }
-      *reinterpret_cast<double2 *>(&sm.pn[sl][r][cs]) = pn[e];
-      if (own && t.stencil[e]) store_pair(g_pn + t.rowoff[e], t, G.np, pn[e], false);
+      R[u][e] = pn;
+      *reinterpret_cast<double2 *>(&sm.pn[u][r][cs]) = pn;
+      if (q >= 1 && q <= L && t.stencil[e]) store_pair(g_pn + t.rowoff[e], t, G.np, pn, false);
     }
+    if (q >= 1 && q <= L) g_pn += PL;
     // ---- stencil of plane il-1 (its slot was completed before this barrier) ----
     if (q >= 2) {
       const PlaneC Ps = ps.get();
-      const double *sb = &sm.pn[sl ^ 1][0][0];
+      ps.next();
+      const double *sb = &sm.pn[um][0][0];
 #pragma unroll
       for (int e = 0; e < RPW; e++) {
         if (!t.stencil[e]) continue;
         const int r = t.row[e];
-        const RowC rw = row_tc(tcs, r);
         const double *so = sb + r * SROW + cs;
-        const double2 up = (RPW == 2 && e == 1) ? pc[0] : *reinterpret_cast<const double2 *>(so - SROW);
-        const double2 dn = (RPW == 2 && e == 0) ? pc[RPW - 1] : *reinterpret_cast<const double2 *>(so + SROW);
+        const double2 c = R[um][e];
+        const double2 up = (RPW == 2 && e == 1) ? R[um][0] : *reinterpret_cast<const double2 *>(so - SROW);
+        const double2 dn = (RPW == 2 && e == 0) ? R[um][RPW - 1] : *reinterpret_cast<const double2 *>(so + SROW);
         const double lf = so[-1], rt = so[2];
-        const double q0 = stencil7(pc[e].x, pn[e].x, pm[e].x, dn.x, up.x, pc[e].y, lf, dp.x, ap.x, am.x, Ps, rw);
-        const double q1 = stencil7(pc[e].y, pn[e].y, pm[e].y, dn.y, up.y, rt, pc[e].x, dp.y, ap.y, am.y, Ps, rw);
-        acc = fma(m0 * pc[e].x, q0, acc);
-        acc = fma(m1 * pc[e].y, q1, acc);
+        const double q0 = stencil7(c.x, R[u][e].x, R[umm][e].x, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e]);
+        const double q1 = stencil7(c.y, R[u][e].y, R[umm][e].y, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e]);
+        acc = fma(m0 * c.x, q0, acc);
+        acc = fma(m1 * c.y, q1, acc);
       }
-      ps.next();
     }
-    pp.next();
-    if (own) g_pn += PL;
-#pragma unroll
-    for (int e = 0; e < RPW; e++) {
-      pm[e] = pc[e];
-      pc[e] = pn[e];
-    }
-    st = wrap_inc(st, NS_A);
-    ph ^= (st == 0);
+  };
+
+  const int last = L + 1;
+#pragma unroll 1
+  for (int q = 0;; q += 3) {
+    step(IC<0>{}, q);
+    if (q + 1 > last) break;
+    step(IC<1>{}, q + 1);
+    if (q + 2 > last) break;
+    step(IC<2>{}, q + 2);
+    ph ^= 1u;
+    if (q + 3 > last) break;
   }
 
   double v[1] = {acc}, tot[1];
@@ -332,14 +320,17 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
 
   const TileThread t = tile_thread(G);
   const int L = t.c1 - t.c0;
-  load_tile_const(tcs, G, M, t.j0, t.k0);
+  load_tile_const(tcs, G, M, t.k0);
   const int cs = 2 + 2 * t.lane;
   const double alpha = S->alpha;
   const long long PL = G.plane;
   const void *map_p = &T.p_h[parity ^ 1];
   const void *map_r = &T.r_i;
   const void *map_x = &T.x_i;
-  constexpr unsigned PB = TR * SROW * 8u, RB = TJ * TK * 8u;
+  constexpr unsigned PB = TR * SROW * 8u, RB = TJ * TKB * 8u;
+  RowC rw[RPW];
+#pragma unroll
+  for (int e = 0; e < RPW; e++) rw[e] = row_c(M, min(max(t.j0 - 1 + t.row[e], 0), G.nt - 1));
 
   int qi = 0, si = 0;
   auto issue = [&]() {
@@ -347,10 +338,10 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
       const int il = t.c0 - 1 + qi;
       const bool rown = (qi >= 1) && (qi <= L);
       mbar_arrive_expect_tx(&sm.bar[si], rown ? PB + 2 * RB : PB);
-      tma_load_3d(&sm.pn[si][0][0], map_p, &sm.bar[si], t.k0, t.j0 - 1, il + 1);
+      tma_load_3d(&sm.pn[si][0][0], map_p, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
       if (rown) {
-        tma_load_3d(&sm.r[si][0][0], map_r, &sm.bar[si], t.k0 + COFF, t.j0, il + 1);
-        tma_load_3d(&sm.x[si][0][0], map_x, &sm.bar[si], t.k0 + COFF, t.j0, il + 1);
+        tma_load_3d(&sm.r[si][0][0], map_r, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
+        tma_load_3d(&sm.x[si][0][0], map_x, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
       }
     }
     ++qi;
@@ -369,7 +360,7 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
 #pragma unroll
   for (int e = 0; e < RPW; e++) pm[e] = pc[e] = pn[e] = Z2;
   double acc_rz = 0.0, acc_rr = 0.0;
-  const double m0 = t.kv0 ? 1.0 : 0.0, m1 = t.kv1 ? 1.0 : 0.0;
+  const double m0 = t.st0 ? 1.0 : 0.0, m1 = t.st1 ? 1.0 : 0.0;
   double *g_w = A.r_out + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: r of plane c0
   double *g_x = A.x + (long long)(t.c0 + 1) * PL;      // + rowoff[e]: x of plane c0
   PlanePtr ps = plane_ptr(M, G.i0 + t.c0);             // metrics of the stencil plane
@@ -394,22 +385,24 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
       for (int e = 0; e < RPW; e++) {
         if (!t.stencil[e]) continue;
         const int r = t.row[e];
-        const RowC rw = row_tc(tcs, r);
         const double *sr = sb + r * SROW + cs;
         const double2 up = (RPW == 2 && e == 1) ? pc[0] : *reinterpret_cast<const double2 *>(sr - SROW);
         const double2 dn = (RPW == 2 && e == 0) ? pc[RPW - 1] : *reinterpret_cast<const double2 *>(sr + SROW);
         const double lf = sr[-1], rt = sr[2];
-        const double q0 = stencil7(pc[e].x, pn[e].x, pm[e].x, dn.x, up.x, pc[e].y, lf, dp.x, ap.x, am.x, P, rw);
-        const double q1 = stencil7(pc[e].y, pn[e].y, pm[e].y, dn.y, up.y, rt, pc[e].x, dp.y, ap.y, am.y, P, rw);
+        const double q0 = stencil7(pc[e].x, pn[e].x, pm[e].x, dn.x, up.x, pc[e].y, lf, dp.x, ap.x, am.x, P, rw[e]);
+        const double q1 = stencil7(pc[e].y, pn[e].y, pm[e].y, dn.y, up.y, rt, pc[e].x, dp.y, ap.y, am.y, P, rw[e]);
         const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[so][r - 1][2 * t.lane]);
-        double2 rn;
+        const double2 xv = *reinterpret_cast<const double2 *>(&sm.x[so][r - 1][2 * t.lane]);
+        double2 rn, xn;
         rn.x = fma(-alpha, q0, rv.x);
         rn.y = fma(-alpha, q1, rv.y);
+        xn.x = fma(alpha, pc[e].x, xv.x);
+        xn.y = fma(alpha, pc[e].y, xv.y);
         if (USE_Z) {
           acc_rr = fma(m0 * rn.x, rn.x, acc_rr);
           acc_rr = fma(m1 * rn.y, rn.y, acc_rr);
         } else {
-          const DiagRow d = diag_row(P, rw);
+          const DiagRow d = diag_row(P, rw[e]);
           const double z0 = fdiv(rn.x, dp.x * d.a + d.b * (ap.x + am.x));
           const double z1 = fdiv(rn.y, dp.y * d.a + d.b * (ap.y + am.y));
           acc_rz = fma(m0 * rn.x, z0, acc_rz);
@@ -418,12 +411,12 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
           acc_rr = fma(m1 * rn.y, rn.y, acc_rr);
         }
         store_pair(g_w + t.rowoff[e], t, G.np, rn, true);
-        const double2 xv = *reinterpret_cast<const double2 *>(&sm.x[so][r - 1][2 * t.lane]);
-        const double2 xn = make_double2(fma(alpha, pc[e].x, xv.x), fma(alpha, pc[e].y, xv.y));
-        if (t.kv1)
+        if (t.st0 && t.st1) {
           __stcs(reinterpret_cast<double2 *>(g_x + t.rowoff[e]), xn);
-        else if (t.kv0)
-          g_x[t.rowoff[e]] = xn.x;
+        } else {
+          if (t.st0) g_x[t.rowoff[e]] = xn.x;
+          if (t.st1) g_x[t.rowoff[e] + 1] = xn.y;
+        }
       }
       ps.next();
       g_w += PL;
@@ -462,7 +455,7 @@ __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
     k_pass_b_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_b_body<true>(T, A, parity); }
 
-// ghost columns of shells [il0, il0 + n): physical 1 <- k = np-1, physical np+2 <- k = 0
+// ghost columns of shells [il0, il0 + n): physical 0 <- k = np-1, physical np+1 <- k = 0
 __global__ void k_fix_ghost_cols(Grid G, double *a, int il0, int n) {
   const long long rows = (long long)n * G.nt;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < rows;

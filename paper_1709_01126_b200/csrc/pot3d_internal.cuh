@@ -29,7 +29,7 @@ namespace pot3d {
 // the rows above/below the tile are loaded and transformed by warps 0 and
 // TR-1), each lane two phi-adjacent cells (128-bit fp64 accesses).
 #ifndef POT3D_NS_A
-#define POT3D_NS_A 3
+#define POT3D_NS_A 3            // pass A is unrolled by 3: NS_A must be 3
 #endif
 #ifndef POT3D_NS_B
 #define POT3D_NS_B 4
@@ -37,19 +37,21 @@ namespace pot3d {
 #ifndef POT3D_MINB
 #define POT3D_MINB 2
 #endif
-constexpr int TK = 64;          // phi columns per tile (32 lanes x double2)
+constexpr int TK = 62;          // interior phi columns per tile: lane l owns logical
+                                // columns k0-1+2l, k0+2l (lanes 0/31 hold the halo columns)
 constexpr int TJ = 14;          // interior theta rows per tile
 constexpr int TR = TJ + 2;      // haloed rows
 constexpr int RPW = 2;          // haloed rows per warp (each lane: 2 rows x 2 phi cells)
 constexpr int NWARPS = TR / RPW;
 constexpr int NTHREADS = NWARPS * 32;
-constexpr int SROW = TK + 4;    // smem row: [pad][left halo][TK interior][right halo][pad]
+constexpr int SROW = 68;        // smem row: index i <-> logical column k0-3+i (2..65 used)
+constexpr int TKB = 64;         // width of the interior boxes (r, x): logical k0-1 .. k0+62
 constexpr int NS_A = POT3D_NS_A; // cp.async stages of pass A (NS_A-1 planes in flight)
 constexpr int NS_B = POT3D_NS_B; // cp.async stages of pass B (NS_B-2 planes in flight)
 constexpr int PASS_MINB = POT3D_MINB;  // resident blocks per SM the passes are compiled for
 // dynamic shared memory of the passes (bytes)
-constexpr int SMEM_A = (2 * NS_A + 2) * TR * SROW * 8 + 128;  // + mbarriers
-constexpr int SMEM_B = NS_B * (TR * SROW + 2 * TJ * TK) * 8 + 128;
+constexpr int SMEM_A = (2 * NS_A + 3) * TR * SROW * 8 + 128;  // + mbarriers
+constexpr int SMEM_B = NS_B * (TR * SROW + 2 * TJ * TKB) * 8 + 128;
 
 struct Metrics {
   // r (global index, size nr)
@@ -87,11 +89,11 @@ struct Grid {
   int ntj, ntk;       // tiles
 };
 
-// Physical column of logical phi index k: two leading columns, the second of
-// which (physical 1) is the periodic ghost copy of k = np-1; physical np+2 is
-// the ghost copy of k = 0.  The ghost columns let a TMA box cover the
-// wrap neighbours of every tile; every writer of a stencil operand keeps them.
-constexpr int COFF = 2;
+// Physical column of logical phi index k is k + COFF: physical 0 is the
+// periodic ghost copy of k = np-1 and physical np+1 the ghost copy of k = 0
+// (P:54).  The ghost columns let a TMA box cover the wrap neighbours of every
+// tile; every writer of a stencil operand keeps them.
+constexpr int COFF = 1;
 // Cell (il, j, k) of an array with ghost shells (il in [-1, nr_loc]).
 __host__ __device__ inline long long cidx(const Grid &g, int il, int j, int k) {
   return (long long)(il + 1) * g.plane + (long long)j * g.PK + k + COFF;
@@ -107,8 +109,8 @@ __host__ __device__ inline long long pidx(const Grid &g, int j, int k) {
 struct TMaps {
   CUtensorMap src_h;    // pass A source: r (PC1) or z (PC2), haloed box {SROW, TR, 1}
   CUtensorMap p_h[2];   // P[0], P[1], haloed box
-  CUtensorMap r_i;      // r, interior box {TK, TJ, 1}
-  CUtensorMap x_i;      // x, interior box {TK, TJ, 1}
+  CUtensorMap r_i;      // r, interior box {TKB, TJ, 1}
+  CUtensorMap x_i;      // x, interior box {TKB, TJ, 1}
 };
 
 
@@ -153,7 +155,7 @@ __global__ void k_pass_a_pc1(const __grid_constant__ TMaps T, PassArgs A, int pa
 __global__ void k_pass_a_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a3
 __global__ void k_pass_b_pc1(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a7 + a8
 __global__ void k_pass_b_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a7
-// ghost columns (physical 1 and np+2) of shells [il0, il0 + n) from the interior
+// ghost columns (physical 0 and np+1) of shells [il0, il0 + n) from the interior
 __global__ void k_fix_ghost_cols(Grid G, double *a, int il0, int n);
 __global__ void k_finalize_alpha(Scalars *S, const double *gathered, int nranks);
 __global__ void k_finalize_beta(Scalars *S, const double *gathered, int nranks, double *hist);

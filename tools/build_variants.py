@@ -6,10 +6,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "a3b4m3": ["POT3D_NS_A=3", "POT3D_NS_B=4", "POT3D_MINB=3"],
-    "a3b4m2": ["POT3D_NS_A=3", "POT3D_NS_B=4", "POT3D_MINB=2"],
-    "a4b4m2": ["POT3D_NS_A=4", "POT3D_NS_B=4", "POT3D_MINB=2"],
-    "a3b3m3": ["POT3D_NS_A=3", "POT3D_NS_B=3", "POT3D_MINB=3"],
+    "b4m2": ["POT3D_NS_B=4", "POT3D_MINB=2"],
+    "b3m2": ["POT3D_NS_B=3", "POT3D_MINB=2"],
+    "b5m2": ["POT3D_NS_B=5", "POT3D_MINB=2"],
 }
 out = Path(build.PKG) / "variants"
 out.mkdir(exist_ok=True)
