@@ -1,11 +1,319 @@
-// pc2.cu -- placeholder (filled in by the PC2 milestone)
-#include "pot3d_internal.cuh"
+// pc2.cu -- PC2: zero-fill ILU of each r-slab block ("non-overlapping
+// domain decomposition with zero-fill incomplete LU"), as the D-ILU
+// factorisation that ILU0 reduces to for the 7-point pattern (A11):
+//
+//   factor:   d_m = diag_m - sum_{n in N-(m)} A_mn^2 / d_n
+//   forward:  w_m = (r_m + sum_{n in N-(m)} A_mn w_n) / d_m           (D + L) w = r
+//   backward: z_m = w_m + (1/d_m) sum_{n in N+(m)} A_mn z_n            (I + D^-1 U) z = w
+//
+// with A_mn > 0 the face coupling (off-diagonal -A_mn), N-(m) = {i-1, j-1, k-1}
+// and N+(m) = {i+1, j+1, k+1} inside the block: couplings that leave the
+// block's shells and the periodic phi wrap are dropped; the full
+// diagonal is kept.  The triangular solves are "not vectorizable" as a
+// sequential sweep; here they run as a 3-D wavefront on hyperplanes
+// i+j+k, tiled: a CTA owns a WJ x WK theta-phi tile over all shells of one
+// block and walks its own hyperplanes (thread (jj,kk) handles shell
+// t-jj-kk at step t, neighbours inside the tile through a shared double
+// buffer, the r neighbour in a register); tiles wait on the published
+// progress of the tiles above / to the left (acquire/release flags), CTAs
+// take tiles in topological order from a ticket counter so that every tile
+// a CTA waits on belongs to a CTA that is already running.  Every cell is
+// computed by exactly the sequential formula, only the order of the three
+// neighbour terms is fixed (r, theta, phi), so the sweep equals the
+// sequential ILU0 solve up to rounding.
+#include <algorithm>
+#include <vector>
+
+#include "device_common.cuh"
+
 namespace pot3d {
-struct Pc2 { int dummy; };
-int pc2_create(Pc2 **out, const Grid &, int, const int *, void *(*)(size_t, void *), void *) { *out = nullptr; return -1; }
-int pc2_factor(Pc2 *, const Metrics &, cudaStream_t, double *) { return -1; }
-int pc2_apply(Pc2 *, const Metrics &, Scalars *, const double *, double *, double *, int, double *, cudaStream_t, bool) { return -1; }
-void pc2_destroy(Pc2 *, void (*)(void *, void *), void *) {}
-size_t pc2_bytes(const Pc2 *) { return 0; }
-int pc2_kernels_per_apply(const Pc2 *) { return 0; }
+
+constexpr int WJ = 8;            // tile rows (theta)
+constexpr int WK = 32;           // tile columns (phi): one warp per row
+constexpr int WT = WJ * WK;      // threads per CTA
+constexpr int PUB = 2;           // publish progress every PUB steps
+
+enum SweepMode { SW_FACTOR = 0, SW_FWD = 1, SW_BWD = 2 };
+
+struct Pc2 {
+  Grid G;
+  int nblk;                 // ILU blocks on this rank
+  int ntj, ntk, ntiles;     // tile grid
+  int *d_l0;                // block bounds: nblk+1 local shell indices
+  int2 *d_order;            // tiles in topological (start-time) order
+  int *d_sync;              // [0] ticket, [1] breakdown flag, [2..] progress per (block, tile)
+  int nsync;
+  double *inv_d;            // 1/d_m, cell layout
+  std::vector<void *> allocs;
+  size_t bytes;
+};
+
+struct SweepArgs {
+  Grid G;
+  Metrics M;
+  Scalars *S;
+  const int *l0;
+  const int2 *order;
+  int *sync;
+  int nblk, ntj, ntk, ntiles;
+  const double *r;   // FWD: rhs r; BWD: r for the r.z partial
+  double *z;         // FWD: writes w; BWD: w -> z in place
+  double *inv_d;     // FACTOR writes, FWD/BWD read
+  double *partials;
+  int predicated;    // skip when the PCG loop has stopped
+  int finalize;      // BWD: 1 single rank (rho/beta), 0 local_sum
+  double *local_sum;
+};
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
+  const Grid &G = A.G;
+  const Metrics &M = A.M;
+  if (A.predicated && A.S->stop) return;
+  __shared__ double sw[2][WJ][WK];
+  __shared__ int s_ticket;
+  __shared__ double sred[WT / 32];
+  const int tid = threadIdx.x;
+  const int jj = tid / WK, kk = tid % WK;
+  if (tid == 0) s_ticket = atomicAdd(&A.sync[0], 1);
+  __syncthreads();
+  const int ticket = s_ticket;
+  const int b = ticket % A.nblk;
+  const int pos = ticket / A.nblk;
+  const int2 tl = A.order[pos];  // virtual tile (tj, tk)
+  const int l0 = A.l0[b], l1 = A.l0[b + 1];
+  const int nb = l1 - l0;
+  const bool rev = (MODE == SW_BWD);
+  // virtual coordinates (dependencies on iv-1, jv-1, kv-1); real = mirrored for BWD
+  const int jv = tl.x * WJ + jj, kv = tl.y * WK + kk;
+  const bool valid = (jv < G.nt) && (kv < G.np);
+  const int j = rev ? G.nt - 1 - jv : jv;
+  const int k = rev ? G.np - 1 - kv : kv;
+  const int jc = valid ? j : 0, kc = valid ? k : 0;
+  int *prog = A.sync + 2 + b * A.ntiles;
+  const int my = tl.x * A.ntk + tl.y;
+  const int up = (tl.x > 0) ? (tl.x - 1) * A.ntk + tl.y : -1;
+  const int lf = (tl.y > 0) ? tl.x * A.ntk + tl.y - 1 : -1;
+  const int nsteps = nb + WJ + WK - 2;
+
+  // row / column factors
+  const double g = __ldg(M.g + jc), q = __ldg(M.q + jc);
+  const double atp = __ldg(M.atp + jc), atm = __ldg(M.atm + jc);
+  const double dpk = __ldg(M.dp + kc), app = __ldg(M.app + kc), apm = __ldg(M.apm + kc);
+  // couplings to the virtual predecessors (theta / phi parts; zero across the
+  // block / pole / dropped wrap)
+  const double ct = rev ? atp : atm;                  // times dr_i dp_k
+  const double cp = rev ? ((k < G.np - 1) ? app : 0.0) : ((k > 0) ? apm : 0.0);  // times dr_i q_j
+  const int dj = rev ? 1 : -1, dk = rev ? 1 : -1;     // real offset of the theta / phi predecessor
+
+  double wprev = 0.0, acc = 0.0;
+  int have_up = 0, have_lf = 0;
+  bool bad = false;
+  for (int t = 0; t < nsteps; t++) {
+    __syncthreads();  // step t-1 complete in this CTA
+    if (tid == 0) {
+      if (t > 0 && (t % PUB) == 0) st_release(prog + my, t);
+      const int need_up = min(t + WJ, nsteps), need_lf = min(t + WK, nsteps);
+      if (up >= 0)
+        while (have_up < need_up) have_up = ld_acquire(prog + up);
+      if (lf >= 0)
+        while (have_lf < need_lf) have_lf = ld_acquire(prog + lf);
+    }
+    __syncthreads();
+    const int ivt = t - jj - kk;  // virtual local shell of this thread at step t
+    const bool active = valid && ivt >= 0 && ivt < nb;
+    double val = 0.0;
+    if (active) {
+      const int il = rev ? l1 - 1 - ivt : l0 + ivt;  // real local shell
+      const int ig = G.i0 + il;
+      const long long o = cidx(G, il, j, k);
+      const double dr = __ldg(M.dr + ig);
+      // predecessor values: r-direction in register, theta/phi in smem or neighbour tiles
+      const double vi = (ivt > 0) ? wprev : 0.0;
+      double vj, vk;
+      if (jj > 0)
+        vj = sw[(t - 1) & 1][jj - 1][kk];
+      else
+        vj = (jv > 0) ? ((MODE == SW_FACTOR) ? __ldcg(A.inv_d + o + dj * G.PK) : __ldcg(A.z + o + dj * G.PK)) : 0.0;
+      if (kk > 0)
+        vk = sw[(t - 1) & 1][jj][kk - 1];
+      else
+        vk = (kv > 0) ? ((MODE == SW_FACTOR) ? __ldcg(A.inv_d + o + dk) : __ldcg(A.z + o + dk)) : 0.0;
+      const double cr = (ivt > 0) ? (rev ? __ldg(M.arp + ig) : __ldg(M.arm + ig)) : 0.0;
+      const double Ar = cr * g * dpk, At = dr * ct * dpk, Ap = dr * q * cp;
+      if (MODE == SW_FACTOR) {
+        const double diag = dpk * (g * (__ldg(M.arp + ig) + __ldg(M.arm + ig) + __ldg(M.ss + ig)) +
+                                   dr * (atp + atm)) + dr * q * (app + apm);
+        // the wrap coupling and the inter-block couplings are dropped from L/U,
+        // the full diagonal is kept (A11)
+        const double d = diag - Ar * Ar * vi - At * At * vj - Ap * Ap * vk;
+        bad |= !(d > 1e-300);
+        val = 1.0 / d;
+        A.inv_d[o] = val;
+      } else if (MODE == SW_FWD) {
+        val = (__ldg(A.r + o) + Ar * vi + At * vj + Ap * vk) * __ldg(A.inv_d + o);
+        A.z[o] = val;
+      } else {
+        const double w = A.z[o];
+        val = w + __ldg(A.inv_d + o) * (Ar * vi + At * vj + Ap * vk);
+        A.z[o] = val;
+        acc += __ldg(A.r + o) * val;
+      }
+      wprev = val;
+      sw[t & 1][jj][kk] = val;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) st_release(prog + my, nsteps);
+  if (MODE == SW_FACTOR) {
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(&A.sync[1], 1);
+  }
+  if (MODE == SW_BWD) {
+    double v[1] = {acc}, tot[1];
+    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot) && tid == 0) {
+      if (A.finalize)
+        finalize_rho(A.S, tot[0]);
+      else
+        A.local_sum[0] = tot[0];
+    }
+  }
+}
+
+// periodic ghost columns of z (read by the TMA boxes of pass A)
+__global__ void k_pc2_ghost(Grid G, double *a, const Scalars *S, int predicated) {
+  if (predicated && S->stop) return;
+  const long long rows = (long long)G.nr_loc * G.nt;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < rows;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int il = (int)(c / G.nt), j = (int)(c % G.nt);
+    double *row = a + cidx(G, il, j, 0);
+    row[-1] = row[G.np - 1];
+    row[G.np] = row[0];
+  }
+}
+
+static void *p_alloc(Pc2 *P, size_t bytes, void *(*alloc)(size_t, void *), void *actx) {
+  void *p = nullptr;
+  if (alloc)
+    p = alloc(bytes, actx);
+  else if (cudaMalloc(&p, bytes) != cudaSuccess)
+    p = nullptr;
+  if (p) {
+    P->allocs.push_back(p);
+    P->bytes += bytes;
+  }
+  return p;
+}
+
+int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
+               void *(*alloc)(size_t, void *), void *actx) {
+  Pc2 *P = new Pc2();
+  P->G = G;
+  P->nblk = nblocks_local;
+  P->ntj = (G.nt + WJ - 1) / WJ;
+  P->ntk = (G.np + WK - 1) / WK;
+  P->ntiles = P->ntj * P->ntk;
+  P->nsync = 2 + P->nblk * P->ntiles;
+  P->bytes = 0;
+  P->d_l0 = (int *)p_alloc(P, sizeof(int) * (nblocks_local + 1), alloc, actx);
+  P->d_order = (int2 *)p_alloc(P, sizeof(int2) * P->ntiles, alloc, actx);
+  P->d_sync = (int *)p_alloc(P, sizeof(int) * P->nsync, alloc, actx);
+  const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
+  P->inv_d = (double *)p_alloc(P, sizeof(double) * cells, alloc, actx);
+  if (!P->d_l0 || !P->d_order || !P->d_sync || !P->inv_d) {
+    *out = P;
+    return -1;
+  }
+  // topological order: by estimated start step tj*WJ + tk*WK (both predecessors
+  // start strictly earlier), ties by tj
+  std::vector<int2> order;
+  order.reserve(P->ntiles);
+  for (int a = 0; a < P->ntj; a++)
+    for (int c = 0; c < P->ntk; c++) order.push_back(make_int2(a, c));
+  std::stable_sort(order.begin(), order.end(), [](const int2 &x, const int2 &y) {
+    const int sx = x.x * WJ + x.y * WK, sy = y.x * WJ + y.y * WK;
+    return sx != sy ? sx < sy : x.x < y.x;
+  });
+  cudaMemcpy(P->d_order, order.data(), sizeof(int2) * P->ntiles, cudaMemcpyHostToDevice);
+  cudaMemcpy(P->d_l0, block_l0, sizeof(int) * (nblocks_local + 1), cudaMemcpyHostToDevice);
+  cudaMemset(P->inv_d, 0, sizeof(double) * cells);
+  *out = P;
+  return 0;
+}
+
+static SweepArgs sweep_args(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z,
+                            double *partials, int predicated, int finalize, double *local_sum) {
+  SweepArgs a{};
+  a.G = P->G;
+  a.M = M;
+  a.S = S;
+  a.l0 = P->d_l0;
+  a.order = P->d_order;
+  a.sync = P->d_sync;
+  a.nblk = P->nblk;
+  a.ntj = P->ntj;
+  a.ntk = P->ntk;
+  a.ntiles = P->ntiles;
+  a.r = r;
+  a.z = z;
+  a.inv_d = P->inv_d;
+  a.partials = partials;
+  a.predicated = predicated;
+  a.finalize = finalize;
+  a.local_sum = local_sum;
+  return a;
+}
+
+int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host) {
+  cudaMemsetAsync(P->d_sync, 0, sizeof(int) * P->nsync, s);
+  SweepArgs a = sweep_args(P, M, nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr);
+  k_sweep<SW_FACTOR><<<P->nblk * P->ntiles, WT, 0, s>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  int flags[2];
+  cudaMemcpyAsync(flags, P->d_sync, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+  *min_pivot_host = flags[1] ? 0.0 : 1.0;  // breakdown (pivot <= 1e-300) -> 0
+  return 0;
+}
+
+// z = M^-1 r; returns the number of kernels launched (memsets excluded) or -1.
+int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, double *partials,
+              int finalize, double *local_sum, cudaStream_t s, bool iteration) {
+  const int pred = iteration ? 1 : 0;
+  SweepArgs a = sweep_args(P, M, S, r, z, partials, pred, finalize, local_sum);
+  cudaMemsetAsync(P->d_sync, 0, sizeof(int) * P->nsync, s);
+  k_sweep<SW_FWD><<<P->nblk * P->ntiles, WT, 0, s>>>(a);
+  cudaMemsetAsync(P->d_sync, 0, sizeof(int) * P->nsync, s);
+  if (!iteration) a.finalize = 0, a.local_sum = local_sum;
+  k_sweep<SW_BWD><<<P->nblk * P->ntiles, WT, 0, s>>>(a);
+  const Grid &G = P->G;
+  k_pc2_ghost<<<(unsigned)std::min<long long>(((long long)G.nr_loc * G.nt + 255) / 256, 4096), 256, 0,
+                s>>>(G, z, S, pred);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  return 3;
+}
+
+void pc2_destroy(Pc2 *P, void (*fr)(void *, void *), void *actx) {
+  if (!P) return;
+  for (void *p : P->allocs) {
+    if (fr)
+      fr(p, actx);
+    else
+      cudaFree(p);
+  }
+  delete P;
+}
+
+size_t pc2_bytes(const Pc2 *P) { return P ? P->bytes : 0; }
+int pc2_kernels_per_apply(const Pc2 *P) { return P ? 3 : 0; }
+
+}  // namespace pot3d

@@ -187,3 +187,49 @@ def test_medium_config_fixed_iterations():
     assert res.iters == 10
     scale = np.abs(ref["x"]).max()
     assert np.abs(res.phi - ref["x"]).max() <= 1e-9 * scale
+
+
+# ---------------------------------------------------------------------------
+# PC2: block ILU0 -- GPU D-ILU wavefront sweeps vs the oracle's CSR
+# IKJ ILU0 + sequential triangular solves
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dims", [(2, 2, 2), (3, 5, 7), (5, 9, 33), (12, 17, 70), (21, 31, 61)])
+@pytest.mark.parametrize("blocks", [1, 2, 3])
+def test_pc2_apply_matches_oracle(dims, blocks):
+    if blocks > dims[0]:
+        pytest.skip("more blocks than shells")
+    rf, tf, pf = synth.grid(*dims)
+    n = int(np.prod(dims))
+    r = synth.random_vector(n, 7).reshape(dims[::-1])
+    z_ref = oracle.precond(rf, tf, pf, r, pc=2, pc2_blocks=blocks)
+    with solver(rf, tf, pf, synth.br0_map(tf, pf, 0), pc=2, pc2_blocks=blocks) as s:
+        assert s.info()["pc"] == 2
+        z = s.precond(r)
+    assert np.abs(z - z_ref).max() <= 1e-12 * np.abs(z_ref).max()
+
+
+@pytest.mark.parametrize("blocks", [1, 2, 4, 8])
+def test_pc2_tiny_solve_parity(blocks):
+    c = synth.CONFIGS["tiny"]
+    rf, tf, pf = c.faces()
+    res, ref = _check_solve(rf, tf, pf, c.br0(), pc=2, blocks=blocks)
+
+
+def test_pc2_iterations_grow_with_blocks_gpu():
+    """P:270: PC2 'becomes less effective as the number of processors increases'."""
+    c = synth.CONFIGS["small"]
+    rf, tf, pf = c.faces()
+    its = []
+    for blocks in (1, 2, 4, 8):
+        with solver(rf, tf, pf, c.br0(), pc=2, pc2_blocks=blocks) as s:
+            its.append(s.solve(rtol=1e-9).iters)
+    with solver(rf, tf, pf, c.br0(), pc=1) as s:
+        pc1 = s.solve(rtol=1e-9).iters
+    assert its[0] <= 0.75 * pc1
+    assert all(its[i] <= its[i + 1] for i in range(3)), its
+
+
+def test_pc2_small_parity_closed_wall():
+    c = synth.CONFIGS["small"]
+    rf, tf, pf = c.faces()
+    _check_solve(rf, tf, pf, c.br0(), bc=CW, pc=2, blocks=2)
