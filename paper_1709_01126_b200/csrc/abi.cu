@@ -559,7 +559,9 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   if (R.cuda_stream) {
     ctx->stream = (cudaStream_t)R.cuda_stream;
   } else {
-    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    // a blocking stream: implicitly ordered with the legacy default stream the
+    // caller (e.g. torch's default stream) produces device inputs on
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault));
     ctx->own_stream = true;
   }
 
@@ -656,7 +658,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
     std::vector<int> lb(ctx->pc2_blocks + 1);
     for (int b = 0; b < ctx->pc2_blocks; b++) lb[b] = bi0[ctx->rank * ctx->pc2_blocks + b] - G.i0;
     lb[ctx->pc2_blocks] = G.nr_loc;
-    rc = pc2_create(&ctx->pc2, G, ctx->pc2_blocks, lb.data(), ctx->ualloc, ctx->actx);
+    rc = pc2_create(&ctx->pc2, G, ctx->pc2_blocks, lb.data(), ctx->ualloc, ctx->actx, ctx->stream);
     if (rc) { ctx->err = "pc2_create failed"; return fail(POT3D_ERR_OOM); }
     double minpiv = 0;
     rc = pc2_factor(ctx->pc2, ctx->M, ctx->stream, &minpiv);
@@ -792,7 +794,30 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
   CK(cudaMemcpyAsync(ctx->hS, ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const Scalars hs = *ctx->hS;
+  ctx->last_iters = hs.iter;
   if (hs.status == -4) {
+    if (getenv("POT3D_DEBUG")) {  // diagnostics: scalars and non-finite counts of the vectors
+      fprintf(stderr, "POT3D_DEBUG iter %lld rho %g alpha %g beta %g sigma %g rr %g bnorm %g\n",
+              hs.iter, hs.rho, hs.alpha, hs.beta, hs.sigma, hs.rr, hs.bnorm);
+      const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
+      std::vector<double> h(cells);
+      const char *nm[5] = {"x", "r", "P0", "P1", "z"};
+      double *ar[5] = {ctx->x, ctx->r, ctx->P[0], ctx->P[1], ctx->z};
+      for (int q = 0; q < 5; q++) {
+        if (!ar[q]) continue;
+        cudaMemcpy(h.data(), ar[q], cells * 8, cudaMemcpyDeviceToHost);
+        size_t bad = 0, first = (size_t)-1;
+        double mx = 0;
+        for (size_t c = 0; c < cells; c++) {
+          if (!std::isfinite(h[c])) { if (!bad) first = c; bad++; }
+          else mx = std::max(mx, std::fabs(h[c]));
+        }
+        long long fi = first == (size_t)-1 ? -1 : (long long)first;
+        fprintf(stderr, "  %s: nonfinite %zu first %lld (shell %lld row %lld col %lld) max|.| %g\n", nm[q], bad, fi,
+                fi < 0 ? -1 : fi / G.plane - 1, fi < 0 ? -1 : (fi % G.plane) / G.PK,
+                fi < 0 ? -1 : (fi % G.PK) - COFF, mx);
+      }
+    }
     ctx->err = "p.Ap <= 0: operator or preconditioner not positive definite (S:341)";
     return POT3D_ERR_INDEFINITE;
   }
@@ -839,7 +864,7 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
 
 int64_t pot3d_history(pot3d_ctx *ctx, double *hist, int64_t len) {
   if (!ctx || !hist) return POT3D_ERR_INVALID;
-  if (!ctx->solved || !ctx->hist) return POT3D_ERR_STATE;
+  if (!ctx->hist) return POT3D_ERR_STATE;
   int64_t n = std::min<int64_t>(len, ctx->last_iters + 1);
   if (cudaMemcpy(hist, ctx->hist, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
     ctx->err = "history copy failed";

@@ -196,18 +196,27 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   auto issue = [&](int q, int st) {
     if (q <= L + 1) {
       const int il = t.c0 - 1 + q;
-      const bool ghost = (il < 0) || (il >= G.nr_loc);  // ghost shells hold the final p_k
-      mbar_arrive_expect_tx(&sm.bar[st], STAGE_BYTES);
-      tma_load_3d(&sm.r[st][0][0], ghost ? map_new : map_src, &sm.bar[st], t.k0 - 3 + COFF,
-                  t.j0 - 1, il + 1);
-      // p_{k-1} on a ghost shell is not used: an out-of-range shell zero-fills the stage
-      tma_load_3d(&sm.p[st][0][0], map_old, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1,
-                  ghost ? G.nr_loc + 2 : il + 1);
+      if ((il < 0) || (il >= G.nr_loc)) {
+        // ghost shell: it holds the final p_k (halo / zeros); p_{k-1} is not loaded
+        // (a fully out-of-range box is not a reliable zero fill)
+        mbar_arrive_expect_tx(&sm.bar[st], STAGE_BYTES / 2);
+        tma_load_3d(&sm.r[st][0][0], map_new, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
+      } else {
+        mbar_arrive_expect_tx(&sm.bar[st], STAGE_BYTES);
+        tma_load_3d(&sm.r[st][0][0], map_src, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
+        tma_load_3d(&sm.p[st][0][0], map_old, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
+      }
     }
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS_A; s++) mbar_init(&sm.bar[s], 1);
     fence_mbar_init();
+  }
+  // slot columns 0, 1, 66, 67 are never produced by the transform; they are read
+  // only by the masked halo elements of lanes 0 / 31 and must hold finite values
+  for (int i = threadIdx.x; i < 3 * TR; i += blockDim.x) {
+    double *row = &sm.pn[i / TR][i % TR][0];
+    row[0] = row[1] = row[SROW - 2] = row[SROW - 1] = 0.0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -222,7 +231,6 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
 #pragma unroll
     for (int e = 0; e < RPW; e++) R[u][e] = Z2;
   double *g_pn = A.p_new + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: p_k at plane c0
-  const double m0 = t.st0 ? 1.0 : 0.0, m1 = t.st1 ? 1.0 : 0.0;
   PlanePtr pp = plane_ptr(M, G.i0 + t.c0 - 1);  // metrics of the transformed plane
   PlanePtr ps = plane_ptr(M, G.i0 + t.c0);      // metrics of the stencil plane
   double acc = 0.0;
@@ -246,11 +254,11 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     for (int e = 0; e < RPW; e++) {
       const int r = t.row[e];
       const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[u][r][cs]);
-      const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[u][r][cs]);
+      const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[u][r][cs]);  // unused on ghosts
       double2 pn;
       if (USE_Z) {
-        pn.x = fma(beta, pv.x, rv.x);  // ghost shells: pv = 0 -> pn = rv (final p_k)
-        pn.y = fma(beta, pv.y, rv.y);
+        pn.x = ghost ? rv.x : fma(beta, pv.x, rv.x);
+        pn.y = ghost ? rv.y : fma(beta, pv.y, rv.y);
       } else {
         const DiagRow d = diag_row(P, rw[e]);
         pn.x = ghost ? rv.x : fdiv(rv.x, dp.x * d.a + d.b * (ap.x + am.x)) + beta * pv.x;
@@ -277,8 +285,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
         const double lf = so[-1], rt = so[2];
         const double q0 = stencil7(c.x, R[u][e].x, R[umm][e].x, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e]);
         const double q1 = stencil7(c.y, R[u][e].y, R[umm][e].y, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e]);
-        acc = fma(m0 * c.x, q0, acc);
-        acc = fma(m1 * c.y, q1, acc);
+        acc += (t.st0 ? c.x * q0 : 0.0) + (t.st1 ? c.y * q1 : 0.0);
       }
     }
   };
@@ -360,7 +367,6 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
 #pragma unroll
   for (int e = 0; e < RPW; e++) pm[e] = pc[e] = pn[e] = Z2;
   double acc_rz = 0.0, acc_rr = 0.0;
-  const double m0 = t.st0 ? 1.0 : 0.0, m1 = t.st1 ? 1.0 : 0.0;
   double *g_w = A.r_out + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: r of plane c0
   double *g_x = A.x + (long long)(t.c0 + 1) * PL;      // + rowoff[e]: x of plane c0
   PlanePtr ps = plane_ptr(M, G.i0 + t.c0);             // metrics of the stencil plane
@@ -399,16 +405,13 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
         xn.x = fma(alpha, pc[e].x, xv.x);
         xn.y = fma(alpha, pc[e].y, xv.y);
         if (USE_Z) {
-          acc_rr = fma(m0 * rn.x, rn.x, acc_rr);
-          acc_rr = fma(m1 * rn.y, rn.y, acc_rr);
+          acc_rr += (t.st0 ? rn.x * rn.x : 0.0) + (t.st1 ? rn.y * rn.y : 0.0);
         } else {
           const DiagRow d = diag_row(P, rw[e]);
           const double z0 = fdiv(rn.x, dp.x * d.a + d.b * (ap.x + am.x));
           const double z1 = fdiv(rn.y, dp.y * d.a + d.b * (ap.y + am.y));
-          acc_rz = fma(m0 * rn.x, z0, acc_rz);
-          acc_rz = fma(m1 * rn.y, z1, acc_rz);
-          acc_rr = fma(m0 * rn.x, rn.x, acc_rr);
-          acc_rr = fma(m1 * rn.y, rn.y, acc_rr);
+          acc_rz += (t.st0 ? rn.x * z0 : 0.0) + (t.st1 ? rn.y * z1 : 0.0);
+          acc_rr += (t.st0 ? rn.x * rn.x : 0.0) + (t.st1 ? rn.y * rn.y : 0.0);
         }
         store_pair(g_w + t.rowoff[e], t, G.np, rn, true);
         if (t.st0 && t.st1) {

@@ -31,7 +31,10 @@ namespace pot3d {
 constexpr int WJ = 8;            // tile rows (theta)
 constexpr int WK = 32;           // tile columns (phi): one warp per row
 constexpr int WT = WJ * WK;      // threads per CTA
-constexpr int PUB = 2;           // publish progress every PUB steps
+#ifndef POT3D_SWEEP_PUB
+#define POT3D_SWEEP_PUB 2
+#endif
+constexpr int PUB = POT3D_SWEEP_PUB;  // publish progress every PUB steps
 
 enum SweepMode { SW_FACTOR = 0, SW_FWD = 1, SW_BWD = 2 };
 
@@ -119,6 +122,9 @@ __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
   int have_up = 0, have_lf = 0;
   bool bad = false;
   for (int t = 0; t < nsteps; t++) {
+#ifdef POT3D_SWEEP_STRICT
+    if (t > 0 && (t % PUB) == 0) __threadfence();  // every writer orders its stores
+#endif
     __syncthreads();  // step t-1 complete in this CTA
     if (tid == 0) {
       if (t > 0 && (t % PUB) == 0) st_release(prog + my, t);
@@ -179,7 +185,8 @@ __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
   }
   if (MODE == SW_BWD) {
     double v[1] = {acc}, tot[1];
-    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot) && tid == 0) {
+    // partials indexed by ticket (tile identity), not blockIdx: a fixed summation order
+    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket) && tid == 0) {
       if (A.finalize)
         finalize_rho(A.S, tot[0]);
       else
@@ -215,7 +222,7 @@ static void *p_alloc(Pc2 *P, size_t bytes, void *(*alloc)(size_t, void *), void 
 }
 
 int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
-               void *(*alloc)(size_t, void *), void *actx) {
+               void *(*alloc)(size_t, void *), void *actx, cudaStream_t s) {
   Pc2 *P = new Pc2();
   P->G = G;
   P->nblk = nblocks_local;
@@ -243,11 +250,12 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
     const int sx = x.x * WJ + x.y * WK, sy = y.x * WJ + y.y * WK;
     return sx != sy ? sx < sy : x.x < y.x;
   });
-  cudaMemcpy(P->d_order, order.data(), sizeof(int2) * P->ntiles, cudaMemcpyHostToDevice);
-  cudaMemcpy(P->d_l0, block_l0, sizeof(int) * (nblocks_local + 1), cudaMemcpyHostToDevice);
-  cudaMemset(P->inv_d, 0, sizeof(double) * cells);
+  // everything on the context stream (the factor kernel runs there too)
+  cudaMemcpyAsync(P->d_order, order.data(), sizeof(int2) * P->ntiles, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(P->d_l0, block_l0, sizeof(int) * (nblocks_local + 1), cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(P->inv_d, 0, sizeof(double) * cells, s);
   *out = P;
-  return 0;
+  return cudaStreamSynchronize(s) == cudaSuccess ? 0 : -1;
 }
 
 static SweepArgs sweep_args(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z,

@@ -188,7 +188,7 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
 // pc2.cu -- PC2 (block ILU0 = D-ILU, A11) with tiled sync-free wavefront sweeps
 struct Pc2;
 int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
-               void *(*alloc)(size_t, void *), void *actx);
+               void *(*alloc)(size_t, void *), void *actx, cudaStream_t s);
 int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host);
 // z = M^-1 r; partial r.z -> finalize (single rank: rho/beta update, mode iteration) or
 // local_sum[0]; `iteration` selects the predicated in-loop variant.

@@ -6,9 +6,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "b4m2": ["POT3D_NS_B=4", "POT3D_MINB=2"],
-    "b3m2": ["POT3D_NS_B=3", "POT3D_MINB=2"],
-    "b5m2": ["POT3D_NS_B=5", "POT3D_MINB=2"],
+    "strict1": ["POT3D_SWEEP_STRICT=1", "POT3D_SWEEP_PUB=1"],
+    "pub1": ["POT3D_SWEEP_PUB=1"],
+    "strict2": ["POT3D_SWEEP_STRICT=1"],
 }
 out = Path(build.PKG) / "variants"
 out.mkdir(exist_ok=True)
