@@ -32,9 +32,10 @@ constexpr int WJ = 8;            // tile rows (theta)
 constexpr int WK = 32;           // tile columns (phi): one warp per row
 constexpr int WT = WJ * WK;      // threads per CTA
 #ifndef POT3D_SWEEP_PUB
-#define POT3D_SWEEP_PUB 2
+#define POT3D_SWEEP_PUB 4
 #endif
-constexpr int PUB = POT3D_SWEEP_PUB;  // publish progress every PUB steps
+constexpr int PUB = POT3D_SWEEP_PUB;      // publish progress every PUB steps (a release costs an L2 round trip)
+constexpr long long SPIN_LIMIT = 1ll << 28;  // bounded waits: a protocol error never hangs the GPU
 
 enum SweepMode { SW_FACTOR = 0, SW_FWD = 1, SW_BWD = 2 };
 
@@ -77,6 +78,11 @@ __device__ __forceinline__ void st_release(int *p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
+#ifndef POT3D_SWEEP_D
+#define POT3D_SWEEP_D 8
+#endif
+constexpr int PD = POT3D_SWEEP_D;  // prefetch distance (steps): operands of step t+PD load at step t
+
 template <int MODE>
 __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
   const Grid &G = A.G;
@@ -112,70 +118,103 @@ __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
   const double g = __ldg(M.g + jc), q = __ldg(M.q + jc);
   const double atp = __ldg(M.atp + jc), atm = __ldg(M.atm + jc);
   const double dpk = __ldg(M.dp + kc), app = __ldg(M.app + kc), apm = __ldg(M.apm + kc);
-  // couplings to the virtual predecessors (theta / phi parts; zero across the
-  // block / pole / dropped wrap)
-  const double ct = rev ? atp : atm;                  // times dr_i dp_k
-  const double cp = rev ? ((k < G.np - 1) ? app : 0.0) : ((k > 0) ? apm : 0.0);  // times dr_i q_j
-  const int dj = rev ? 1 : -1, dk = rev ? 1 : -1;     // real offset of the theta / phi predecessor
+  // couplings to the virtual predecessors (zero across the pole / the dropped wrap)
+  const double ct = rev ? atp : atm;                                              // x dr_i dp_k
+  const double cp = rev ? ((k < G.np - 1) ? app : 0.0) : ((k > 0) ? apm : 0.0);  // x dr_i q_j
+  const long long dj = rev ? G.PK : -G.PK;  // real offset of the theta predecessor
+  const long long dk = rev ? 1 : -1;        // real offset of the phi predecessor
+  const long long o_base = cidx(G, rev ? l1 - 1 : l0, jc, kc);
+  const long long o_step = rev ? -G.plane : G.plane;  // one virtual shell
+  const int ig_base = G.i0 + (rev ? l1 - 1 : l0), ig_step = rev ? -1 : 1;
+  const bool need_j = (jj == 0) && (jv > 0), need_k = (kk == 0) && (kv > 0);
+  const double *nsrc = (MODE == SW_FACTOR) ? A.inv_d : A.z;
+
+  // prefetch ring: operands of the cell this thread handles at step t+PD
+  double ra[PD], rb[PD], rc[PD], rnj[PD], rnk[PD];
+  auto fetch = [&](int ts, double &xa, double &xb, double &xc, double &xj, double &xk) {
+    const int iv = ts - jj - kk;
+    xa = xb = xc = xj = xk = 0.0;
+    if (valid && iv >= 0 && iv < nb) {
+      const long long o = o_base + (long long)iv * o_step;
+      if (MODE == SW_FWD) {
+        xa = __ldg(A.r + o);
+        xb = __ldg(A.inv_d + o);
+      } else if (MODE == SW_BWD) {
+        xa = __ldcg(A.z + o);   // w of this cell (forward sweep output)
+        xb = __ldg(A.inv_d + o);
+        xc = __ldg(A.r + o);    // r of this cell for the r.z partial
+      }
+      if (need_j) xj = __ldcg(nsrc + o + dj);
+      if (need_k) xk = __ldcg(nsrc + o + dk);
+    }
+  };
+  int have_up = 0, have_lf = 0;
+  auto wait_neighbours = [&](int need_step) {  // neighbours completed step need_step + W - 1
+    if (up >= 0) {
+      const int need = min(need_step + WJ, nsteps);
+      long long spins = 0;
+      while (have_up < need && spins++ < SPIN_LIMIT) have_up = ld_acquire(prog + up);
+      if (have_up < need) atomicOr(&A.sync[1], 2);  // protocol error: flag, never hang
+    }
+    if (lf >= 0) {
+      const int need = min(need_step + WK, nsteps);
+      long long spins = 0;
+      while (have_lf < need && spins++ < SPIN_LIMIT) have_lf = ld_acquire(prog + lf);
+      if (have_lf < need) atomicOr(&A.sync[1], 2);
+    }
+  };
+  if (tid == 0) wait_neighbours(PD - 1);
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < PD; u++) fetch(u, ra[u], rb[u], rc[u], rnj[u], rnk[u]);
 
   double wprev = 0.0, acc = 0.0;
-  int have_up = 0, have_lf = 0;
   bool bad = false;
-  for (int t = 0; t < nsteps; t++) {
-#ifdef POT3D_SWEEP_STRICT
-    if (t > 0 && (t % PUB) == 0) __threadfence();  // every writer orders its stores
-#endif
-    __syncthreads();  // step t-1 complete in this CTA
-    if (tid == 0) {
-      if (t > 0 && (t % PUB) == 0) st_release(prog + my, t);
-      const int need_up = min(t + WJ, nsteps), need_lf = min(t + WK, nsteps);
-      if (up >= 0)
-        while (have_up < need_up) have_up = ld_acquire(prog + up);
-      if (lf >= 0)
-        while (have_lf < need_lf) have_lf = ld_acquire(prog + lf);
-    }
-    __syncthreads();
-    const int ivt = t - jj - kk;  // virtual local shell of this thread at step t
-    const bool active = valid && ivt >= 0 && ivt < nb;
-    double val = 0.0;
-    if (active) {
-      const int il = rev ? l1 - 1 - ivt : l0 + ivt;  // real local shell
-      const int ig = G.i0 + il;
-      const long long o = cidx(G, il, j, k);
-      const double dr = __ldg(M.dr + ig);
-      // predecessor values: r-direction in register, theta/phi in smem or neighbour tiles
-      const double vi = (ivt > 0) ? wprev : 0.0;
-      double vj, vk;
-      if (jj > 0)
-        vj = sw[(t - 1) & 1][jj - 1][kk];
-      else
-        vj = (jv > 0) ? ((MODE == SW_FACTOR) ? __ldcg(A.inv_d + o + dj * G.PK) : __ldcg(A.z + o + dj * G.PK)) : 0.0;
-      if (kk > 0)
-        vk = sw[(t - 1) & 1][jj][kk - 1];
-      else
-        vk = (kv > 0) ? ((MODE == SW_FACTOR) ? __ldcg(A.inv_d + o + dk) : __ldcg(A.z + o + dk)) : 0.0;
-      const double cr = (ivt > 0) ? (rev ? __ldg(M.arp + ig) : __ldg(M.arm + ig)) : 0.0;
-      const double Ar = cr * g * dpk, At = dr * ct * dpk, Ap = dr * q * cp;
-      if (MODE == SW_FACTOR) {
-        const double diag = dpk * (g * (__ldg(M.arp + ig) + __ldg(M.arm + ig) + __ldg(M.ss + ig)) +
-                                   dr * (atp + atm)) + dr * q * (app + apm);
-        // the wrap coupling and the inter-block couplings are dropped from L/U,
-        // the full diagonal is kept (A11)
-        const double d = diag - Ar * Ar * vi - At * At * vj - Ap * Ap * vk;
-        bad |= !(d > 1e-300);
-        val = 1.0 / d;
-        A.inv_d[o] = val;
-      } else if (MODE == SW_FWD) {
-        val = (__ldg(A.r + o) + Ar * vi + At * vj + Ap * vk) * __ldg(A.inv_d + o);
-        A.z[o] = val;
-      } else {
-        const double w = A.z[o];
-        val = w + __ldg(A.inv_d + o) * (Ar * vi + At * vj + Ap * vk);
-        A.z[o] = val;
-        acc += __ldg(A.r + o) * val;
+  for (int t0 = 0; t0 < nsteps; t0 += PD) {
+#pragma unroll
+    for (int u = 0; u < PD; u++) {
+      const int t = t0 + u;
+      if (t >= nsteps) break;
+      __syncthreads();  // step t-1 complete in this CTA
+      if (tid == 0) {
+        if (t > 0 && (t % PUB) == 0) st_release(prog + my, t);
+        wait_neighbours(t + PD);
       }
-      wprev = val;
-      sw[t & 1][jj][kk] = val;
+      __syncthreads();
+      // operands of step t (fetched PD steps ago), then prefetch step t+PD
+      const double a0 = ra[u], b0 = rb[u], c0 = rc[u], nj = rnj[u], nk = rnk[u];
+      fetch(t + PD, ra[u], rb[u], rc[u], rnj[u], rnk[u]);
+      const int ivt = t - jj - kk;  // virtual local shell of this thread at step t
+      if (valid && ivt >= 0 && ivt < nb) {
+        const long long o = o_base + (long long)ivt * o_step;
+        const int ig = ig_base + ivt * ig_step;
+        const double dr = __ldg(M.dr + ig);
+        const double vi = (ivt > 0) ? wprev : 0.0;
+        const double vj = (jj > 0) ? sw[(t - 1) & 1][jj - 1][kk] : nj;
+        const double vk = (kk > 0) ? sw[(t - 1) & 1][jj][kk - 1] : nk;
+        const double cr = (ivt > 0) ? (rev ? __ldg(M.arp + ig) : __ldg(M.arm + ig)) : 0.0;
+        const double Ar = cr * g * dpk, At = dr * ct * dpk, Ap = dr * q * cp;
+        double val;
+        if (MODE == SW_FACTOR) {
+          const double diag = dpk * (g * (__ldg(M.arp + ig) + __ldg(M.arm + ig) + __ldg(M.ss + ig)) +
+                                     dr * (atp + atm)) + dr * q * (app + apm);
+          // the wrap coupling and the inter-block couplings are dropped from L/U,
+          // the full diagonal is kept (A11)
+          const double d = diag - Ar * Ar * vi - At * At * vj - Ap * Ap * vk;
+          bad |= !(d > 1e-300);
+          val = 1.0 / d;
+          A.inv_d[o] = val;
+        } else if (MODE == SW_FWD) {
+          val = (a0 + Ar * vi + At * vj + Ap * vk) * b0;
+          A.z[o] = val;
+        } else {
+          val = a0 + b0 * (Ar * vi + At * vj + Ap * vk);
+          A.z[o] = val;
+          acc += c0 * val;
+        }
+        wprev = val;
+        sw[t & 1][jj][kk] = val;
+      }
     }
   }
   __syncthreads();

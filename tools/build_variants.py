@@ -6,9 +6,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "strict1": ["POT3D_SWEEP_STRICT=1", "POT3D_SWEEP_PUB=1"],
-    "pub1": ["POT3D_SWEEP_PUB=1"],
-    "strict2": ["POT3D_SWEEP_STRICT=1"],
+    "d4p4": ["POT3D_SWEEP_D=4", "POT3D_SWEEP_PUB=4"],
+    "d8p4": ["POT3D_SWEEP_D=8", "POT3D_SWEEP_PUB=4"],
+    "d8p2": ["POT3D_SWEEP_D=8", "POT3D_SWEEP_PUB=2"],
+    "d16p4": ["POT3D_SWEEP_D=16", "POT3D_SWEEP_PUB=4"],
 }
 out = Path(build.PKG) / "variants"
 out.mkdir(exist_ok=True)
