@@ -202,18 +202,13 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1709_01126_b200 import Pot3d, nccl_unique_id
+    from paper_1709_01126_b200 import Pot3d
 
     c = make_config(args, world)
     rf, tf, pf = c.faces()
     br_np = c.br0((rf, tf, pf))
-    nid = None
-    if world > 1:
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
-    s = Pot3d(rf, tf, pf, br_np, bc=c.bc, pc=c.pc, rank=rank, nranks=world, nccl_id=nid,
-              pc2_blocks=args.pc2_blocks, unroll=8)
+    s = Pot3d(rf, tf, pf, br_np, bc=c.bc, pc=c.pc, rank=rank, nranks=world,
+              pc2_blocks=args.pc2_blocks, unroll=8)  # fresh NCCL id broadcast inside
     info = s.info()
     fixed_iters = args.weak_iters if args.config == "weak" else 0
     rtol = 0.0 if fixed_iters else c.rtol

@@ -106,6 +106,45 @@ def library(build_if_missing: bool = True):
     return L
 
 
+def slab_bounds(nr: int, nranks: int, rank: int, pc2_blocks: int = 1, pc: int = PC1):
+    """This rank's shells [i0, i1) -- the same leading-remainder partition the
+    library uses: PC1 splits nr over ranks; PC2 over nranks*pc2_blocks
+    ILU blocks, a rank owning pc2_blocks consecutive blocks (host logic only)."""
+    def bounds(n, parts, b):
+        base, rem = divmod(n, parts)
+        a = b * base + min(b, rem)
+        return a, a + base + (1 if b < rem else 0)
+
+    if pc == PC1:
+        return bounds(nr, nranks, rank)
+    B = nranks * max(1, pc2_blocks)
+    return bounds(nr, B, rank * pc2_blocks)[0], bounds(nr, B, (rank + 1) * pc2_blocks - 1)[1]
+
+
+def gather_slabs(local, nr: int, group=None, dst: int = 0):
+    """Assemble the global r-fastest array (np, nt, nr) from every rank's slab
+    (np, nt, nr_loc) with torch.distributed (gloo for CPU tensors, NCCL for CUDA
+    tensors).  Returns the full array on `dst`, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    t = local if isinstance(local, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(local))
+    world = dist.get_world_size(group)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=t.device) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([t.shape[-1]], dtype=torch.int64, device=t.device), group=group)
+    widths = [int(s.item()) for s in sizes]
+    if sum(widths) != nr:
+        raise ValueError(f"slab widths {widths} do not tile nr={nr}")
+    wmax = max(widths)
+    pad = torch.zeros(t.shape[:-1] + (wmax,), dtype=t.dtype, device=t.device)
+    pad[..., : t.shape[-1]] = t
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    if dist.get_rank(group) != dst:
+        return None
+    return torch.cat([b[..., :w] for b, w in zip(bufs, widths)], dim=-1)
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     rc = library().pot3d_nccl_unique_id(buf)
@@ -162,6 +201,13 @@ class Pot3d:
                   self.rf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                   self.tf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                   self.pf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        if nranks > 1 and nccl_id is None:
+            # a ncclUniqueId is single-use: every context gets a fresh one from rank 0
+            import torch.distributed as dist
+
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
         rt = _Runtime()
         rt.rank, rt.nranks = rank, nranks
         self._nccl_id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None

@@ -1,0 +1,52 @@
+"""Multi-GPU parity check, run under torchrun (one process per GPU):
+   torchrun --nproc-per-node N tools/mgpu_check.py
+Solves configs with the r-slab decomposition and compares the gathered Phi with
+the CPU oracle (PC1: iterations +-1, rel L2 <= 1e-9; PC2 with N*b blocks)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1709_01126_b200 import Pot3d, gather_slabs  # noqa: E402
+
+rank = int(os.environ["RANK"])
+world = int(os.environ["WORLD_SIZE"])
+local = int(os.environ.get("LOCAL_RANK", rank))
+torch.cuda.set_device(local)
+dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+fails = 0
+cases = [("tiny", 1, 1, synth.SOURCE_SURFACE), ("small", 1, 1, synth.SOURCE_SURFACE),
+         ("small", 1, 1, synth.CLOSED_WALL), ("small", 2, 1, synth.SOURCE_SURFACE),
+         ("small", 2, 2, synth.SOURCE_SURFACE)]
+for name, pc, blocks, bc in cases:
+    c = synth.CONFIGS[name]
+    rf, tf, pf = c.faces()
+    br = c.br0()
+    t0 = time.time()
+    with Pot3d(rf, tf, pf, br, bc=bc, pc=pc, rank=rank, nranks=world, pc2_blocks=blocks) as s:
+        res = s.solve(rtol=1e-9)
+        br_f, bt_f, bp_f = s.field()
+        phi = gather_slabs(torch.from_numpy(res.phi).cuda(), c.nr)
+        brg = gather_slabs(torch.from_numpy(np.ascontiguousarray(br_f)).cuda(), c.nr + 1)
+    if rank == 0:
+        import oracle
+
+        ref = oracle.solve(rf, tf, pf, br, bc=bc, pc=pc, pc2_blocks=world * blocks, rtol=1e-9)
+        phi = phi.cpu().numpy()
+        rel = np.linalg.norm(phi - ref["x"]) / np.linalg.norm(ref["x"])
+        obr, _, _ = oracle.field(rf, tf, pf, br, ref["x"], bc=bc)
+        ferr = np.abs(brg.cpu().numpy() - obr).max() / np.abs(obr).max()
+        ok = abs(res.iters - ref["iters"]) <= 1 and rel <= 1e-9 and ferr <= 1e-7
+        fails += 0 if ok else 1
+        print(f"[{world} ranks] {name} pc{pc} blocks/rank {blocks} bc {bc}: iters {res.iters} "
+              f"(oracle {ref['iters']}) rel {rel:.2e} field {ferr:.2e} true_res "
+              f"{res.true_rel_residual:.2e} {'OK' if ok else 'FAIL'} ({time.time() - t0:.1f}s)",
+              flush=True)
+dist.barrier()
+dist.destroy_process_group()
+sys.exit(1 if fails else 0)
