@@ -32,6 +32,8 @@ struct pot3d_ctx {
   // runtime
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t comm_stream = nullptr;          // NCCL halo exchange (overlapped with pass A)
+  cudaEvent_t ev_edge = nullptr, ev_halo = nullptr;
   void *(*ualloc)(size_t, void *) = nullptr;
   void (*ufree)(void *, void *) = nullptr;
   void *actx = nullptr;
@@ -207,18 +209,19 @@ int gather_sums(pot3d_ctx *ctx, int count) {
 }
 
 // halo exchange of one shell per r face of a cell array with ghost shells
-int halo_exchange(pot3d_ctx *ctx, double *a) {
+int halo_exchange(pot3d_ctx *ctx, double *a, cudaStream_t st = nullptr) {
   if (ctx->nranks == 1) return 0;
+  if (!st) st = ctx->stream;
   const Grid &G = ctx->G;
   const size_t cnt = (size_t)G.plane;
   NK(ncclGroupStart());
   if (ctx->rank > 0) {
-    NK(ncclSend(a + sidx(G, 0), cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
-    NK(ncclRecv(a + sidx(G, -1), cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+    NK(ncclSend(a + sidx(G, 0), cnt, ncclDouble, ctx->rank - 1, ctx->comm, st));
+    NK(ncclRecv(a + sidx(G, -1), cnt, ncclDouble, ctx->rank - 1, ctx->comm, st));
   }
   if (ctx->rank < ctx->nranks - 1) {
-    NK(ncclSend(a + sidx(G, G.nr_loc - 1), cnt, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
-    NK(ncclRecv(a + sidx(G, G.nr_loc), cnt, ncclDouble, ctx->rank + 1, ctx->comm, ctx->stream));
+    NK(ncclSend(a + sidx(G, G.nr_loc - 1), cnt, ncclDouble, ctx->rank + 1, ctx->comm, st));
+    NK(ncclRecv(a + sidx(G, G.nr_loc), cnt, ncclDouble, ctx->rank + 1, ctx->comm, st));
   }
   NK(ncclGroupEnd());
   return 0;
@@ -299,19 +302,55 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   dim3 grd(G.ntj * G.ntk, G.nchunks);
   const bool pc2 = ctx->pc == 2;
   const bool multi = ctx->nranks > 1;
-  if (multi) {
+  if (multi && G.nr_loc >= 3) {
+    // edge shells first; their halo travels on the comm stream while pass A
+    // covers the interior shells, then pass A finishes the two edge shells
     k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
                                                 ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0);
     CK(cudaGetLastError());
     ctx->n_enq++;
-    TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
-  }
-  if (pc2)
-    k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, a, parity);
-  else
-    k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, a, parity);
-  CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev_edge, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_edge, 0));
+    TRY(halo_exchange(ctx, ctx->P[parity ^ 1], ctx->comm_stream));
+    CK(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
+    const int nci = std::max(1, std::min(G.nchunks, G.nr_loc - 2));
+    const int ntl = G.ntj * G.ntk;
+    PassArgs ai = a, ae = a;
+    ai.G.part = 1;
+    ai.G.nchunks = nci;
+    ai.G.blk_off = 0;
+    ai.G.blk_total = ntl * (nci + 2);
+    ae.G.part = 2;
+    ae.G.blk_off = ntl * nci;
+    ae.G.blk_total = ntl * (nci + 2);
+    if (pc2)
+      k_pass_a_pc2<<<dim3(ntl, nci), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ai, parity);
+    else
+      k_pass_a_pc1<<<dim3(ntl, nci), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ai, parity);
+    CK(cudaGetLastError());
     ctx->n_enq++;
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+    if (pc2)
+      k_pass_a_pc2<<<dim3(ntl, 2), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ae, parity);
+    else
+      k_pass_a_pc1<<<dim3(ntl, 2), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ae, parity);
+    CK(cudaGetLastError());
+    ctx->n_enq++;
+  } else {
+    if (multi) {
+      k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
+                                                  ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0);
+      CK(cudaGetLastError());
+      ctx->n_enq++;
+      TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
+    }
+    if (pc2)
+      k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, a, parity);
+    else
+      k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, a, parity);
+    CK(cudaGetLastError());
+    ctx->n_enq++;
+  }
   if (multi) {
     TRY(gather_sums(ctx, 1));
     k_finalize_alpha<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks);
@@ -565,6 +604,11 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
     ctx->own_stream = true;
   }
 
+  if (ctx->nranks > 1) {
+    CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_edge, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+  }
   // r-slab of this rank: union of its pc2_blocks consecutive blocks
   std::vector<int> bi0(B), bi1(B);
   for (int b = 0; b < B; b++) block_bounds(nr, B, b, bi0[b], bi1[b]);
@@ -630,7 +674,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   if (pc == POT3D_PC2) DA(ctx->z, cells);
   DA(ctx->bshell, G.plane + 16); DA(ctx->br_dev, G.plane + 16); DA(ctx->mean2, 2);
   DA(ctx->S, 1);
-  ctx->partials_len = 4 * (size_t)std::max<long long>(pass_blocks(ctx), 4096);
+  ctx->partials_len = 4 * (size_t)std::max<long long>((long long)G.ntj * G.ntk * (G.nchunks + 2), 65536);
   DA(ctx->partials, ctx->partials_len);
   DA(ctx->local_sum, 2);
   DA(ctx->gathered, 2 * (size_t)ctx->nranks + 2);
@@ -1046,6 +1090,9 @@ int pot3d_destroy(pot3d_ctx *ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   dfree_all(ctx);
   if (ctx->hS) cudaFreeHost(ctx->hS);
+  if (ctx->ev_edge) cudaEventDestroy(ctx->ev_edge);
+  if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return 0;

@@ -41,10 +41,11 @@ __device__ __forceinline__ void block_sum(double (&v)[N], double *sred) {
 // where `tot` then holds the grid total in every thread 0.
 template <int N>
 __device__ __forceinline__ bool grid_sum(double (&v)[N], double *partials, unsigned int *counter, double *sred,
-                         double (&tot)[N], int bid = -1) {
+                         double (&tot)[N], int bid = -1, int nb = -1) {
   __shared__ bool s_last;
-  const int nb = gridDim.x * gridDim.y;
-  // bid: a deterministic identity of the block's work (default: blockIdx)
+  // bid: a deterministic identity of the block's work (default: blockIdx); nb:
+  // the number of blocks of the reduction (several launches may share it)
+  if (nb < 0) nb = gridDim.x * gridDim.y;
   if (bid < 0) bid = blockIdx.x + gridDim.x * blockIdx.y;
   block_sum<N>(v, sred);
   if (threadIdx.x == 0) {

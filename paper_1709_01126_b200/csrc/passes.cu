@@ -46,9 +46,22 @@ static_assert((TR * SROW * 8) % 128 == 0 && (TJ * TKB * 8) % 128 == 0, "TMA boxe
 static_assert(TR % RPW == 0 && TKB == 2 * 32 && TK == TKB - 2, "tile geometry");
 
 __device__ __forceinline__ void chunk_bounds(const Grid &G, int c, int &c0, int &c1) {
-  int base = G.nr_loc / G.nchunks, rem = G.nr_loc % G.nchunks;
-  c0 = c * base + (c < rem ? c : rem);
+  if (G.part == 2) {  // the two edge shells
+    c0 = (c == 0) ? 0 : G.nr_loc - 1;
+    c1 = c0 + 1;
+    return;
+  }
+  const int s0 = (G.part == 1) ? 1 : 0, n = (G.part == 1) ? G.nr_loc - 2 : G.nr_loc;
+  int base = n / G.nchunks, rem = n % G.nchunks;
+  c0 = s0 + c * base + (c < rem ? c : rem);
   c1 = c0 + base + (c < rem ? 1 : 0);
+}
+
+__device__ __forceinline__ int pass_bid(const Grid &G) {
+  return G.blk_off + blockIdx.x + gridDim.x * blockIdx.y;
+}
+__device__ __forceinline__ int pass_nb(const Grid &G) {
+  return G.blk_total > 0 ? G.blk_total : gridDim.x * gridDim.y;
 }
 
 // Column metric factors of the tile per smem index i (logical column k0-3+i,
@@ -303,7 +316,8 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   }
 
   double v[1] = {acc}, tot[1];
-  if (grid_sum<1>(v, A.partials, &S->counter[0], sred, tot) && threadIdx.x == 0) {
+  if (grid_sum<1>(v, A.partials, &S->counter[0], sred, tot, pass_bid(G), pass_nb(G)) &&
+      threadIdx.x == 0) {
     if (A.finalize)
       finalize_alpha(S, tot[0]);
     else
@@ -436,7 +450,8 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   }
 
   double v[2] = {acc_rz, acc_rr}, tot[2];
-  if (grid_sum<2>(v, A.partials, &S->counter[1], sred, tot) && threadIdx.x == 0) {
+  if (grid_sum<2>(v, A.partials, &S->counter[1], sred, tot, pass_bid(G), pass_nb(G)) &&
+      threadIdx.x == 0) {
     if (A.finalize) {
       if (USE_Z)
         finalize_rr(S, tot[1], A.hist);  // PC2: rho' comes from the sweeps

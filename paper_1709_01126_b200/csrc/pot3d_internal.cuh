@@ -87,6 +87,11 @@ struct Grid {
   long long plane;    // nt * PK
   int nchunks;        // r chunks per fused pass
   int ntj, ntk;       // tiles
+  // per-launch split of the fused passes (halo overlap):
+  //   part 0: all shells in nchunks chunks; part 1: shells [1, nr_loc-1) in
+  //   nchunks chunks; part 2: the two edge shells (blockIdx.y = 0 / 1).
+  int part;
+  int blk_off, blk_total;  // this launch's blocks within a reduction spanning launches
 };
 
 // Physical column of logical phi index k is k + COFF: physical 0 is the
