@@ -839,6 +839,10 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
   CK(cudaStreamSynchronize(s));
   const Scalars hs = *ctx->hS;
   ctx->last_iters = hs.iter;
+  if (ctx->pc == 2 && (pc2_status(ctx->pc2, s) & 2)) {
+    ctx->err = "PC2 sweep handoff protocol error (bounded wait expired)";
+    return POT3D_ERR_CUDA;
+  }
   if (hs.status == -4) {
     if (getenv("POT3D_DEBUG")) {  // diagnostics: scalars and non-finite counts of the vectors
       fprintf(stderr, "POT3D_DEBUG iter %lld rho %g alpha %g beta %g sigma %g rr %g bnorm %g\n",

@@ -14,14 +14,17 @@
 // i+j+k, tiled: a CTA owns a WJ x WK theta-phi tile over all shells of one
 // block and walks its own hyperplanes (thread (jj,kk) handles shell
 // t-jj-kk at step t, neighbours inside the tile through a shared double
-// buffer, the r neighbour in a register); tiles wait on the published
-// progress of the tiles above / to the left (acquire/release flags), CTAs
-// take tiles in topological order from a ticket counter so that every tile
-// a CTA waits on belongs to a CTA that is already running.  Every cell is
+// buffer, the r neighbour in a register); the values a tile needs from the
+// tiles above / to the left arrive through sentinel-armed edge slots (no
+// flags, no fences), CTAs take tiles in topological order from a ticket
+// counter so that every tile a CTA waits on belongs to a CTA that is already
+// running, and every wait is bounded.  Every cell is
 // computed by exactly the sequential formula, only the order of the three
 // neighbour terms is fixed (r, theta, phi), so the sweep equals the
 // sequential ILU0 solve up to rounding.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "device_common.cuh"
@@ -31,11 +34,7 @@ namespace pot3d {
 constexpr int WJ = 8;            // tile rows (theta)
 constexpr int WK = 32;           // tile columns (phi): one warp per row
 constexpr int WT = WJ * WK;      // threads per CTA
-#ifndef POT3D_SWEEP_PUB
-#define POT3D_SWEEP_PUB 4
-#endif
-constexpr int PUB = POT3D_SWEEP_PUB;      // publish progress every PUB steps (a release costs an L2 round trip)
-constexpr long long SPIN_LIMIT = 1ll << 28;  // bounded waits: a protocol error never hangs the GPU
+
 
 enum SweepMode { SW_FACTOR = 0, SW_FWD = 1, SW_BWD = 2 };
 
@@ -45,8 +44,11 @@ struct Pc2 {
   int ntj, ntk, ntiles;     // tile grid
   int *d_l0;                // block bounds: nblk+1 local shell indices
   int2 *d_order;            // tiles in topological (start-time) order
-  int *d_sync;              // [0] ticket, [1] breakdown flag, [2..] progress per (block, tile)
+  int *d_sync;              // [0] ticket, [1] flags: 1 breakdown, 2 handoff protocol error
   int nsync;
+  double *edge;             // tile-edge handoff slots (sentinel-armed)
+  long long edge_len;       // doubles
+  int nbmax;                // largest block (shells)
   double *inv_d;            // 1/d_m, cell layout
   std::vector<void *> allocs;
   size_t bytes;
@@ -64,27 +66,42 @@ struct SweepArgs {
   double *z;         // FWD: writes w; BWD: w -> z in place
   double *inv_d;     // FACTOR writes, FWD/BWD read
   double *partials;
+  double *edge;
+  int nbmax;
   int predicated;    // skip when the PCG loop has stopped
   int finalize;      // BWD: 1 single rank (rho/beta), 0 local_sum
   double *local_sum;
 };
 
-__device__ __forceinline__ int ld_acquire(const int *p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int *p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-
+// Tile-edge handoff without flags or fences: the bottom row / right column of
+// every tile is also written into an edge buffer whose slots hold a sentinel
+// (a signalling-NaN bit pattern arithmetic never produces) until the producer
+// stores the value; the single consumer prefetches the slot PD steps ahead with
+// ld.global.cv, polls only while it still reads the sentinel, and re-arms it.
+constexpr unsigned SENT32 = 0x7FF57FF5u;
+constexpr unsigned long long SENT = 0x7FF57FF57FF57FF5ull;
+constexpr long long SPIN_LIMIT = 1ll << 26;  // bounded waits: a protocol error never hangs the GPU
 #ifndef POT3D_SWEEP_D
 #define POT3D_SWEEP_D 8
 #endif
-constexpr int PD = POT3D_SWEEP_D;  // prefetch distance (steps): operands of step t+PD load at step t
+constexpr int PD = POT3D_SWEEP_D;  // prefetch distance (steps)
 
+// polling load: volatile asm so the compiler cannot hoist it out of a spin loop
+__device__ __forceinline__ double ld_poll(const double *p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ bool is_sent(double v) {
+  return (unsigned long long)__double_as_longlong(v) == SENT;
+}
+
+#ifndef POT3D_SWEEP_MINB
+#define POT3D_SWEEP_MINB 1
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
+__global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
   const Grid &G = A.G;
   const Metrics &M = A.M;
   if (A.predicated && A.S->stop) return;
@@ -108,11 +125,20 @@ __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
   const int j = rev ? G.nt - 1 - jv : jv;
   const int k = rev ? G.np - 1 - kv : kv;
   const int jc = valid ? j : 0, kc = valid ? k : 0;
-  int *prog = A.sync + 2 + b * A.ntiles;
-  const int my = tl.x * A.ntk + tl.y;
-  const int up = (tl.x > 0) ? (tl.x - 1) * A.ntk + tl.y : -1;
-  const int lf = (tl.y > 0) ? tl.x * A.ntk + tl.y - 1 : -1;
   const int nsteps = nb + WJ + WK - 2;
+  // edge buffers of this tile (producer) and of its up / left neighbours (consumer)
+  const int my = tl.x * A.ntk + tl.y;
+  const long long tstride = (long long)A.nbmax * (WK + WJ);
+  double *eb_base = A.edge + (long long)b * A.ntiles * tstride;
+  // slots are plane-contiguous per column/row: [kk][iv] and [jj][iv]
+  double *my_bot = eb_base + my * tstride + (long long)kk * A.nbmax;
+  double *my_rgt = eb_base + my * tstride + (long long)A.nbmax * (WK + jj);
+  const bool put_bot = valid && (jj == WJ - 1) && (jv + 1 < G.nt);
+  const bool put_rgt = valid && (kk == WK - 1) && (kv + 1 < G.np);
+  const bool need_j = valid && (jj == 0) && (jv > 0);
+  const bool need_k = valid && (kk == 0) && (kv > 0);
+  double *up_bot = need_j ? eb_base + (long long)(my - A.ntk) * tstride + (long long)kk * A.nbmax : nullptr;
+  double *lf_rgt = need_k ? eb_base + (long long)(my - 1) * tstride + (long long)A.nbmax * (WK + jj) : nullptr;
 
   // row / column factors
   const double g = __ldg(M.g + jc), q = __ldg(M.q + jc);
@@ -121,19 +147,16 @@ __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
   // couplings to the virtual predecessors (zero across the pole / the dropped wrap)
   const double ct = rev ? atp : atm;                                              // x dr_i dp_k
   const double cp = rev ? ((k < G.np - 1) ? app : 0.0) : ((k > 0) ? apm : 0.0);  // x dr_i q_j
-  const long long dj = rev ? G.PK : -G.PK;  // real offset of the theta predecessor
-  const long long dk = rev ? 1 : -1;        // real offset of the phi predecessor
   const long long o_base = cidx(G, rev ? l1 - 1 : l0, jc, kc);
   const long long o_step = rev ? -G.plane : G.plane;  // one virtual shell
   const int ig_base = G.i0 + (rev ? l1 - 1 : l0), ig_step = rev ? -1 : 1;
-  const bool need_j = (jj == 0) && (jv > 0), need_k = (kk == 0) && (kv > 0);
-  const double *nsrc = (MODE == SW_FACTOR) ? A.inv_d : A.z;
 
   // prefetch ring: operands of the cell this thread handles at step t+PD
   double ra[PD], rb[PD], rc[PD], rnj[PD], rnk[PD];
   auto fetch = [&](int ts, double &xa, double &xb, double &xc, double &xj, double &xk) {
     const int iv = ts - jj - kk;
-    xa = xb = xc = xj = xk = 0.0;
+    xa = xb = xc = 0.0;
+    xj = xk = 0.0;
     if (valid && iv >= 0 && iv < nb) {
       const long long o = o_base + (long long)iv * o_step;
       if (MODE == SW_FWD) {
@@ -144,27 +167,12 @@ __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
         xb = __ldg(A.inv_d + o);
         xc = __ldg(A.r + o);    // r of this cell for the r.z partial
       }
-      if (need_j) xj = __ldcg(nsrc + o + dj);
-      if (need_k) xk = __ldcg(nsrc + o + dk);
+      // neighbour-tile values: prefetched, re-polled at use if still the sentinel
+      if (need_j) xj = ld_poll(up_bot + iv);
+      if (need_k) xk = ld_poll(lf_rgt + iv);
     }
   };
-  int have_up = 0, have_lf = 0;
-  auto wait_neighbours = [&](int need_step) {  // neighbours completed step need_step + W - 1
-    if (up >= 0) {
-      const int need = min(need_step + WJ, nsteps);
-      long long spins = 0;
-      while (have_up < need && spins++ < SPIN_LIMIT) have_up = ld_acquire(prog + up);
-      if (have_up < need) atomicOr(&A.sync[1], 2);  // protocol error: flag, never hang
-    }
-    if (lf >= 0) {
-      const int need = min(need_step + WK, nsteps);
-      long long spins = 0;
-      while (have_lf < need && spins++ < SPIN_LIMIT) have_lf = ld_acquire(prog + lf);
-      if (have_lf < need) atomicOr(&A.sync[1], 2);
-    }
-  };
-  if (tid == 0) wait_neighbours(PD - 1);
-  __syncthreads();
+  bool proto = false;
 #pragma unroll
   for (int u = 0; u < PD; u++) fetch(u, ra[u], rb[u], rc[u], rnj[u], rnk[u]);
 
@@ -175,23 +183,30 @@ __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
     for (int u = 0; u < PD; u++) {
       const int t = t0 + u;
       if (t >= nsteps) break;
-      __syncthreads();  // step t-1 complete in this CTA
-      if (tid == 0) {
-        if (t > 0 && (t % PUB) == 0) st_release(prog + my, t);
-        wait_neighbours(t + PD);
-      }
-      __syncthreads();
-      // operands of step t (fetched PD steps ago), then prefetch step t+PD
-      const double a0 = ra[u], b0 = rb[u], c0 = rc[u], nj = rnj[u], nk = rnk[u];
+      __syncthreads();  // step t-1 complete in this CTA (shared double buffer)
+      const double a0 = ra[u], b0 = rb[u], c0 = rc[u];
+      double nj = rnj[u], nk = rnk[u];
       fetch(t + PD, ra[u], rb[u], rc[u], rnj[u], rnk[u]);
       const int ivt = t - jj - kk;  // virtual local shell of this thread at step t
       if (valid && ivt >= 0 && ivt < nb) {
+        if (need_j) {  // value of the tile above (virtual), produced at its step t+WJ-1
+          long long spins = 0;
+          while (is_sent(nj) && spins++ < SPIN_LIMIT) nj = ld_poll(up_bot + ivt);
+          proto |= is_sent(nj);
+          __stcg(reinterpret_cast<unsigned long long *>(up_bot + ivt), SENT);  // re-arm
+        }
+        if (need_k) {
+          long long spins = 0;
+          while (is_sent(nk) && spins++ < SPIN_LIMIT) nk = ld_poll(lf_rgt + ivt);
+          proto |= is_sent(nk);
+          __stcg(reinterpret_cast<unsigned long long *>(lf_rgt + ivt), SENT);
+        }
         const long long o = o_base + (long long)ivt * o_step;
         const int ig = ig_base + ivt * ig_step;
         const double dr = __ldg(M.dr + ig);
         const double vi = (ivt > 0) ? wprev : 0.0;
-        const double vj = (jj > 0) ? sw[(t - 1) & 1][jj - 1][kk] : nj;
-        const double vk = (kk > 0) ? sw[(t - 1) & 1][jj][kk - 1] : nk;
+        const double vj = (jj > 0) ? sw[(t - 1) & 1][jj - 1][kk] : (need_j ? nj : 0.0);
+        const double vk = (kk > 0) ? sw[(t - 1) & 1][jj][kk - 1] : (need_k ? nk : 0.0);
         const double cr = (ivt > 0) ? (rev ? __ldg(M.arp + ig) : __ldg(M.arm + ig)) : 0.0;
         const double Ar = cr * g * dpk, At = dr * ct * dpk, Ap = dr * q * cp;
         double val;
@@ -212,13 +227,14 @@ __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
           A.z[o] = val;
           acc += c0 * val;
         }
+        if (put_bot) __stcg(my_bot + ivt, val);
+        if (put_rgt) __stcg(my_rgt + ivt, val);
         wprev = val;
         sw[t & 1][jj][kk] = val;
       }
     }
   }
-  __syncthreads();
-  if (tid == 0) st_release(prog + my, nsteps);
+  if (__syncthreads_or(proto) && tid == 0) atomicOr(&A.sync[1], 2);  // protocol error
   if (MODE == SW_FACTOR) {
     if (__syncthreads_or(bad) && tid == 0) atomicOr(&A.sync[1], 1);
   }
@@ -232,6 +248,12 @@ __global__ void __launch_bounds__(WT) k_sweep(SweepArgs A) {
         A.local_sum[0] = tot[0];
     }
   }
+}
+
+__global__ void k_fill_u64(unsigned long long *a, long long n, unsigned long long v) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x)
+    a[c] = v;
 }
 
 // periodic ghost columns of z (read by the TMA boxes of pass A)
@@ -268,14 +290,21 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
   P->ntj = (G.nt + WJ - 1) / WJ;
   P->ntk = (G.np + WK - 1) / WK;
   P->ntiles = P->ntj * P->ntk;
-  P->nsync = 2 + P->nblk * P->ntiles;
+  P->nsync = 2;
+  {
+    std::vector<int> l(block_l0, block_l0 + nblocks_local + 1);
+    P->nbmax = 0;
+    for (int q = 0; q < nblocks_local; q++) P->nbmax = std::max(P->nbmax, l[q + 1] - l[q]);
+  }
+  P->edge_len = (long long)P->nblk * P->ntiles * P->nbmax * (WJ + WK);
   P->bytes = 0;
   P->d_l0 = (int *)p_alloc(P, sizeof(int) * (nblocks_local + 1), alloc, actx);
   P->d_order = (int2 *)p_alloc(P, sizeof(int2) * P->ntiles, alloc, actx);
   P->d_sync = (int *)p_alloc(P, sizeof(int) * P->nsync, alloc, actx);
   const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
   P->inv_d = (double *)p_alloc(P, sizeof(double) * cells, alloc, actx);
-  if (!P->d_l0 || !P->d_order || !P->d_sync || !P->inv_d) {
+  P->edge = (double *)p_alloc(P, sizeof(double) * P->edge_len, alloc, actx);
+  if (!P->d_l0 || !P->d_order || !P->d_sync || !P->inv_d || !P->edge) {
     *out = P;
     return -1;
   }
@@ -293,6 +322,7 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
   cudaMemcpyAsync(P->d_order, order.data(), sizeof(int2) * P->ntiles, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(P->d_l0, block_l0, sizeof(int) * (nblocks_local + 1), cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(P->inv_d, 0, sizeof(double) * cells, s);
+  k_fill_u64<<<1024, 256, 0, s>>>(reinterpret_cast<unsigned long long *>(P->edge), P->edge_len, SENT);
   *out = P;
   return cudaStreamSynchronize(s) == cudaSuccess ? 0 : -1;
 }
@@ -314,6 +344,8 @@ static SweepArgs sweep_args(Pc2 *P, const Metrics &M, Scalars *S, const double *
   a.z = z;
   a.inv_d = P->inv_d;
   a.partials = partials;
+  a.edge = P->edge;
+  a.nbmax = P->nbmax;
   a.predicated = predicated;
   a.finalize = finalize;
   a.local_sum = local_sum;
@@ -328,7 +360,9 @@ int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host)
   int flags[2];
   cudaMemcpyAsync(flags, P->d_sync, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
-  *min_pivot_host = flags[1] ? 0.0 : 1.0;  // breakdown (pivot <= 1e-300) -> 0
+  if (getenv("POT3D_DEBUG")) fprintf(stderr, "POT3D_DEBUG pc2_factor flags %d\n", flags[1]);
+  if (flags[1] & 2) return -1;             // handoff protocol error
+  *min_pivot_host = (flags[1] & 1) ? 0.0 : 1.0;  // breakdown (pivot <= 1e-300) -> 0
   return 0;
 }
 
@@ -337,9 +371,9 @@ int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, 
               int finalize, double *local_sum, cudaStream_t s, bool iteration) {
   const int pred = iteration ? 1 : 0;
   SweepArgs a = sweep_args(P, M, S, r, z, partials, pred, finalize, local_sum);
-  cudaMemsetAsync(P->d_sync, 0, sizeof(int) * P->nsync, s);
+  cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);  // ticket only (flags accumulate)
   k_sweep<SW_FWD><<<P->nblk * P->ntiles, WT, 0, s>>>(a);
-  cudaMemsetAsync(P->d_sync, 0, sizeof(int) * P->nsync, s);
+  cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);
   if (!iteration) a.finalize = 0, a.local_sum = local_sum;
   k_sweep<SW_BWD><<<P->nblk * P->ntiles, WT, 0, s>>>(a);
   const Grid &G = P->G;
@@ -347,6 +381,20 @@ int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, 
                 s>>>(G, z, S, pred);
   if (cudaGetLastError() != cudaSuccess) return -1;
   return 3;
+}
+
+// flags of the last sweeps (1: pivot breakdown, 2: handoff protocol error); a
+// protocol error re-arms every edge slot so the next solve starts clean
+int pc2_status(Pc2 *P, cudaStream_t s) {
+  int f = 0;
+  cudaMemcpyAsync(&f, P->d_sync + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  if (f & 2) {
+    k_fill_u64<<<1024, 256, 0, s>>>(reinterpret_cast<unsigned long long *>(P->edge), P->edge_len, SENT);
+    cudaMemsetAsync(P->d_sync + 1, 0, sizeof(int), s);
+    cudaStreamSynchronize(s);
+  }
+  return f;
 }
 
 void pc2_destroy(Pc2 *P, void (*fr)(void *, void *), void *actx) {

@@ -41,7 +41,10 @@ constexpr int TK = 62;          // interior phi columns per tile: lane l owns lo
                                 // columns k0-1+2l, k0+2l (lanes 0/31 hold the halo columns)
 constexpr int TJ = 14;          // interior theta rows per tile
 constexpr int TR = TJ + 2;      // haloed rows
-constexpr int RPW = 2;          // haloed rows per warp (each lane: 2 rows x 2 phi cells)
+#ifndef POT3D_RPW
+#define POT3D_RPW 2
+#endif
+constexpr int RPW = POT3D_RPW;  // haloed rows per warp (each lane: RPW rows x 2 phi cells)
 constexpr int NWARPS = TR / RPW;
 constexpr int NTHREADS = NWARPS * 32;
 constexpr int SROW = 68;        // smem row: index i <-> logical column k0-3+i (2..65 used)
@@ -200,6 +203,7 @@ int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host)
 int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, double *partials,
               int finalize, double *local_sum, cudaStream_t s, bool iteration);
 void pc2_destroy(Pc2 *P, void (*fr)(void *, void *), void *actx);
+int pc2_status(Pc2 *P, cudaStream_t s);
 size_t pc2_bytes(const Pc2 *P);
 int pc2_kernels_per_apply(const Pc2 *P);
 

@@ -6,10 +6,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "d4p4": ["POT3D_SWEEP_D=4", "POT3D_SWEEP_PUB=4"],
-    "d8p4": ["POT3D_SWEEP_D=8", "POT3D_SWEEP_PUB=4"],
-    "d8p2": ["POT3D_SWEEP_D=8", "POT3D_SWEEP_PUB=2"],
-    "d16p4": ["POT3D_SWEEP_D=16", "POT3D_SWEEP_PUB=4"],
+    "sd4m3": ["POT3D_SWEEP_D=4", "POT3D_SWEEP_MINB=3"],
+    "sd4m4": ["POT3D_SWEEP_D=4", "POT3D_SWEEP_MINB=4"],
+    "sd2m4": ["POT3D_SWEEP_D=2", "POT3D_SWEEP_MINB=4"],
+    "sd8m2": ["POT3D_SWEEP_D=8", "POT3D_SWEEP_MINB=2"],
 }
 out = Path(build.PKG) / "variants"
 out.mkdir(exist_ok=True)
