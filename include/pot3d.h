@@ -148,6 +148,12 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info);
 int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_pass_b,
                   double *ms_precond);
 
+/* Diagnostics: one PCG iteration at a time (no graph) with CUDA events on the
+ * context stream after every sub-step (kernels and collectives); returns the
+ * number n of sub-steps, ms[q] their mean duration and `names` (>= 1024 bytes)
+ * their ';'-separated names.  Invalidates the last solution. */
+int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *names, int32_t nmax);
+
 /* Rank 0 creates the 128-byte NCCL unique id that every rank passes in
  * pot3d_runtime.nccl_unique_id (the caller broadcasts it, e.g. with
  * torch.distributed).  Returns 0 or POT3D_ERR_NCCL. */

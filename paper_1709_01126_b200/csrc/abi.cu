@@ -296,6 +296,25 @@ PassArgs make_args(pot3d_ctx *ctx, int parity) {
 //   pass A  (p_new, q = A p_new, sigma partial, lazy x update) -> alpha
 //   pass B  (r -= alpha q, PC1: rho', ||r||^2)                 -> convergence, beta
 //   [PC2]   forward + backward D-ILU sweeps (z, rho')           -> beta
+// optional timing hook: records an event on the main stream after each sub-step
+struct StepTimer {
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char *> name;
+  cudaStream_t s;
+  void mark(const char *n) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+    name.push_back(n);
+  }
+};
+static StepTimer *g_timer = nullptr;
+#define MARK(n) \
+  do {          \
+    if (g_timer) g_timer->mark(n); \
+  } while (0)
+
 int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   const Grid &G = ctx->G;
   PassArgs a = make_args(ctx, parity);
@@ -309,6 +328,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
                                                 ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0);
     CK(cudaGetLastError());
     ctx->n_enq++;
+    MARK("edge_p");
     CK(cudaEventRecord(ctx->ev_edge, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_edge, 0));
     TRY(halo_exchange(ctx, ctx->P[parity ^ 1], ctx->comm_stream));
@@ -329,13 +349,16 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
       k_pass_a_pc1<<<dim3(ntl, nci), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ai, parity);
     CK(cudaGetLastError());
     ctx->n_enq++;
+    MARK("passA_interior");
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+    MARK("halo_wait");
     if (pc2)
       k_pass_a_pc2<<<dim3(ntl, 2), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ae, parity);
     else
       k_pass_a_pc1<<<dim3(ntl, 2), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ae, parity);
     CK(cudaGetLastError());
     ctx->n_enq++;
+    MARK("passA_edge");
   } else {
     if (multi) {
       k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
@@ -353,9 +376,11 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   }
   if (multi) {
     TRY(gather_sums(ctx, 1));
+    MARK("allgather_sigma");
     k_finalize_alpha<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks);
     CK(cudaGetLastError());
     ctx->n_enq++;
+    MARK("finalize_alpha");
   }
   if (pc2)
     k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, a, parity);
@@ -363,8 +388,10 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, a, parity);
   CK(cudaGetLastError());
     ctx->n_enq++;
+  MARK("passB");
   if (multi) {
     TRY(gather_sums(ctx, 2));
+    MARK("allgather_rz_rr");
     if (pc2)
       k_finalize_rr<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks, ctx->hist);
     else
@@ -1083,6 +1110,56 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
   if (ms_precond) *ms_precond = tp / iters;
   ctx->solved = false;
   return 0;
+}
+
+int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *names, int32_t nmax) {
+  if (!ctx || iters < 1 || !ms || !names || nmax < 1) return POT3D_ERR_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemcpyAsync(ctx->hS, ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  Scalars h = *ctx->hS;
+  h.stop = 0;
+  h.status = 0;
+  h.rtol = 0.0;
+  h.maxit = h.iter + iters + 2;
+  if (!(h.rho != 0.0)) h.rho = 1.0;
+  if (!(h.bnorm > 0.0)) h.bnorm = 1.0;
+  *ctx->hS = h;
+  CK(cudaMemcpyAsync(ctx->S, ctx->hS, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+  std::vector<double> acc;
+  std::vector<const char *> nm;
+  for (int it = 0; it < iters; it++) {
+    StepTimer T;
+    T.s = s;
+    g_timer = &T;
+    T.mark("start");
+    int rc = enqueue_iteration(ctx, (int)((h.iter + it) & 1));
+    g_timer = nullptr;
+    if (rc < 0) return rc;
+    CK(cudaStreamSynchronize(s));
+    if (acc.empty()) {
+      acc.assign(T.ev.size(), 0.0);
+      nm = T.name;
+    }
+    for (size_t q = 1; q < T.ev.size() && q < acc.size(); q++) {
+      float f = 0;
+      cudaEventElapsedTime(&f, T.ev[q - 1], T.ev[q]);
+      acc[q] += f;
+    }
+    for (auto e : T.ev) cudaEventDestroy(e);
+  }
+  int n = (int)std::min<size_t>(acc.size() - 1, (size_t)nmax);
+  std::string all;
+  for (int q = 0; q < n; q++) {
+    ms[q] = acc[q + 1] / iters;
+    all += nm[q + 1];
+    all += ";";
+  }
+  strncpy(names, all.c_str(), 1023);
+  names[1023] = 0;
+  ctx->solved = false;
+  return n;
 }
 
 int pot3d_destroy(pot3d_ctx *ctx) {

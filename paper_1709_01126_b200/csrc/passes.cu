@@ -82,30 +82,41 @@ __device__ __forceinline__ void load_tile_const(TileConst &tc, const Grid &G, co
   }
 }
 
-// Per-plane r metric factors through pointers advanced one shell per plane
-// (the metric arrays carry one padding entry on each side for ghost shells).
-struct PlanePtr {
-  const double *arp, *arm, *dr, *ss;
-  __device__ __forceinline__ PlaneC get() const {
-    PlaneC c;
-    c.arp = __ldg(arp);
-    c.arm = __ldg(arm);
-    c.dr = __ldg(dr);
-    c.ss = __ldg(ss);
-    return c;
-  }
-  __device__ __forceinline__ void next() { ++arp; ++arm; ++dr; ++ss; }
-};
-__device__ __forceinline__ PlanePtr plane_ptr(const Metrics &M, int ig) {
-  PlanePtr p;
-  p.arp = M.arp + ig;
-  p.arm = M.arm + ig;
-  p.dr = M.dr + ig;
-  p.ss = M.ss + ig;
-  return p;
-}
-
 __device__ __forceinline__ int wrap_inc(int s, int n) { return (s + 1 == n) ? 0 : s + 1; }
+
+// r-metric factors of the chunk's shells (c0-1 .. c1) staged in shared memory once
+// per block, so the per-plane reads are shared-memory broadcasts instead of L2
+// round trips on the plane loop's critical path.  Chunks longer than PLMAX-2
+// shells read the arrays directly.
+constexpr int PLMAX = 320;
+struct PlaneSm {
+  double arp[PLMAX], arm[PLMAX], dr[PLMAX], ss[PLMAX];
+};
+__device__ __forceinline__ void load_planes(PlaneSm &ps, const Metrics &M, int ig0, int n) {
+  for (int q = threadIdx.x; q < n && q < PLMAX; q += blockDim.x) {
+    ps.arp[q] = __ldg(M.arp + ig0 + q);
+    ps.arm[q] = __ldg(M.arm + ig0 + q);
+    ps.dr[q] = __ldg(M.dr + ig0 + q);
+    ps.ss[q] = __ldg(M.ss + ig0 + q);
+  }
+}
+// metrics of shell il = c0-1+q
+__device__ __forceinline__ PlaneC plane_at(const PlaneSm &ps, const Metrics &M, int ig0, int q,
+                                           bool staged) {
+  PlaneC c;
+  if (staged) {
+    c.arp = ps.arp[q];
+    c.arm = ps.arm[q];
+    c.dr = ps.dr[q];
+    c.ss = ps.ss[q];
+  } else {
+    c.arp = __ldg(M.arp + ig0 + q);
+    c.arm = __ldg(M.arm + ig0 + q);
+    c.dr = __ldg(M.dr + ig0 + q);
+    c.ss = __ldg(M.ss + ig0 + q);
+  }
+  return c;
+}
 
 // (A p)_m = dp_k [g_j (arp (c - p_{i+1}) + arm (c - p_{i-1}) + ss c) + dr (atp (c - p_{j+1})
 //           + atm (c - p_{j-1}))] + dr q_j (app (c - p_{k+1}) + apm (c - p_{k-1}))
@@ -191,9 +202,13 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   __shared__ double sred[NTHREADS / 32];
   __shared__ TileConst tcs;
 
+  __shared__ PlaneSm pls;
   const TileThread t = tile_thread(G);
   const int L = t.c1 - t.c0;
   load_tile_const(tcs, G, M, t.k0);
+  const int ig0 = G.i0 + t.c0 - 1;           // global shell of plane q = 0
+  const bool staged = (L + 2) <= PLMAX;
+  load_planes(pls, M, ig0, L + 2);
   const int cs = 2 + 2 * t.lane;  // smem index of element 0
   const double beta = S->beta;
   const long long PL = G.plane;
@@ -244,8 +259,6 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
 #pragma unroll
     for (int e = 0; e < RPW; e++) R[u][e] = Z2;
   double *g_pn = A.p_new + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: p_k at plane c0
-  PlanePtr pp = plane_ptr(M, G.i0 + t.c0 - 1);  // metrics of the transformed plane
-  PlanePtr ps = plane_ptr(M, G.i0 + t.c0);      // metrics of the stencil plane
   double acc = 0.0;
   unsigned ph = 0;  // mbarrier parity of the current group of 3 planes
 
@@ -259,8 +272,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
     const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
     const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
-    const PlaneC P = pp.get();
-    pp.next();
+    const PlaneC P = plane_at(pls, M, ig0, q, staged);
     mbar_wait(&sm.bar[u], ph);
     // ---- transform plane il -> p_k ----
 #pragma unroll
@@ -284,8 +296,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     if (q >= 1 && q <= L) g_pn += PL;
     // ---- stencil of plane il-1 (its slot was completed before this barrier) ----
     if (q >= 2) {
-      const PlaneC Ps = ps.get();
-      ps.next();
+      const PlaneC Ps = plane_at(pls, M, ig0, q - 1, staged);
       const double *sb = &sm.pn[um][0][0];
 #pragma unroll
       for (int e = 0; e < RPW; e++) {
@@ -339,9 +350,13 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   __shared__ double sred[2 * NTHREADS / 32];
   __shared__ TileConst tcs;
 
+  __shared__ PlaneSm pls;
   const TileThread t = tile_thread(G);
   const int L = t.c1 - t.c0;
   load_tile_const(tcs, G, M, t.k0);
+  const int ig0 = G.i0 + t.c0 - 1;
+  const bool staged = (L + 2) <= PLMAX;
+  load_planes(pls, M, ig0, L + 2);
   const int cs = 2 + 2 * t.lane;
   const double alpha = S->alpha;
   const long long PL = G.plane;
@@ -383,7 +398,6 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   double acc_rz = 0.0, acc_rr = 0.0;
   double *g_w = A.r_out + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: r of plane c0
   double *g_x = A.x + (long long)(t.c0 + 1) * PL;      // + rowoff[e]: x of plane c0
-  PlanePtr ps = plane_ptr(M, G.i0 + t.c0);             // metrics of the stencil plane
   int st = 0, so = NS_B - 1;                           // stages of planes q and q-1
   unsigned ph = 0;
 
@@ -394,8 +408,7 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
     const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
     const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
     const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
-    PlaneC P;
-    if (q >= 2) P = ps.get();
+    const PlaneC P = plane_at(pls, M, ig0, q >= 1 ? q - 1 : 0, staged);  // stencil plane il-1
     mbar_wait(&sm.bar[st], ph);
 #pragma unroll
     for (int e = 0; e < RPW; e++) pn[e] = *reinterpret_cast<const double2 *>(&sm.pn[st][t.row[e]][cs]);
@@ -435,7 +448,6 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
           if (t.st1) g_x[t.rowoff[e] + 1] = xn.y;
         }
       }
-      ps.next();
       g_w += PL;
       g_x += PL;
     }

@@ -32,7 +32,8 @@ STATUS_NAMES = {0: "ok", 1: "not_converged", 2: "pc2_fell_back", -1: "invalid", 
                 -3: "nccl", -4: "indefinite", -5: "oom", -6: "state"}
 
 EXPORTS = ["pot3d_setup", "pot3d_set_br0", "pot3d_solve", "pot3d_field", "pot3d_apply",
-           "pot3d_precond", "pot3d_history", "pot3d_info", "pot3d_profile", "pot3d_nccl_unique_id",
+           "pot3d_precond", "pot3d_history", "pot3d_info", "pot3d_profile",
+           "pot3d_profile_iteration", "pot3d_nccl_unique_id",
            "pot3d_destroy", "pot3d_last_error"]
 
 _ALLOC = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
@@ -98,6 +99,7 @@ def library(build_if_missing: bool = True):
     L.pot3d_history.restype = ctypes.c_int64
     L.pot3d_info.argtypes = [vp, ctypes.POINTER(_Info)]
     L.pot3d_profile.argtypes = [vp, ctypes.c_int32, d, d, d]
+    L.pot3d_profile_iteration.argtypes = [vp, ctypes.c_int32, d, ctypes.c_char_p, ctypes.c_int32]
     L.pot3d_nccl_unique_id.argtypes = [vp]
     L.pot3d_destroy.argtypes = [vp]
     L.pot3d_last_error.argtypes = [vp]
@@ -311,6 +313,13 @@ class Pot3d:
         self._check(self._L.pot3d_profile(self._ctx, int(iters), ctypes.byref(a), ctypes.byref(b),
                                           ctypes.byref(c)))
         return a.value, b.value, c.value
+
+    def profile_iteration(self, iters=10):
+        """[(sub-step name, mean ms)] of one PCG iteration, events between sub-steps."""
+        ms = (ctypes.c_double * 32)()
+        names = ctypes.create_string_buffer(1024)
+        n = self._check(self._L.pot3d_profile_iteration(self._ctx, int(iters), ms, names, 32))
+        return list(zip(names.value.decode().split(";")[:n], list(ms)[:n]))
 
     def close(self):
         if getattr(self, "_ctx", None):
