@@ -104,6 +104,11 @@ typedef struct {
   int64_t device_bytes;          /* device memory held by the context */
   int64_t kernel_launches;       /* cumulative count of this library's kernels launched
                                     (graph launches counted per kernel node) */
+  int32_t exchange;              /* inter-rank exchange of the PCG loop: 0 single rank,
+                                    1 NCCL (send/recv halo + all-gather of the sums),
+                                    2 peer memory (CUDA IPC over NVLink: the kernels store
+                                    halo shells and sums straight into the peers' buffers) */
+  int32_t reserved;
 } pot3d_info_t;
 
 /* Build the context: metric coefficients (a1), r-slab partition, RHS from

@@ -58,6 +58,13 @@ struct pot3d_ctx {
   double *poles = nullptr;
   Pc2 *pc2 = nullptr;
   TMaps tmaps{};
+  // peer-memory exchange (nranks > 1): P[0], P[1] and the mailbox are cudaMalloc'd
+  // (IPC-exportable) and mapped into the neighbours' / all ranks' address spaces
+  bool xfer_want = false, xfer = false;
+  Mailbox *mail = nullptr;
+  PeerTab *peers = nullptr;           // device copy
+  std::vector<void *> ipc_own, ipc_open;
+  unsigned long long epoch = 0;       // solves (and profile runs) so far
   // graphs
   cudaGraphExec_t gexec = nullptr;
   int graph_unroll = 0;
@@ -128,6 +135,37 @@ void dfree_all(pot3d_ctx *ctx) {
       cudaFree(p);
   }
   ctx->allocs.clear();
+}
+
+// IPC-exportable allocation (plain cudaMalloc: an IPC handle maps a whole allocation)
+template <typename T>
+int ipc_alloc(pot3d_ctx *ctx, T **out, size_t count) {
+  void *p = nullptr;
+  if (cudaMalloc(&p, sizeof(T) * count) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->err = "cudaMalloc of " + std::to_string(sizeof(T) * count) + " bytes failed";
+    return POT3D_ERR_OOM;
+  }
+  ctx->ipc_own.push_back(p);
+  ctx->dev_bytes += sizeof(T) * count;
+  *out = static_cast<T *>(p);
+  return 0;
+}
+
+void ipc_release(pot3d_ctx *ctx) {
+  for (void *p : ctx->ipc_open) cudaIpcCloseMemHandle(p);
+  ctx->ipc_open.clear();
+  if (!ctx->ipc_own.empty() && ctx->comm) {
+    // every rank has stopped touching the peers' buffers before any is freed
+    int *d = nullptr;
+    if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
+      ncclAllReduce(d, d, 1, ncclInt32, ncclSum, ctx->comm, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(d);
+    }
+  }
+  for (void *p : ctx->ipc_own) cudaFree(p);
+  ctx->ipc_own.clear();
 }
 
 bool is_device_ptr(const void *p) {
@@ -227,6 +265,76 @@ int halo_exchange(pot3d_ctx *ctx, double *a, cudaStream_t st = nullptr) {
   return 0;
 }
 
+// Peer-memory exchange setup: the IPC handles of P[0], P[1] and the mailbox are
+// all-gathered over NCCL; each rank maps every mailbox and its neighbours' P
+// arrays.  Enabled only when every rank succeeded (else the NCCL path stays).
+int setup_xfer(pot3d_ctx *ctx) {
+  struct IpcInfo {
+    cudaIpcMemHandle_t h[3];
+    int32_t ok, nr_loc, pad0, pad1;
+  };
+  const int n = ctx->nranks, me = ctx->rank;
+  cudaStream_t s = ctx->stream;
+  IpcInfo mine{};
+  mine.ok = ctx->xfer_want && ctx->mail != nullptr;
+  mine.nr_loc = ctx->G.nr_loc;
+  if (mine.ok && (cudaIpcGetMemHandle(&mine.h[0], ctx->P[0]) != cudaSuccess ||
+                  cudaIpcGetMemHandle(&mine.h[1], ctx->P[1]) != cudaSuccess ||
+                  cudaIpcGetMemHandle(&mine.h[2], ctx->mail) != cudaSuccess)) {
+    cudaGetLastError();
+    mine.ok = 0;
+  }
+  char *d = nullptr;
+  TRY(dalloc(ctx, &d, sizeof(IpcInfo) * (n + 1)));
+  CK(cudaMemcpyAsync(d, &mine, sizeof(IpcInfo), cudaMemcpyHostToDevice, s));
+  NK(ncclAllGather(d, d + sizeof(IpcInfo), sizeof(IpcInfo), ncclChar, ctx->comm, s));
+  std::vector<IpcInfo> all(n);
+  CK(cudaMemcpyAsync(all.data(), d + sizeof(IpcInfo), sizeof(IpcInfo) * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  bool ok = true;
+  for (const IpcInfo &a : all) ok = ok && a.ok;
+  PeerTab T{};
+  T.rank = me;
+  T.nranks = n;
+  T.nr_lo = me > 0 ? all[me - 1].nr_loc : 0;
+  auto open = [&](const cudaIpcMemHandle_t &hd) -> void * {
+    void *p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    ctx->ipc_open.push_back(p);
+    return p;
+  };
+  if (ok) {
+    for (int r = 0; r < n && ok; r++) {
+      T.mail[r] = (r == me) ? ctx->mail : static_cast<Mailbox *>(open(all[r].h[2]));
+      ok = T.mail[r] != nullptr;
+    }
+    for (int q = 0; q < 2 && ok; q++) {
+      if (me > 0) ok = ok && (T.p_lo[q] = static_cast<double *>(open(all[me - 1].h[q]))) != nullptr;
+      if (me < n - 1) ok = ok && (T.p_hi[q] = static_cast<double *>(open(all[me + 1].h[q]))) != nullptr;
+    }
+  }
+  // agreement: all ranks or none
+  int32_t okv = ok ? 1 : 0;
+  CK(cudaMemcpyAsync(d, &okv, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  NK(ncclAllReduce(d, d, 1, ncclInt32, ncclMin, ctx->comm, s));
+  CK(cudaMemcpyAsync(&okv, d, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (!okv) {
+    for (void *p : ctx->ipc_open) cudaIpcCloseMemHandle(p);
+    ctx->ipc_open.clear();
+    ctx->xfer = false;
+    return 0;
+  }
+  TRY(dalloc(ctx, &ctx->peers, 1));
+  CK(cudaMemcpyAsync(ctx->peers, &T, sizeof(PeerTab), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->xfer = true;
+  return 0;
+}
+
 // TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry point)
 PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -321,11 +429,56 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   dim3 grd(G.ntj * G.ntk, G.nchunks);
   const bool pc2 = ctx->pc == 2;
   const bool multi = ctx->nranks > 1;
+  if (ctx->xfer) {
+    // peer memory: edge shells of p_k stored into the neighbours' ghost shells
+    // (flag per iteration); pass A waits for that flag only in the blocks whose
+    // chunk touches a ghost shell (scheduled last); the rank sums go straight into
+    // every rank's mailbox from the reductions' last blocks
+    const PeerTab *pt = ctx->peers;
+    k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
+                                                ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0,
+                                                pt, parity ^ 1);
+    CK(cudaGetLastError());
+    MARK("edge_p");
+    PassArgs ax = a;
+    ax.G.part = 3;
+    ax.peers = pt;
+    if (pc2)
+      k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ax, parity);
+    else
+      k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ax, parity);
+    CK(cudaGetLastError());
+    MARK("passA");
+    k_finalize_mail<<<1, 1, 0, ctx->stream>>>(ctx->S, pt, MAIL_A, 0, nullptr);
+    CK(cudaGetLastError());
+    MARK("finalize_alpha");
+    if (pc2)
+      k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, ax, parity);
+    else
+      k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, ax, parity);
+    CK(cudaGetLastError());
+    MARK("passB");
+    k_finalize_mail<<<1, 1, 0, ctx->stream>>>(ctx->S, pt, MAIL_B, pc2 ? 2 : 1, ctx->hist);
+    CK(cudaGetLastError());
+    MARK("finalize_beta");
+    ctx->n_enq += 5;
+    if (pc2) {
+      int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
+                         ctx->stream, true, pt);
+      TRY(nk);
+      k_finalize_mail<<<1, 1, 0, ctx->stream>>>(ctx->S, pt, MAIL_C, 3, nullptr);
+      CK(cudaGetLastError());
+      ctx->n_enq += nk + 1;
+      MARK("pc2");
+    }
+    return 0;
+  }
   if (multi && G.nr_loc >= 3) {
     // edge shells first; their halo travels on the comm stream while pass A
     // covers the interior shells, then pass A finishes the two edge shells
     k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
-                                                ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0);
+                                                ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0,
+                                                nullptr, 0);
     CK(cudaGetLastError());
     ctx->n_enq++;
     MARK("edge_p");
@@ -362,7 +515,8 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   } else {
     if (multi) {
       k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
-                                                  ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0);
+                                                  ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0,
+                                                nullptr, 0);
       CK(cudaGetLastError());
       ctx->n_enq++;
       TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
@@ -497,13 +651,15 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   info->pc2_blocks_total = ctx->pc2_blocks * ctx->nranks;
   int64_t k = 2;
   if (ctx->nranks > 1) k += 3;
-  if (ctx->pc == 2 && ctx->pc2) k += pc2_kernels_per_apply(ctx->pc2);
+  if (ctx->pc == 2 && ctx->pc2) k += pc2_kernels_per_apply(ctx->pc2) + (ctx->nranks > 1 ? 1 : 0);
   info->graph_kernels_per_iter = k;
   // algorithmic bytes: PC1 64 B/cell (pass A 24 + pass B 40), PC2 + 56 B sweeps
   const int64_t cells = (int64_t)ctx->G.nr_loc * ctx->nt * ctx->np;
   info->bytes_per_iter = (ctx->pc == 2 ? 120 : 64) * cells;
   info->device_bytes = (int64_t)ctx->dev_bytes;
   info->kernel_launches = ctx->n_launch;
+  info->exchange = ctx->nranks == 1 ? 0 : (ctx->xfer ? 2 : 1);
+  info->reserved = 0;
   return 0;
 }
 
@@ -552,6 +708,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
     *out = nullptr;
     g_setup_error = ctx->err;  // reachable through pot3d_last_error(NULL)
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    ipc_release(ctx);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     dfree_all(ctx);
     if (ctx->hS) cudaFreeHost(ctx->hS);
@@ -697,7 +854,19 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
 
   // vectors with ghost shells
   const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
-  DA(ctx->x, cells); DA(ctx->r, cells); DA(ctx->P[0], cells); DA(ctx->P[1], cells);
+  DA(ctx->x, cells); DA(ctx->r, cells);
+  {
+    const char *xe = getenv("POT3D_XFER");
+    ctx->xfer_want = ctx->nranks > 1 && ctx->nranks <= MAXR && !(xe && atoi(xe) == 0);
+  }
+  if (ctx->xfer_want) {
+    if ((rc = ipc_alloc(ctx, &ctx->P[0], cells)) || (rc = ipc_alloc(ctx, &ctx->P[1], cells)) ||
+        (rc = ipc_alloc(ctx, &ctx->mail, 1)))
+      return fail(rc);
+    if (cudaMemsetAsync(ctx->mail, 0, sizeof(Mailbox), ctx->stream)) { ctx->err = "memset"; return fail(POT3D_ERR_CUDA); }
+  } else {
+    DA(ctx->P[0], cells); DA(ctx->P[1], cells);
+  }
   if (pc == POT3D_PC2) DA(ctx->z, cells);
   DA(ctx->bshell, G.plane + 16); DA(ctx->br_dev, G.plane + 16); DA(ctx->mean2, 2);
   DA(ctx->S, 1);
@@ -723,6 +892,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
       ctx->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(nr_);
       return fail(POT3D_ERR_NCCL);
     }
+    if ((rc = setup_xfer(ctx))) return fail(rc);
   }
 
   if (pc == POT3D_PC2) {
@@ -800,6 +970,7 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
     ctx->n_launch++;
   }
   Scalars h0{};
+  h0.epoch = ++ctx->epoch;
   h0.rtol = rtol;
   h0.maxit = (long long)std::min<int64_t>(maxit, hlen - 1);
   CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
@@ -868,6 +1039,10 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
   ctx->last_iters = hs.iter;
   if (ctx->pc == 2 && (pc2_status(ctx->pc2, s) & 2)) {
     ctx->err = "PC2 sweep handoff protocol error (bounded wait expired)";
+    return POT3D_ERR_CUDA;
+  }
+  if (hs.xfer_error || hs.status == -5) {
+    ctx->err = "peer-memory exchange: bounded wait expired (a rank stalled or diverged)";
     return POT3D_ERR_CUDA;
   }
   if (hs.status == -4) {
@@ -1045,7 +1220,7 @@ int pot3d_precond(pot3d_ctx *ctx, const double *rin, double *zout) {
     // PC1: the edge-plane kernel computes z = D^-1 r (beta = 0) over any planes
     Scalars h0{};
     CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
-    k_edge_p<<<148 * 8, 256, 0, s>>>(G, ctx->M, ctx->S, rr, nullptr, zz, -1);
+    k_edge_p<<<148 * 8, 256, 0, s>>>(G, ctx->M, ctx->S, rr, nullptr, zz, -1, nullptr, 0);
     CK(cudaGetLastError());
     ctx->n_launch++;
   }
@@ -1123,6 +1298,7 @@ int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *nam
   h.status = 0;
   h.rtol = 0.0;
   h.maxit = h.iter + iters + 2;
+  h.epoch = ++ctx->epoch;
   if (!(h.rho != 0.0)) h.rho = 1.0;
   if (!(h.bnorm > 0.0)) h.bnorm = 1.0;
   *ctx->hS = h;
@@ -1168,6 +1344,7 @@ int pot3d_destroy(pot3d_ctx *ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->pc2) pc2_destroy(ctx->pc2, ctx->ufree, ctx->actx);
+  ipc_release(ctx);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   dfree_all(ctx);
   if (ctx->hS) cudaFreeHost(ctx->hS);

@@ -128,6 +128,75 @@ __device__ __forceinline__ void finalize_rho(Scalars *S, double rz) {
   S->rho = rz;
 }
 // ---------------------------------------------------------------------------
+// Peer-memory exchange (nranks > 1, CUDA IPC over NVLink).  A producer stores its
+// values into the destination's mailbox and then the sequence number with a
+// system-scope release; a consumer spins on the sequence number with a
+// system-scope acquire.  Every wait is bounded (XFER_TIMEOUT_NS of globaltimer)
+// and gives up at once when another waiter has already expired.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long XFER_TIMEOUT_NS = 20000000000ull;  // 20 s
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// generic-proxy data acquired from a peer, about to be read by TMA (async proxy)
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// this rank's (v0, v1) of `kind` into every rank's mailbox
+__device__ __forceinline__ void mail_post(const PeerTab *T, int kind, double v0, double v1,
+                                          unsigned long long seq) {
+  const int me = T->rank;
+  for (int r = 0; r < T->nranks; r++) {
+    MailEntry *e = &T->mail[r]->e[kind][me];
+    *reinterpret_cast<volatile double *>(&e->v0) = v0;
+    *reinterpret_cast<volatile double *>(&e->v1) = v1;
+    st_release_sys(&e->seq, seq);
+  }
+}
+
+// spin until *flag == seq; false (and S->xfer_error set) when the wait expired
+__device__ __forceinline__ bool xfer_wait(const unsigned long long *flag, unsigned long long seq,
+                                          Scalars *S) {
+  if (ld_acquire_sys(flag) == seq) return true;
+  const unsigned long long t0 = global_ns();
+  volatile int *err = &S->xfer_error;
+  while (ld_acquire_sys(flag) != seq) {
+    if (*err || global_ns() - t0 > XFER_TIMEOUT_NS) {
+      *err = 1;
+      return false;
+    }
+  }
+  return true;
+}
+
+// every rank's entry of `kind` for seq, summed in rank order (bit-identical on all ranks)
+__device__ __forceinline__ bool mail_collect(const PeerTab *T, int kind, unsigned long long seq,
+                                             Scalars *S, double &s0, double &s1) {
+  const Mailbox *mb = T->mail[T->rank];
+  s0 = 0.0;
+  s1 = 0.0;
+  for (int r = 0; r < T->nranks; r++) {
+    const MailEntry *e = &mb->e[kind][r];
+    if (!xfer_wait(&e->seq, seq, S)) return false;
+    s0 += *reinterpret_cast<const volatile double *>(&e->v0);
+    s1 += *reinterpret_cast<const volatile double *>(&e->v1);
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // Per-cell helpers.
 // ---------------------------------------------------------------------------
 struct RowC {  // theta factors of one row

@@ -139,11 +139,20 @@ __global__ void k_finalize_rho(Scalars *S, const double *gathered, int nranks) {
 // Edge shells / whole-slab PC1 apply (see pot3d_internal.cuh for the modes).
 // ---------------------------------------------------------------------------
 __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const double *p_old,
-                         double *p_new, int mode) {
+                         double *p_new, int mode, const PeerTab *peers, int parity_new) {
   if (mode >= 0 && S->stop) return;
   const double beta = (mode >= 0) ? S->beta : 0.0;
   const long long per = (long long)G.nt * G.np;
   const long long n = (mode < 0) ? per * G.nr_loc : 2 * per;
+  // peer memory: shell 0 also lands in rank-1's top ghost shell, shell nr_loc-1
+  // in rank+1's bottom ghost shell (same [il+1][j][c] layout, shifted by whole planes)
+  double *lo = nullptr, *hi = nullptr;
+  if (peers) {
+    lo = peers->p_lo[parity_new];
+    hi = peers->p_hi[parity_new];
+    if (lo) lo += (long long)peers->nr_lo * G.plane;
+    if (hi) hi -= (long long)G.nr_loc * G.plane;
+  }
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
        c += (long long)gridDim.x * blockDim.x) {
     long long t = c % per;
@@ -164,7 +173,52 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
     p_new[o] = v;
     if (k == 0) p_new[o + G.np] = v;           // periodic ghost columns
     if (k == G.np - 1) p_new[o - G.np] = v;
+    double *rem = (mode < 0) ? nullptr : (sidx == 0 ? lo : hi);
+    if (rem) {
+      rem[o] = v;
+      if (k == 0) rem[o + G.np] = v;
+      if (k == G.np - 1) rem[o - G.np] = v;
+    }
   }
+  if (peers && mode >= 0) {
+    // all blocks' peer stores are released before the neighbours' flags
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      s_last = atomicAdd(&S->counter[4], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      S->counter[4] = 0u;
+      __threadfence_system();
+      const unsigned long long seq = mail_seq(S->epoch, S->iter + 1);
+      if (peers->rank > 0) st_release_sys(&peers->mail[peers->rank - 1]->halo[1], seq);
+      if (peers->rank < peers->nranks - 1) st_release_sys(&peers->mail[peers->rank + 1]->halo[0], seq);
+    }
+  }
+}
+
+// Peer-memory finalisation (one thread): the reductions of every rank, summed in
+// rank order, then the same scalar updates as the single-rank path.
+__global__ void k_finalize_mail(Scalars *S, const PeerTab *peers, int kind, int what, double *hist) {
+  if (S->stop) return;
+  // kinds A/B belong to iteration iter+1 (iter not yet advanced); C follows finalize_rr
+  const unsigned long long seq = mail_seq(S->epoch, what == 3 ? S->iter : S->iter + 1);
+  double s0, s1;
+  if (!mail_collect(peers, kind, seq, S, s0, s1)) {
+    S->status = -5;
+    S->stop = 1;
+    return;
+  }
+  if (what == 0)
+    finalize_alpha(S, s0);
+  else if (what == 1)
+    finalize_beta(S, s0, s1, hist);
+  else if (what == 2)
+    finalize_rr(S, s1, hist);
+  else
+    finalize_rho(S, s0);
 }
 
 // ---------------------------------------------------------------------------

@@ -146,7 +146,12 @@ __device__ __forceinline__ TileThread tile_thread(const Grid &G) {
   const int tile = blockIdx.x;
   t.j0 = (tile % G.ntj) * TJ;
   t.k0 = (tile / G.ntj) * TK;
-  chunk_bounds(G, blockIdx.y, t.c0, t.c1);
+  // part 3: all shells, the two chunks touching a ghost shell scheduled last (their
+  // blocks wait for the neighbours' halo, which meanwhile arrives in peer memory)
+  int cy = blockIdx.y;
+  if (G.part == 3 && G.nchunks >= 3)
+    cy = (cy < G.nchunks - 2) ? cy + 1 : (cy == G.nchunks - 2 ? 0 : G.nchunks - 1);
+  chunk_bounds(G, cy, t.c0, t.c1);
   const int k = t.k0 - 1 + 2 * t.lane;  // logical column of element 0
 #pragma unroll
   for (int e = 0; e < RPW; e++) {
@@ -226,7 +231,15 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
       const int il = t.c0 - 1 + q;
       if ((il < 0) || (il >= G.nr_loc)) {
         // ghost shell: it holds the final p_k (halo / zeros); p_{k-1} is not loaded
-        // (a fully out-of-range box is not a reliable zero fill)
+        // (a fully out-of-range box is not a reliable zero fill).  With peer
+        // memory the neighbour stores it there: wait for its flag of this iteration.
+        if (A.peers) {
+          const int side = (il < 0) ? 0 : 1;
+          if (side == 0 ? A.peers->rank > 0 : A.peers->rank < A.peers->nranks - 1) {
+            xfer_wait(&A.peers->mail[A.peers->rank]->halo[side], mail_seq(S->epoch, S->iter + 1), S);
+            fence_proxy_async_global();
+          }
+        }
         mbar_arrive_expect_tx(&sm.bar[st], STAGE_BYTES / 2);
         tma_load_3d(&sm.r[st][0][0], map_new, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
       } else {
@@ -331,6 +344,8 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
       threadIdx.x == 0) {
     if (A.finalize)
       finalize_alpha(S, tot[0]);
+    else if (A.peers)
+      mail_post(A.peers, MAIL_A, tot[0], 0.0, mail_seq(S->epoch, S->iter + 1));
     else
       A.local_sum[0] = tot[0];
   }
@@ -469,6 +484,8 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
         finalize_rr(S, tot[1], A.hist);  // PC2: rho' comes from the sweeps
       else
         finalize_beta(S, tot[0], tot[1], A.hist);
+    } else if (A.peers) {
+      mail_post(A.peers, MAIL_B, tot[0], tot[1], mail_seq(S->epoch, S->iter + 1));
     } else {
       A.local_sum[0] = tot[0];
       A.local_sum[1] = tot[1];

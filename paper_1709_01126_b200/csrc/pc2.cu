@@ -71,6 +71,7 @@ struct SweepArgs {
   int predicated;    // skip when the PCG loop has stopped
   int finalize;      // BWD: 1 single rank (rho/beta), 0 local_sum
   double *local_sum;
+  const PeerTab *peers;  // BWD, nranks > 1 with peer memory: post r.z to every mailbox
 };
 
 // Tile-edge handoff without flags or fences: the bottom row / right column of
@@ -244,6 +245,8 @@ __global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
     if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket) && tid == 0) {
       if (A.finalize)
         finalize_rho(A.S, tot[0]);
+      else if (A.peers)
+        mail_post(A.peers, MAIL_C, tot[0], 0.0, mail_seq(A.S->epoch, A.S->iter));
       else
         A.local_sum[0] = tot[0];
     }
@@ -368,9 +371,10 @@ int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host)
 
 // z = M^-1 r; returns the number of kernels launched (memsets excluded) or -1.
 int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, double *partials,
-              int finalize, double *local_sum, cudaStream_t s, bool iteration) {
+              int finalize, double *local_sum, cudaStream_t s, bool iteration, const PeerTab *peers) {
   const int pred = iteration ? 1 : 0;
   SweepArgs a = sweep_args(P, M, S, r, z, partials, pred, finalize, local_sum);
+  a.peers = iteration ? peers : nullptr;
   cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);  // ticket only (flags accumulate)
   k_sweep<SW_FWD><<<P->nblk * P->ntiles, WT, 0, s>>>(a);
   cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);

@@ -80,8 +80,33 @@ struct Scalars {
   long long maxit;
   int stop;          // 1: loop finished (converged, maxit, error)
   int status;        // 0 ok / 1 not converged / -4 indefinite
-  unsigned int counter[4]; // last-block counters
+  unsigned int counter[6]; // last-block counters
+  unsigned long long epoch;  // solve number (peer-memory sequence numbers)
+  int xfer_error;    // peer-memory wait expired
+  int pad1;
 };
+
+// ---- peer-memory exchange between the rank processes (CUDA IPC over NVLink) ----
+constexpr int MAXR = 16;
+struct MailEntry {          // one rank's contribution to a reduction
+  double v0, v1;
+  unsigned long long seq;   // (epoch << 32) | iteration (1-based)
+  unsigned long long pad;
+};
+enum MailKind { MAIL_A = 0, MAIL_B = 1, MAIL_C = 2 };
+struct Mailbox {
+  MailEntry e[3][MAXR];         // [kind][source rank]
+  unsigned long long halo[2];   // ghost shell filled: [0] from rank-1, [1] from rank+1
+  unsigned long long pad[6];
+};
+struct PeerTab {
+  Mailbox *mail[MAXR];          // every rank's mailbox (own included)
+  double *p_lo[2], *p_hi[2];    // P[0], P[1] of rank-1 / rank+1 (nullptr at the ends)
+  int rank, nranks, nr_lo, pad; // nr_lo: nr_loc of rank-1 (its top ghost shell index)
+};
+__host__ __device__ inline unsigned long long mail_seq(unsigned long long epoch, long long iter1) {
+  return (epoch << 32) | (unsigned long long)iter1;
+}
 
 struct Grid {
   int nr, nt, np;     // global cells
@@ -92,7 +117,8 @@ struct Grid {
   int ntj, ntk;       // tiles
   // per-launch split of the fused passes (halo overlap):
   //   part 0: all shells in nchunks chunks; part 1: shells [1, nr_loc-1) in
-  //   nchunks chunks; part 2: the two edge shells (blockIdx.y = 0 / 1).
+  //   nchunks chunks; part 2: the two edge shells (blockIdx.y = 0 / 1); part 3:
+  //   as part 0 with the two chunks next to the ghost shells scheduled last.
   int part;
   int blk_off, blk_total;  // this launch's blocks within a reduction spanning launches
 };
@@ -137,6 +163,7 @@ struct PassArgs {
   double *hist;
   int finalize;         // 1: single rank, finalise scalars in the last block
   double *local_sum;    // nranks > 1: this rank's sums for the all-gather
+  const PeerTab *peers; // nranks > 1 with peer memory: mailbox / ghost-shell exchange
 };
 
 // Arguments of the field kernels (a11).
@@ -191,7 +218,10 @@ __global__ void k_pole_avg(Grid G, const double *x, const double *dp, double per
 // mode -1: z = D^-1 src on every plane (PC1 apply); 0: p_new = D^-1 src + beta p_old on the
 // two edge shells (PC1); 1: p_new = src + beta p_old on the edge shells (PC2, src = z)
 __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const double *p_old,
-                         double *p_new, int mode);
+                         double *p_new, int mode, const PeerTab *peers, int parity_new);
+// peer-memory finalisation: poll every rank's mailbox entry of `kind` for this
+// iteration, sum in rank order, update the scalars (what = 0 alpha, 1 beta, 2 rr, 3 rho)
+__global__ void k_finalize_mail(Scalars *S, const PeerTab *peers, int kind, int what, double *hist);
 
 // pc2.cu -- PC2 (block ILU0 = D-ILU, A11) with tiled sync-free wavefront sweeps
 struct Pc2;
@@ -201,7 +231,8 @@ int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host)
 // z = M^-1 r; partial r.z -> finalize (single rank: rho/beta update, mode iteration) or
 // local_sum[0]; `iteration` selects the predicated in-loop variant.
 int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, double *partials,
-              int finalize, double *local_sum, cudaStream_t s, bool iteration);
+              int finalize, double *local_sum, cudaStream_t s, bool iteration,
+              const PeerTab *peers = nullptr);
 void pc2_destroy(Pc2 *P, void (*fr)(void *, void *), void *actx);
 int pc2_status(Pc2 *P, cudaStream_t s);
 size_t pc2_bytes(const Pc2 *P);

@@ -22,7 +22,7 @@ dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 fails = 0
 cases = [("tiny", 1, 1, synth.SOURCE_SURFACE), ("small", 1, 1, synth.SOURCE_SURFACE),
          ("small", 1, 1, synth.CLOSED_WALL), ("small", 2, 1, synth.SOURCE_SURFACE),
-         ("small", 2, 2, synth.SOURCE_SURFACE)]
+         ("small", 2, 2, synth.SOURCE_SURFACE), ("small", 2, 1, synth.CLOSED_WALL)]
 for name, pc, blocks, bc in cases:
     c = synth.CONFIGS[name]
     rf, tf, pf = c.faces()
@@ -30,6 +30,10 @@ for name, pc, blocks, bc in cases:
     t0 = time.time()
     with Pot3d(rf, tf, pf, br, bc=bc, pc=pc, rank=rank, nranks=world, pc2_blocks=blocks) as s:
         res = s.solve(rtol=1e-9)
+        exch = s.info()["exchange"]
+        # a second solve in the same context (new epoch of the peer sequence numbers)
+        res2 = s.solve(rtol=1e-9)
+        same = res2.iters == res.iters and np.array_equal(res2.phi, res.phi)
         br_f, bt_f, bp_f = s.field()
         phi = gather_slabs(torch.from_numpy(res.phi).cuda(), c.nr)
         brg = gather_slabs(torch.from_numpy(np.ascontiguousarray(br_f)).cuda(), c.nr + 1)
@@ -41,11 +45,12 @@ for name, pc, blocks, bc in cases:
         rel = np.linalg.norm(phi - ref["x"]) / np.linalg.norm(ref["x"])
         obr, _, _ = oracle.field(rf, tf, pf, br, ref["x"], bc=bc)
         ferr = np.abs(brg.cpu().numpy() - obr).max() / np.abs(obr).max()
-        ok = abs(res.iters - ref["iters"]) <= 1 and rel <= 1e-9 and ferr <= 1e-7
+        ok = abs(res.iters - ref["iters"]) <= 1 and rel <= 1e-9 and ferr <= 1e-7 and same
         fails += 0 if ok else 1
         print(f"[{world} ranks] {name} pc{pc} blocks/rank {blocks} bc {bc}: iters {res.iters} "
               f"(oracle {ref['iters']}) rel {rel:.2e} field {ferr:.2e} true_res "
-              f"{res.true_rel_residual:.2e} {'OK' if ok else 'FAIL'} ({time.time() - t0:.1f}s)",
+              f"{res.true_rel_residual:.2e} exchange {exch} repeat {'same' if same else 'DIFF'} "
+              f"{'OK' if ok else 'FAIL'} ({time.time() - t0:.1f}s)",
               flush=True)
 dist.barrier()
 dist.destroy_process_group()
