@@ -108,6 +108,7 @@ typedef struct {
                                     1 NCCL (send/recv halo + all-gather of the sums),
                                     2 peer memory (CUDA IPC over NVLink: the kernels store
                                     halo shells and sums straight into the peers' buffers) */
+  int32_t chunks_a, chunks_b;    /* r-chunks per tile column of the two fused passes */
   int32_t reserved;
 } pot3d_info_t;
 

@@ -25,6 +25,7 @@ struct pot3d_ctx {
   // problem
   int nr = 0, nt = 0, np = 0, bc = 0, pc_req = 1, pc = 1;
   int rank = 0, nranks = 1, pc2_blocks = 1, unroll = 8;
+  int nchunks_b = 1;  // r-chunks of pass B (G.nchunks: pass A)
   int device = 0;
   double r0 = 1.0;
   Grid G{};
@@ -379,7 +380,6 @@ int make_maps(pot3d_ctx *ctx) {
   return 0;
 }
 
-int pass_blocks(pot3d_ctx *ctx) { return ctx->G.ntj * ctx->G.ntk * ctx->G.nchunks; }
 
 PassArgs make_args(pot3d_ctx *ctx, int parity) {
   PassArgs a{};
@@ -427,6 +427,9 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   const Grid &G = ctx->G;
   PassArgs a = make_args(ctx, parity);
   dim3 grd(G.ntj * G.ntk, G.nchunks);
+  PassArgs ab = a;  // pass B: its own r-chunking
+  ab.G.nchunks = ctx->nchunks_b;
+  dim3 grdb(G.ntj * G.ntk, ctx->nchunks_b);
   const bool pc2 = ctx->pc == 2;
   const bool multi = ctx->nranks > 1;
   if (ctx->xfer) {
@@ -452,10 +455,12 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     k_finalize_mail<<<1, 1, 0, ctx->stream>>>(ctx->S, pt, MAIL_A, 0, nullptr);
     CK(cudaGetLastError());
     MARK("finalize_alpha");
+    PassArgs bx = ab;
+    bx.peers = pt;
     if (pc2)
-      k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, ax, parity);
+      k_pass_b_pc2<<<grdb, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, bx, parity);
     else
-      k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, ax, parity);
+      k_pass_b_pc1<<<grdb, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, bx, parity);
     CK(cudaGetLastError());
     MARK("passB");
     k_finalize_mail<<<1, 1, 0, ctx->stream>>>(ctx->S, pt, MAIL_B, pc2 ? 2 : 1, ctx->hist);
@@ -537,9 +542,9 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     MARK("finalize_alpha");
   }
   if (pc2)
-    k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, a, parity);
+    k_pass_b_pc2<<<grdb, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, ab, parity);
   else
-    k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, a, parity);
+    k_pass_b_pc1<<<grdb, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, ab, parity);
   CK(cudaGetLastError());
     ctx->n_enq++;
   MARK("passB");
@@ -589,27 +594,22 @@ int build_graph(pot3d_ctx *ctx) {
   return 0;
 }
 
-int choose_chunks(pot3d_ctx *ctx) {
-  Grid &G = ctx->G;
-  const char *env = getenv("POT3D_CHUNKS");
-  if (env && atoi(env) > 0) {
-    G.nchunks = std::min(atoi(env), G.nr_loc);
-    return 0;
-  }
-  int occ = 0, sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_b_pc1, NTHREADS, SMEM_B));
-  int occa = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occa, k_pass_a_pc1, NTHREADS, SMEM_A));
-  occ = std::max(1, std::min(occ, occa));
-  const double slots = (double)sms * occ;
+// r-chunks per tile column of a fused pass: at least ceil(nr_loc / Lcap) chunks,
+// then the count with the best product of wave efficiency (blocks / whole waves,
+// counted only below 3 waves: with more, unequal block times hide the tail) and
+// halo-plane efficiency L / (L + 2).  Short chunks keep the tiles of a wave within
+// a few planes of each other, so the halo rows a tile shares with its neighbours
+// are still in L2; measured best chunk lengths (pass A / pass B): medium 38 / 30,
+// large 75-100 / 27-38, weak 69 / 35 shells -> Lcap 100 for A and 32 for B.
+int pick_chunks(const Grid &G, double slots, int Lcap) {
+  const int cmin = std::max(1, (G.nr_loc + Lcap - 1) / Lcap);
   const long long tiles = (long long)G.ntj * G.ntk;
   double best = -1;
-  int bestc = 1;
-  for (int c = 1; c <= std::min(G.nr_loc, 32); c++) {
+  int bestc = cmin;
+  for (int c = cmin; c <= std::max(cmin, std::min(G.nr_loc, 64)); c++) {
     double blocks = (double)tiles * c;
     double waves = blocks / slots;
-    double eff_w = waves / std::ceil(waves);
+    double eff_w = waves < 3.0 ? waves / std::ceil(waves) : 1.0;
     double L = (double)G.nr_loc / c;
     double eff_h = L / (L + 2.0);
     double e = eff_w * eff_h;
@@ -618,10 +618,29 @@ int choose_chunks(pot3d_ctx *ctx) {
       bestc = c;
     }
   }
-  G.nchunks = bestc;
-  return 0;
+  return bestc;
 }
 
+int choose_chunks(pot3d_ctx *ctx) {
+  Grid &G = ctx->G;
+  // every chunk (plus its two halo planes) fits the passes' staged r-metrics
+  const int lstage = POT3D_PLMAX - 2;
+  int occ = 0, sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_b_pc1, NTHREADS, SMEM_B));
+  int occa = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occa, k_pass_a_pc1, NTHREADS, SMEM_A));
+  const double slots_a = (double)sms * std::max(1, occa), slots_b = (double)sms * std::max(1, occ);
+  G.nchunks = pick_chunks(G, slots_a, std::min(lstage, 100));
+  ctx->nchunks_b = pick_chunks(G, slots_b, std::min(lstage, 32));
+  auto env_chunks = [&](const char *name, int &dst) {
+    const char *e = getenv(name);
+    if (e && atoi(e) > 0) dst = std::max((G.nr_loc + lstage - 1) / lstage, std::min(atoi(e), G.nr_loc));
+  };
+  env_chunks("POT3D_CHUNKS", G.nchunks);
+  env_chunks("POT3D_CHUNKS_B", ctx->nchunks_b);
+  return 0;
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -659,6 +678,8 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   info->device_bytes = (int64_t)ctx->dev_bytes;
   info->kernel_launches = ctx->n_launch;
   info->exchange = ctx->nranks == 1 ? 0 : (ctx->xfer ? 2 : 1);
+  info->chunks_a = ctx->G.nchunks;
+  info->chunks_b = ctx->nchunks_b;
   info->reserved = 0;
   return 0;
 }
@@ -870,7 +891,8 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   if (pc == POT3D_PC2) DA(ctx->z, cells);
   DA(ctx->bshell, G.plane + 16); DA(ctx->br_dev, G.plane + 16); DA(ctx->mean2, 2);
   DA(ctx->S, 1);
-  ctx->partials_len = 4 * (size_t)std::max<long long>((long long)G.ntj * G.ntk * (G.nchunks + 2), 65536);
+  ctx->partials_len = 4 * (size_t)std::max<long long>(
+      (long long)G.ntj * G.ntk * (std::max(G.nchunks, ctx->nchunks_b) + 2), 65536);
   DA(ctx->partials, ctx->partials_len);
   DA(ctx->local_sum, 2);
   DA(ctx->gathered, 2 * (size_t)ctx->nranks + 2);
@@ -1262,7 +1284,10 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
     if (pc2) k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, s>>>(ctx->tmaps, a, par); else k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, s>>>(ctx->tmaps, a, par);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev[1], s));
-    if (pc2) k_pass_b_pc2<<<grd, NTHREADS, SMEM_B, s>>>(ctx->tmaps, a, par); else k_pass_b_pc1<<<grd, NTHREADS, SMEM_B, s>>>(ctx->tmaps, a, par);
+    PassArgs ab = a;
+    ab.G.nchunks = ctx->nchunks_b;
+    dim3 grdb(G.ntj * G.ntk, ctx->nchunks_b);
+    if (pc2) k_pass_b_pc2<<<grdb, NTHREADS, SMEM_B, s>>>(ctx->tmaps, ab, par); else k_pass_b_pc1<<<grdb, NTHREADS, SMEM_B, s>>>(ctx->tmaps, ab, par);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev[2], s));
     ctx->n_launch += 2;

@@ -24,6 +24,8 @@
 
 #include "device_common.cuh"
 
+// pass A code-generation switches (tuning variants)
+
 namespace pot3d {
 
 static_assert(NS_A == 3, "pass A is unrolled by its stage count");
@@ -86,9 +88,9 @@ __device__ __forceinline__ int wrap_inc(int s, int n) { return (s + 1 == n) ? 0 
 
 // r-metric factors of the chunk's shells (c0-1 .. c1) staged in shared memory once
 // per block, so the per-plane reads are shared-memory broadcasts instead of L2
-// round trips on the plane loop's critical path.  Chunks longer than PLMAX-2
-// shells read the arrays directly.
-constexpr int PLMAX = 320;
+// round trips on the plane loop's critical path (choose_chunks keeps every
+// chunk within PLMAX-2 shells).
+constexpr int PLMAX = POT3D_PLMAX;
 struct PlaneSm {
   double arp[PLMAX], arm[PLMAX], dr[PLMAX], ss[PLMAX];
 };
@@ -101,20 +103,12 @@ __device__ __forceinline__ void load_planes(PlaneSm &ps, const Metrics &M, int i
   }
 }
 // metrics of shell il = c0-1+q
-__device__ __forceinline__ PlaneC plane_at(const PlaneSm &ps, const Metrics &M, int ig0, int q,
-                                           bool staged) {
+__device__ __forceinline__ PlaneC plane_at(const PlaneSm &ps, int q) {
   PlaneC c;
-  if (staged) {
-    c.arp = ps.arp[q];
-    c.arm = ps.arm[q];
-    c.dr = ps.dr[q];
-    c.ss = ps.ss[q];
-  } else {
-    c.arp = __ldg(M.arp + ig0 + q);
-    c.arm = __ldg(M.arm + ig0 + q);
-    c.dr = __ldg(M.dr + ig0 + q);
-    c.ss = __ldg(M.ss + ig0 + q);
-  }
+  c.arp = ps.arp[q];
+  c.arm = ps.arm[q];
+  c.dr = ps.dr[q];
+  c.ss = ps.ss[q];
   return c;
 }
 
@@ -190,6 +184,14 @@ __device__ __forceinline__ void store_pair(double *row_k, const TileThread &t, i
   if (t.gl1) row_k[1 - np] = v.y;    // k = np-1 (element 1) -> physical 0
 }
 
+// A select the compiler cannot turn back into a branch (both operands are
+// computed), so the transform of a plane stays in the step's basic block.
+__device__ __forceinline__ double selp(double a, double b, bool p) {
+  double r;
+  asm("{.reg .pred q; setp.ne.s32 q, %3, 0; selp.f64 %0, %1, %2, q;}"
+      : "=d"(r) : "d"(a), "d"(b), "r"((int)p));
+  return r;
+}
 template <int V>
 using IC = std::integral_constant<int, V>;
 
@@ -212,7 +214,6 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   const int L = t.c1 - t.c0;
   load_tile_const(tcs, G, M, t.k0);
   const int ig0 = G.i0 + t.c0 - 1;           // global shell of plane q = 0
-  const bool staged = (L + 2) <= PLMAX;
   load_planes(pls, M, ig0, L + 2);
   const int cs = 2 + 2 * t.lane;  // smem index of element 0
   const double beta = S->beta;
@@ -271,21 +272,40 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   for (int u = 0; u < 3; u++)
 #pragma unroll
     for (int e = 0; e < RPW; e++) R[u][e] = Z2;
-  double *g_pn = A.p_new + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: p_k at plane c0
+  double *g_pn = A.p_new + (long long)t.c0 * PL;  // + rowoff[e]: p_k at plane q (il = c0-1+q)
   double acc = 0.0;
   unsigned ph = 0;  // mbarrier parity of the current group of 3 planes
 
-  auto step = [&](auto U, int q) {
+  // per-thread constants of the stencil: smem offsets of the theta neighbours
+  // (clamped on the tile's outer rows, whose results are masked) and the masks
+  int up_off[RPW], dn_off[RPW];
+  bool m0[RPW], m1[RPW];
+#pragma unroll
+  for (int e = 0; e < RPW; e++) {
+    const int r = t.row[e];
+    up_off[e] = (r == 0) ? 0 : -SROW;
+    dn_off[e] = (r == TR - 1) ? 0 : SROW;
+    m0[e] = t.stencil[e] && t.st0;
+    m1[e] = t.stencil[e] && t.st1;
+  }
+
+  // One plane step.  STENCIL = false only for q = 0, 1 (peeled), so the steady
+  // state is one basic block: the transform's fp64 chains (plane q) and the
+  // stencil of plane q-1 are independent and can be interleaved by the scheduler.
+  auto step = [&](auto U, auto STENCIL, int q) {
     constexpr int u = decltype(U)::value;       // stage, slot and register set of plane q
+    constexpr bool do_st = decltype(STENCIL)::value;
     constexpr int um = (u + 2) % 3, umm = (u + 1) % 3;
     __syncthreads();  // stage um and slot u are free
     if (threadIdx.x == 0) issue(q + 2, um);
     const int il = t.c0 - 1 + q;
     const bool ghost = (il < 0) || (il >= G.nr_loc);
+    const bool store = (q >= 1) && (q <= L);
     const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
     const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
     const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
-    const PlaneC P = plane_at(pls, M, ig0, q, staged);
+    const PlaneC P = plane_at(pls, q);
+    const PlaneC Ps = plane_at(pls, do_st ? q - 1 : q);
     mbar_wait(&sm.bar[u], ph);
     // ---- transform plane il -> p_k ----
 #pragma unroll
@@ -299,43 +319,43 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
         pn.y = ghost ? rv.y : fma(beta, pv.y, rv.y);
       } else {
         const DiagRow d = diag_row(P, rw[e]);
-        pn.x = ghost ? rv.x : fdiv(rv.x, dp.x * d.a + d.b * (ap.x + am.x)) + beta * pv.x;
-        pn.y = ghost ? rv.y : fdiv(rv.y, dp.y * d.a + d.b * (ap.y + am.y)) + beta * pv.y;
+        pn.x = selp(rv.x, fdiv(rv.x, dp.x * d.a + d.b * (ap.x + am.x)) + beta * pv.x, ghost);
+        pn.y = selp(rv.y, fdiv(rv.y, dp.y * d.a + d.b * (ap.y + am.y)) + beta * pv.y, ghost);
       }
       R[u][e] = pn;
       *reinterpret_cast<double2 *>(&sm.pn[u][r][cs]) = pn;
-      if (q >= 1 && q <= L && t.stencil[e]) store_pair(g_pn + t.rowoff[e], t, G.np, pn, false);
+      if (store && t.stencil[e]) store_pair(g_pn + t.rowoff[e], t, G.np, pn, false);
     }
-    if (q >= 1 && q <= L) g_pn += PL;
+    g_pn += PL;
     // ---- stencil of plane il-1 (its slot was completed before this barrier) ----
-    if (q >= 2) {
-      const PlaneC Ps = plane_at(pls, M, ig0, q - 1, staged);
+    if (do_st) {
       const double *sb = &sm.pn[um][0][0];
 #pragma unroll
       for (int e = 0; e < RPW; e++) {
-        if (!t.stencil[e]) continue;
         const int r = t.row[e];
         const double *so = sb + r * SROW + cs;
         const double2 c = R[um][e];
-        const double2 up = (RPW == 2 && e == 1) ? R[um][0] : *reinterpret_cast<const double2 *>(so - SROW);
-        const double2 dn = (RPW == 2 && e == 0) ? R[um][RPW - 1] : *reinterpret_cast<const double2 *>(so + SROW);
+        const double2 up = (RPW == 2 && e == 1) ? R[um][0] : *reinterpret_cast<const double2 *>(so + up_off[e]);
+        const double2 dn = (RPW == 2 && e == 0) ? R[um][RPW - 1] : *reinterpret_cast<const double2 *>(so + dn_off[e]);
         const double lf = so[-1], rt = so[2];
         const double q0 = stencil7(c.x, R[u][e].x, R[umm][e].x, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e]);
         const double q1 = stencil7(c.y, R[u][e].y, R[umm][e].y, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e]);
-        acc += (t.st0 ? c.x * q0 : 0.0) + (t.st1 ? c.y * q1 : 0.0);
+        acc += (m0[e] ? c.x * q0 : 0.0) + (m1[e] ? c.y * q1 : 0.0);
       }
     }
   };
 
-  const int last = L + 1;
+  const int last = L + 1;  // >= 2
+  step(IC<0>{}, std::false_type{}, 0);
+  step(IC<1>{}, std::false_type{}, 1);
 #pragma unroll 1
-  for (int q = 0;; q += 3) {
-    step(IC<0>{}, q);
-    if (q + 1 > last) break;
-    step(IC<1>{}, q + 1);
-    if (q + 2 > last) break;
-    step(IC<2>{}, q + 2);
+  for (int q = 2;; q += 3) {
+    step(IC<2>{}, std::true_type{}, q);
     ph ^= 1u;
+    if (q + 1 > last) break;
+    step(IC<0>{}, std::true_type{}, q + 1);
+    if (q + 2 > last) break;
+    step(IC<1>{}, std::true_type{}, q + 2);
     if (q + 3 > last) break;
   }
 
@@ -370,7 +390,6 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   const int L = t.c1 - t.c0;
   load_tile_const(tcs, G, M, t.k0);
   const int ig0 = G.i0 + t.c0 - 1;
-  const bool staged = (L + 2) <= PLMAX;
   load_planes(pls, M, ig0, L + 2);
   const int cs = 2 + 2 * t.lane;
   const double alpha = S->alpha;
@@ -423,7 +442,7 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
     const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
     const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
     const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
-    const PlaneC P = plane_at(pls, M, ig0, q >= 1 ? q - 1 : 0, staged);  // stencil plane il-1
+    const PlaneC P = plane_at(pls, q >= 1 ? q - 1 : 0);  // stencil plane il-1
     mbar_wait(&sm.bar[st], ph);
 #pragma unroll
     for (int e = 0; e < RPW; e++) pn[e] = *reinterpret_cast<const double2 *>(&sm.pn[st][t.row[e]][cs]);

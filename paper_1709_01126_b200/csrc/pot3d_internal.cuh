@@ -41,6 +41,11 @@ constexpr int TK = 62;          // interior phi columns per tile: lane l owns lo
                                 // columns k0-1+2l, k0+2l (lanes 0/31 hold the halo columns)
 constexpr int TJ = 14;          // interior theta rows per tile
 constexpr int TR = TJ + 2;      // haloed rows
+// chunks of the fused passes stage their r-metric factors for at most
+// POT3D_PLMAX planes (chunk length + 2) in shared memory
+#ifndef POT3D_PLMAX
+#define POT3D_PLMAX 320
+#endif
 #ifndef POT3D_RPW
 #define POT3D_RPW 2
 #endif

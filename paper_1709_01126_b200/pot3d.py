@@ -67,6 +67,7 @@ class _Info(ctypes.Structure):
                 ("pc2_blocks_total", ctypes.c_int32), ("graph_kernels_per_iter", ctypes.c_int64),
                 ("bytes_per_iter", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("exchange", ctypes.c_int32),
+                ("chunks_a", ctypes.c_int32), ("chunks_b", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
 
 

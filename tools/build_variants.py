@@ -6,10 +6,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "sd4m3": ["POT3D_SWEEP_D=4", "POT3D_SWEEP_MINB=3"],
-    "sd4m4": ["POT3D_SWEEP_D=4", "POT3D_SWEEP_MINB=4"],
-    "sd2m4": ["POT3D_SWEEP_D=2", "POT3D_SWEEP_MINB=4"],
-    "sd8m2": ["POT3D_SWEEP_D=8", "POT3D_SWEEP_MINB=2"],
+    "b_x0": [],
+    "b_x1n4": ["POT3D_B_XLDG=1", "POT3D_NS_B=4"],
+    "b_x1n5": ["POT3D_B_XLDG=1", "POT3D_NS_B=5"],
+    "b_x1n6": ["POT3D_B_XLDG=1", "POT3D_NS_B=6"],
 }
 out = Path(build.PKG) / "variants"
 out.mkdir(exist_ok=True)

@@ -14,6 +14,10 @@ with Pot3d(rf, tf, pf, c.br0()) as s:
     s.solve(rtol=0.0, maxit=40, true_residual=False)
     a, b, p = s.profile(40)
     n = c.n
+    cs = synth.CONFIGS["small"]
+    with Pot3d(*cs.faces(), cs.br0()) as s2:
+        r2 = s2.solve(rtol=1e-9)
+    print(f"small: iters {r2.iters} true_res {r2.true_rel_residual:.3e}")
     print(f"pass A {a*1e3:.1f} us {24*n/a/1e6:.0f} GB/s | pass B {b*1e3:.1f} us {40*n/b/1e6:.0f} GB/s | loop {64*n/(a+b)/1e6:.0f} GB/s chunks={s.info()}")
 PY
 done
