@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/pot3d.h"
@@ -26,6 +27,7 @@ struct pot3d_ctx {
   int nr = 0, nt = 0, np = 0, bc = 0, pc_req = 1, pc = 1;
   int rank = 0, nranks = 1, pc2_blocks = 1, unroll = 8;
   int nchunks_b = 1;  // r-chunks of pass B (G.nchunks: pass A)
+  bool pdl = true;    // programmatic dependent launch for the loop kernels (POT3D_PDL=0: off)
   int device = 0;
   double r0 = 1.0;
   Grid G{};
@@ -167,6 +169,25 @@ void ipc_release(pot3d_ctx *ctx) {
   }
   for (void *p : ctx->ipc_own) cudaFree(p);
   ctx->ipc_own.clear();
+}
+
+// Kernel launch, optionally with the programmatic-dependent-launch attribute: the
+// kernel may begin (its prologue) while the previous kernel on the stream drains;
+// every kernel launched this way calls pdl_wait() before reading its inputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t s, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? at : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 bool is_device_ptr(const void *p) {
@@ -438,33 +459,26 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     // chunk touches a ghost shell (scheduled last); the rank sums go straight into
     // every rank's mailbox from the reductions' last blocks
     const PeerTab *pt = ctx->peers;
-    k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
-                                                ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0,
-                                                pt, parity ^ 1);
-    CK(cudaGetLastError());
+    CK(launch_k(ctx->pdl, k_edge_p, dim3(148 * 4), dim3(256), 0, ctx->stream, G, ctx->M, ctx->S,
+                (const double *)(pc2 ? ctx->z : ctx->r), (const double *)ctx->P[parity],
+                ctx->P[parity ^ 1], pc2 ? 1 : 0, pt, parity ^ 1));
     MARK("edge_p");
     PassArgs ax = a;
     ax.G.part = 3;
     ax.peers = pt;
-    if (pc2)
-      k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ax, parity);
-    else
-      k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ax, parity);
-    CK(cudaGetLastError());
+    CK(launch_k(ctx->pdl, pc2 ? k_pass_a_pc2 : k_pass_a_pc1, grd, dim3(NTHREADS), SMEM_A,
+                ctx->stream, ctx->tmaps, ax, parity));
     MARK("passA");
-    k_finalize_mail<<<1, 1, 0, ctx->stream>>>(ctx->S, pt, MAIL_A, 0, nullptr);
-    CK(cudaGetLastError());
+    CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_A, 0,
+                (double *)nullptr));
     MARK("finalize_alpha");
     PassArgs bx = ab;
     bx.peers = pt;
-    if (pc2)
-      k_pass_b_pc2<<<grdb, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, bx, parity);
-    else
-      k_pass_b_pc1<<<grdb, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, bx, parity);
-    CK(cudaGetLastError());
+    CK(launch_k(ctx->pdl, pc2 ? k_pass_b_pc2 : k_pass_b_pc1, grdb, dim3(NTHREADS), SMEM_B,
+                ctx->stream, ctx->tmaps, bx, parity));
     MARK("passB");
-    k_finalize_mail<<<1, 1, 0, ctx->stream>>>(ctx->S, pt, MAIL_B, pc2 ? 2 : 1, ctx->hist);
-    CK(cudaGetLastError());
+    CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_B,
+                pc2 ? 2 : 1, ctx->hist));
     MARK("finalize_beta");
     ctx->n_enq += 5;
     if (pc2) {
@@ -526,11 +540,8 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
       ctx->n_enq++;
       TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
     }
-    if (pc2)
-      k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, a, parity);
-    else
-      k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, a, parity);
-    CK(cudaGetLastError());
+    CK(launch_k(ctx->pdl && !multi, pc2 ? k_pass_a_pc2 : k_pass_a_pc1, grd, dim3(NTHREADS), SMEM_A,
+                ctx->stream, ctx->tmaps, a, parity));
     ctx->n_enq++;
   }
   if (multi) {
@@ -541,11 +552,8 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     ctx->n_enq++;
     MARK("finalize_alpha");
   }
-  if (pc2)
-    k_pass_b_pc2<<<grdb, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, ab, parity);
-  else
-    k_pass_b_pc1<<<grdb, NTHREADS, SMEM_B, ctx->stream>>>(ctx->tmaps, ab, parity);
-  CK(cudaGetLastError());
+  CK(launch_k(ctx->pdl && !multi, pc2 ? k_pass_b_pc2 : k_pass_b_pc1, grdb, dim3(NTHREADS), SMEM_B,
+              ctx->stream, ctx->tmaps, ab, parity));
     ctx->n_enq++;
   MARK("passB");
   if (multi) {
@@ -776,6 +784,10 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   ctx->bc = outer_bc;
   ctx->pc_req = ctx->pc = pc;
   ctx->r0 = ctx->rf[0];
+  {
+    const char *e = getenv("POT3D_PDL");
+    ctx->pdl = !(e && atoi(e) == 0);
+  }
   pot3d_runtime R{};
   R.nranks = 1;
   R.device = -1;

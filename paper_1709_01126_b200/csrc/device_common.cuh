@@ -292,6 +292,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
 }
 // 3-D tiled TMA load of the box at (c0 inner, c1, c2 outer) into smem; bytes land
 // on `bar` (complete_tx).  Out-of-bounds elements are zero-filled.
+// Programmatic dependent launch: a kernel launched with the PDL attribute may start
+// while its predecessor drains; pdl_wait() blocks until the predecessor grid has
+// completed and its writes are visible (a no-op without the attribute), and
+// pdl_trigger() lets this grid's successor launch once every block has called it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 __device__ __forceinline__ void tma_load_3d(void *smem_dst, const void *map, uint64_t *bar, int c0,
                                             int c1, int c2) {
   asm volatile(

@@ -140,6 +140,8 @@ __global__ void k_finalize_rho(Scalars *S, const double *gathered, int nranks) {
 // ---------------------------------------------------------------------------
 __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const double *p_old,
                          double *p_new, int mode, const PeerTab *peers, int parity_new) {
+  pdl_trigger();
+  pdl_wait();
   if (mode >= 0 && S->stop) return;
   const double beta = (mode >= 0) ? S->beta : 0.0;
   const long long per = (long long)G.nt * G.np;
@@ -202,6 +204,8 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
 // Peer-memory finalisation (one thread): the reductions of every rank, summed in
 // rank order, then the same scalar updates as the single-rank path.
 __global__ void k_finalize_mail(Scalars *S, const PeerTab *peers, int kind, int what, double *hist) {
+  pdl_trigger();
+  pdl_wait();
   if (S->stop) return;
   // kinds A/B belong to iteration iter+1 (iter not yet advanced); C follows finalize_rr
   const unsigned long long seq = mail_seq(S->epoch, what == 3 ? S->iter : S->iter + 1);

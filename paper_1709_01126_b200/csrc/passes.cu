@@ -203,7 +203,6 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   const Grid &G = A.G;
   const Metrics &M = A.M;
   Scalars *S = A.S;
-  if (S->stop) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemA &sm = *reinterpret_cast<SmemA *>(smem_raw);
   __shared__ double sred[NTHREADS / 32];
@@ -216,7 +215,6 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   const int ig0 = G.i0 + t.c0 - 1;           // global shell of plane q = 0
   load_planes(pls, M, ig0, L + 2);
   const int cs = 2 + 2 * t.lane;  // smem index of element 0
-  const double beta = S->beta;
   const long long PL = G.plane;
   const void *map_src = &T.src_h;
   const void *map_old = &T.p_h[parity];
@@ -261,6 +259,12 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     row[0] = row[1] = row[SROW - 2] = row[SROW - 1] = 0.0;
   }
   __syncthreads();
+  // everything above reads only launch constants and metrics: with PDL it overlaps
+  // the previous kernel's tail; S, r|z and p are read only after the wait
+  pdl_trigger();
+  pdl_wait();
+  if (S->stop) return;
+  const double beta = S->beta;
   if (threadIdx.x == 0) {
     issue(0, 0);
     issue(1, 1);
@@ -379,7 +383,6 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   const Grid &G = A.G;
   const Metrics &M = A.M;
   Scalars *S = A.S;
-  if (S->stop) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemB &sm = *reinterpret_cast<SmemB *>(smem_raw);
   __shared__ double sred[2 * NTHREADS / 32];
@@ -392,7 +395,6 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   const int ig0 = G.i0 + t.c0 - 1;
   load_planes(pls, M, ig0, L + 2);
   const int cs = 2 + 2 * t.lane;
-  const double alpha = S->alpha;
   const long long PL = G.plane;
   const void *map_p = &T.p_h[parity ^ 1];
   const void *map_r = &T.r_i;
@@ -422,6 +424,10 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  if (S->stop) return;
+  const double alpha = S->alpha;
   if (threadIdx.x == 0)
     for (int s = 0; s < NS_B - 2; s++) issue();
 

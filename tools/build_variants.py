@@ -6,10 +6,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "b_x0": [],
-    "b_x1n4": ["POT3D_B_XLDG=1", "POT3D_NS_B=4"],
-    "b_x1n5": ["POT3D_B_XLDG=1", "POT3D_NS_B=5"],
-    "b_x1n6": ["POT3D_B_XLDG=1", "POT3D_NS_B=6"],
+    "base": [],
+    "r1m2": ["POT3D_RPW=1", "POT3D_MINB=2"],
+    "r1m1": ["POT3D_RPW=1", "POT3D_MINB=1"],
 }
 out = Path(build.PKG) / "variants"
 out.mkdir(exist_ok=True)
