@@ -50,6 +50,11 @@ struct Pc2 {
   long long edge_len;       // doubles
   int nbmax;                // largest block (shells)
   double *inv_d;            // 1/d_m, cell layout
+  // run-vectorised sweeps (k_sweep4)
+  int ntj4, ntk4, ntiles4, koff_f, koff_b;
+  int2 *d_order4;
+  double *edge4;
+  long long edge4_len;
   std::vector<void *> allocs;
   size_t bytes;
 };
@@ -81,7 +86,6 @@ struct SweepArgs {
 // ld.global.cv, polls only while it still reads the sentinel, and re-arms it.
 constexpr unsigned SENT32 = 0x7FF57FF5u;
 constexpr unsigned long long SENT = 0x7FF57FF57FF57FF5ull;
-constexpr long long SPIN_LIMIT = 1ll << 26;  // bounded waits: a protocol error never hangs the GPU
 #ifndef POT3D_SWEEP_D
 #define POT3D_SWEEP_D 8
 #endif
@@ -96,6 +100,29 @@ __device__ __forceinline__ double ld_poll(const double *p) {
 
 __device__ __forceinline__ bool is_sent(double v) {
   return (unsigned long long)__double_as_longlong(v) == SENT;
+}
+
+// Wait until the edge slot p holds a value (v: its prefetched content).  Bounded:
+// after POLL_TIMEOUT_NS, or at once when another thread has already given up
+// (flags bit 2), the protocol error is recorded and the sweep runs on with
+// garbage, which the solve then reports.
+constexpr unsigned long long POLL_TIMEOUT_NS = 2000000000ull;  // 2 s
+__device__ __forceinline__ double poll_slot(const double *p, double v, int *flags, bool &proto) {
+  if (!is_sent(v)) return v;
+  const unsigned long long t0 = global_ns();
+  for (int n = 0;; n++) {
+    v = ld_poll(p);
+    if (!is_sent(v)) return v;
+    if ((n & 63) == 63) {
+      if (*reinterpret_cast<volatile int *>(flags) & 2) break;
+      if (global_ns() - t0 > POLL_TIMEOUT_NS) {
+        atomicOr(flags, 2);
+        break;
+      }
+    }
+  }
+  proto = true;
+  return v;
 }
 
 #ifndef POT3D_SWEEP_MINB
@@ -191,15 +218,11 @@ __global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
       const int ivt = t - jj - kk;  // virtual local shell of this thread at step t
       if (valid && ivt >= 0 && ivt < nb) {
         if (need_j) {  // value of the tile above (virtual), produced at its step t+WJ-1
-          long long spins = 0;
-          while (is_sent(nj) && spins++ < SPIN_LIMIT) nj = ld_poll(up_bot + ivt);
-          proto |= is_sent(nj);
+          nj = poll_slot(up_bot + ivt, nj, A.sync + 1, proto);
           __stcg(reinterpret_cast<unsigned long long *>(up_bot + ivt), SENT);  // re-arm
         }
         if (need_k) {
-          long long spins = 0;
-          while (is_sent(nk) && spins++ < SPIN_LIMIT) nk = ld_poll(lf_rgt + ivt);
-          proto |= is_sent(nk);
+          nk = poll_slot(lf_rgt + ivt, nk, A.sync + 1, proto);
           __stcg(reinterpret_cast<unsigned long long *>(lf_rgt + ivt), SENT);
         }
         const long long o = o_base + (long long)ivt * o_step;
@@ -242,6 +265,303 @@ __global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
   if (MODE == SW_BWD) {
     double v[1] = {acc}, tot[1];
     // partials indexed by ticket (tile identity), not blockIdx: a fixed summation order
+    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket) && tid == 0) {
+      if (A.finalize)
+        finalize_rho(A.S, tot[0]);
+      else if (A.peers)
+        mail_post(A.peers, MAIL_C, tot[0], 0.0, mail_seq(A.S->epoch, A.S->iter));
+      else
+        A.local_sum[0] = tot[0];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Run-vectorised forward / backward sweeps.  Same wavefront and handoff
+// protocol as k_sweep, but a thread owns SV = 4 phi-consecutive cells of one
+// row (a "run", one 32-B sector per array) instead of one cell: step t of
+// thread (jj, m) handles shell t - jj - m of run m, so the lanes of a warp read
+// and write whole sectors (the one-cell mapping used a quarter of every sector
+// it moved).  Inside a run the phi dependency is sequential in the thread;
+// the run's first cell takes the last cell of run m-1 (previous step, shared
+// memory, or the left tile's edge slot).  Runs are aligned to 32 B in memory
+// (virtual offset koff), operands are prefetched SPD steps ahead by cp.async
+// into a shared ring, edge slots included (re-polled at use while they still
+// hold the sentinel).  FACTOR keeps the one-cell kernel (setup only).
+// ---------------------------------------------------------------------------
+constexpr int SV = 4;            // cells per thread along phi
+constexpr int SNR = 32;          // runs per tile row (one warp)
+constexpr int SWK = SV * SNR;    // 128 phi columns per tile
+#ifndef POT3D_SWJ
+#define POT3D_SWJ 8
+#endif
+#ifndef POT3D_SPD_F
+#define POT3D_SPD_F 4
+#endif
+#ifndef POT3D_SPD_B
+#define POT3D_SPD_B 4
+#endif
+constexpr int SWJ = POT3D_SWJ;   // tile rows
+constexpr int SWT = SWJ * SNR;   // 256 threads
+
+template <int MODE> struct Sw4 {
+  static constexpr int NA = (MODE == SW_FWD) ? 2 : 3;  // FWD: r, 1/d; BWD: w, 1/d, r
+  static constexpr int PD = (MODE == SW_FWD) ? POT3D_SPD_F : POT3D_SPD_B;  // prefetch depth (power of 2)
+  static constexpr int RING = PD * NA * SWT * SV;      // doubles
+  static constexpr int JR = PD * SNR * SV, KR = PD * SWJ * 2, XW = 2 * SWJ * SNR * SV;
+  static constexpr size_t SMEM = (size_t)(RING + JR + KR + XW) * sizeof(double);
+};
+
+// virtual phi offset of the first run so that every run starts on a 32-B
+// boundary of the physical columns (c = k + COFF): FWD k = kv, BWD k = np-1-kv
+__host__ __device__ inline int sweep4_koff(int np, bool rev) {
+  if (!rev) return -1;                  // kv0 = 4m - 1  ->  c0 = 4m
+  int o = (np - 3) % 4;                 // kv0 = np - 3 (mod 4) -> lowest column 4m
+  return o > 0 ? o - 4 : o;
+}
+
+__device__ __forceinline__ double2 lds2(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double lds1(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts2(unsigned a, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(SWT, 1) k_sweep4(SweepArgs A, int koff, int ntk4) {
+  using C = Sw4<MODE>;
+  constexpr int PD = C::PD, NA = C::NA;
+  constexpr bool rev = (MODE == SW_BWD);
+  constexpr unsigned ASTR = SWT * SV * 8, SLOT = NA * ASTR;        // ring: array / slot strides
+  constexpr unsigned XB = SWJ * SNR * SV * 8;                      // xw buffer stride
+  const Grid &G = A.G;
+  const Metrics &M = A.M;
+  if (A.predicated && A.S->stop) return;
+  extern __shared__ __align__(16) double sm4[];
+  double *ring = sm4;                       // [PD][NA][SWT][SV]
+  double *jring = ring + C::RING;           // [PD][SNR][SV]
+  double *kring = jring + C::JR;            // [PD][SWJ][2]
+  double *xw = kring + C::KR;               // [2][SWJ][SNR][SV]
+  double *crs = xw + C::XW;                 // [nbmax] r coupling factor of virtual shell iv
+  double *drs = crs + A.nbmax;              // [nbmax] dr of virtual shell iv
+  __shared__ int s_ticket;
+  __shared__ double sred[SWT / 32];
+  const int tid = threadIdx.x;
+  const int jj = tid / SNR, m = tid % SNR;
+  if (tid == 0) s_ticket = atomicAdd(&A.sync[0], 1);
+  __syncthreads();
+  const int ticket = s_ticket;
+  const int b = ticket % A.nblk;
+  const int pos = ticket / A.nblk;
+  const int2 tl = A.order[pos];
+  const int l0 = A.l0[b], l1 = A.l0[b + 1];
+  const int nb = l1 - l0;
+  // per-shell factors of this block in virtual order (r predecessor: arm for FWD, arp for BWD)
+  for (int iv = tid; iv < nb; iv += SWT) {
+    const int ig = G.i0 + (rev ? l1 - 1 - iv : l0 + iv);
+    crs[iv] = (iv > 0) ? (rev ? __ldg(M.arp + ig) : __ldg(M.arm + ig)) : 0.0;
+    drs[iv] = __ldg(M.dr + ig);
+  }
+  const int jv = tl.x * SWJ + jj;
+  const bool vrow = jv < G.nt;
+  const int jc = vrow ? (rev ? G.nt - 1 - jv : jv) : 0;
+  const int kv0 = koff + tl.y * SWK + SV * m;        // virtual k of element 0
+  const double g = __ldg(M.g + jc), q = __ldg(M.q + jc);
+  const double ct = rev ? __ldg(M.atp + jc) : __ldg(M.atm + jc);
+  bool ve[SV];
+  double gd[SV], td[SV], qc[SV];  // g dp_k, ct dp_k, q cp_k: A^r = cr gd, A^t = dr td, A^p = dr qc
+  bool any = false, full = true;
+#pragma unroll
+  for (int e = 0; e < SV; e++) {
+    const int kv = kv0 + e;
+    ve[e] = vrow && kv >= 0 && kv < G.np;
+    any |= ve[e];
+    full &= ve[e];
+    const int k = rev ? G.np - 1 - kv : kv;
+    const int kc = ve[e] ? k : 0;
+    const double dpk = ve[e] ? __ldg(M.dp + kc) : 0.0;
+    const double cpk = !ve[e] ? 0.0 : rev ? ((k < G.np - 1) ? __ldg(M.app + kc) : 0.0)
+                                          : ((k > 0) ? __ldg(M.apm + kc) : 0.0);
+    gd[e] = g * dpk;
+    td[e] = ct * dpk;
+    qc[e] = q * cpk;
+  }
+  // lowest physical column of the run (32-B aligned); element e <-> col_lo + (rev ? 3-e : e)
+  const int col_lo = rev ? G.np - kv0 - 3 : kv0 + COFF;
+  // cell offset of the run at step ts: o0 + ts * ostep (virtual shell iv = ts - jj - m)
+  const long long ostep = rev ? -G.plane : G.plane;
+  const long long o0 = (long long)((rev ? l1 - 1 : l0) + 1) * G.plane + (long long)jc * G.PK + col_lo -
+                       (long long)(jj + m) * ostep;
+
+  // edge slots: per tile, bottom [SNR][nbmax][SV] then right [SWJ][nbmax][2]
+  const int my = tl.x * ntk4 + tl.y;
+  const long long tstride = (long long)A.nbmax * (SNR * SV + SWJ * 2);
+  double *eb = A.edge + (long long)b * A.ntiles * tstride;
+  double *my_bot = eb + my * tstride + (long long)m * A.nbmax * SV;
+  double *my_rgt = eb + my * tstride + (long long)SNR * A.nbmax * SV + (long long)jj * A.nbmax * 2;
+  const bool put_bot = (jj == SWJ - 1) && (jv + 1 < G.nt) && any;
+  const bool put_rgt = (m == SNR - 1) && vrow && (kv0 + SV < G.np);
+  const bool need_j = (jj == 0) && vrow && (jv > 0) && any;
+  const bool need_k = (m == 0) && vrow && (kv0 > 0);
+  double *up_bot = eb + (long long)(my - ntk4) * tstride + (long long)m * A.nbmax * SV;
+  double *lf_rgt = eb + (long long)(my - 1) * tstride + (long long)SNR * A.nbmax * SV + (long long)jj * A.nbmax * 2;
+
+  const double *src0 = (MODE == SW_FWD) ? A.r : A.z;  // FWD: r; BWD: w (forward output)
+  const double *src1 = A.inv_d;
+  const double *src2 = A.r;                          // BWD: r for the r.z partial
+  // shared addresses (32-bit)
+  const unsigned ring_me = smem_u32(ring) + (unsigned)(tid * SV * 8);
+  const unsigned jr_me = smem_u32(jring) + (unsigned)(m * SV * 8);
+  const unsigned kr_me = smem_u32(kring) + (unsigned)(jj * 2 * 8);
+  const unsigned xw0 = smem_u32(xw);
+  const unsigned xo_me = xw0 + (unsigned)((jj * SNR + m) * SV * 8);
+  const unsigned xj_me = xw0 + (unsigned)(((jj > 0 ? jj - 1 : 0) * SNR + m) * SV * 8);
+  const unsigned xk_me = xw0 + (unsigned)((jj * SNR + (m > 0 ? m - 1 : 0)) * SV * 8 + (SV - 1) * 8);
+  const unsigned crs_a = smem_u32(crs), drs_a = smem_u32(drs);
+  const int ts_lo = jj + m, ts_hi = jj + m + nb;     // steps with a cell of this thread
+  auto prefetch = [&](int ts) {
+    const bool ok = any && ts >= ts_lo && ts < ts_hi;
+    const long long o = ok ? o0 + (long long)ts * ostep : 0;
+    const int sb = ok ? 16 : 0;
+    const unsigned sl = (unsigned)(ts & (PD - 1));
+    const unsigned d = ring_me + sl * SLOT;
+    cp_async16s(d, src0 + o, sb);
+    cp_async16s(d + 16, src0 + o + 2, sb);
+    cp_async16s(d + ASTR, src1 + o, sb);
+    cp_async16s(d + ASTR + 16, src1 + o + 2, sb);
+    if (NA == 3) {
+      cp_async16s(d + 2 * ASTR, src2 + o, sb);
+      cp_async16s(d + 2 * ASTR + 16, src2 + o + 2, sb);
+    }
+    if (need_j) {
+      const double *g0 = up_bot + (ok ? (long long)(ts - ts_lo) * SV : 0);
+      cp_async16s(jr_me + sl * (SNR * SV * 8), g0, sb);
+      cp_async16s(jr_me + sl * (SNR * SV * 8) + 16, g0 + 2, sb);
+    }
+    if (need_k)
+      cp_async16s(kr_me + sl * (SWJ * 2 * 8), lf_rgt + (ok ? (long long)(ts - ts_lo) * 2 : 0), sb);
+    cp_async_commit();
+  };
+
+  const int nsteps = nb + SWJ + SNR - 2;
+#pragma unroll 1
+  for (int u = 0; u < PD; u++) prefetch(u);
+  double wprev[SV];
+#pragma unroll
+  for (int e = 0; e < SV; e++) wprev[e] = 0.0;
+  double acc = 0.0;
+  bool proto = false;
+#pragma unroll 1
+  for (int t = 0; t < nsteps; t++) {
+    cp_async_wait<PD - 1>();  // this thread's operands of step t have landed
+    __syncthreads();          // step t-1 of the neighbouring threads is in xw; crs/drs staged
+    const int ivt = t - ts_lo;
+    if (any && ivt >= 0 && ivt < nb) {
+      const unsigned sl = (unsigned)(t & (PD - 1));
+      const unsigned rs = ring_me + sl * SLOT;
+      double a0[SV], b0[SV], c0[SV];
+      {
+        const double2 x0 = lds2(rs), x1 = lds2(rs + 16);
+        const double2 y0 = lds2(rs + ASTR), y1 = lds2(rs + ASTR + 16);
+        // the ring holds physical column order
+        a0[0] = rev ? x1.y : x0.x; a0[1] = rev ? x1.x : x0.y; a0[2] = rev ? x0.y : x1.x; a0[3] = rev ? x0.x : x1.y;
+        b0[0] = rev ? y1.y : y0.x; b0[1] = rev ? y1.x : y0.y; b0[2] = rev ? y0.y : y1.x; b0[3] = rev ? y0.x : y1.y;
+        if (NA == 3) {
+          const double2 w0 = lds2(rs + 2 * ASTR), w1 = lds2(rs + 2 * ASTR + 16);
+          c0[0] = w1.y; c0[1] = w1.x; c0[2] = w0.y; c0[3] = w0.x;
+        } else {
+          c0[0] = c0[1] = c0[2] = c0[3] = 0.0;
+        }
+      }
+      const unsigned xb_prev = ((t - 1) & 1) ? XB : 0u;
+      double vj[SV], vk;
+      if (jj > 0) {
+        const double2 u0 = lds2(xj_me + xb_prev), u1 = lds2(xj_me + xb_prev + 16);
+        vj[0] = u0.x; vj[1] = u0.y; vj[2] = u1.x; vj[3] = u1.y;
+      } else {
+        const unsigned jr = jr_me + sl * (SNR * SV * 8);
+        const double2 u0 = lds2(jr), u1 = lds2(jr + 16);
+        vj[0] = u0.x; vj[1] = u0.y; vj[2] = u1.x; vj[3] = u1.y;
+        if (need_j) {
+          double *slot = up_bot + (long long)ivt * SV;
+#pragma unroll
+          for (int e = 0; e < SV; e++) {
+            if (ve[e]) {
+              if (is_sent(vj[e])) vj[e] = poll_slot(slot + e, vj[e], A.sync + 1, proto);
+            } else {
+              vj[e] = 0.0;
+            }
+          }
+          // re-arm all four slots: the producer stores whole runs, and FWD / BWD
+          // (different run offsets) share the slots
+          const ulonglong2 s2 = make_ulonglong2(SENT, SENT);
+          __stcg(reinterpret_cast<ulonglong2 *>(slot), s2);
+          __stcg(reinterpret_cast<ulonglong2 *>(slot + 2), s2);
+        } else {
+          vj[0] = vj[1] = vj[2] = vj[3] = 0.0;
+        }
+      }
+      if (m > 0) {
+        vk = lds1(xk_me + xb_prev);
+      } else if (need_k) {
+        vk = lds1(kr_me + sl * (SWJ * 2 * 8));
+        if (is_sent(vk)) vk = poll_slot(lf_rgt + (long long)ivt * 2, vk, A.sync + 1, proto);
+        __stcg(reinterpret_cast<unsigned long long *>(lf_rgt + (long long)ivt * 2), SENT);
+      } else {
+        vk = 0.0;
+      }
+      const double cr = lds1(crs_a + ivt * 8), dr = lds1(drs_a + ivt * 8);
+      double val[SV];
+#pragma unroll
+      for (int e = 0; e < SV; e++) {
+        const double Ar = cr * gd[e], At = dr * td[e], Ap = dr * qc[e];
+        double v;
+        if (MODE == SW_FWD)
+          v = (a0[e] + Ar * wprev[e] + At * vj[e] + Ap * vk) * b0[e];
+        else
+          v = a0[e] + b0[e] * (Ar * wprev[e] + At * vj[e] + Ap * vk);
+        v = ve[e] ? v : 0.0;
+        if (MODE == SW_BWD) acc += c0[e] * v;
+        val[e] = v;
+        vk = v;
+      }
+      // results: z (w for FWD), physical order col_lo .. col_lo+3
+      double *zr = A.z + o0 + (long long)t * ostep;
+      const double2 p0 = rev ? make_double2(val[3], val[2]) : make_double2(val[0], val[1]);
+      const double2 p1 = rev ? make_double2(val[1], val[0]) : make_double2(val[2], val[3]);
+      if (full) {
+        *reinterpret_cast<double2 *>(zr) = p0;
+        *reinterpret_cast<double2 *>(zr + 2) = p1;
+      } else {
+        if (rev ? ve[3] : ve[0]) zr[0] = p0.x;
+        if (rev ? ve[2] : ve[1]) zr[1] = p0.y;
+        if (rev ? ve[1] : ve[2]) zr[2] = p1.x;
+        if (rev ? ve[0] : ve[3]) zr[3] = p1.y;
+      }
+      if (put_bot) {
+        __stcg(reinterpret_cast<double2 *>(my_bot + (long long)ivt * SV), make_double2(val[0], val[1]));
+        __stcg(reinterpret_cast<double2 *>(my_bot + (long long)ivt * SV + 2), make_double2(val[2], val[3]));
+      }
+      if (put_rgt) __stcg(my_rgt + (long long)ivt * 2, val[SV - 1]);
+      const unsigned xb = (t & 1) ? XB : 0u;
+      sts2(xo_me + xb, val[0], val[1]);
+      sts2(xo_me + xb + 16, val[2], val[3]);
+#pragma unroll
+      for (int e = 0; e < SV; e++) wprev[e] = val[e];
+    }
+    prefetch(t + PD);  // into the ring slot this step has just consumed
+  }
+  cp_async_wait<0>();
+  if (__syncthreads_or(proto) && tid == 0) atomicOr(&A.sync[1], 2);  // protocol error
+  if (MODE == SW_BWD) {
+    double v[1] = {acc}, tot[1];
     if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket) && tid == 0) {
       if (A.finalize)
         finalize_rho(A.S, tot[0]);
@@ -307,7 +627,23 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
   const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
   P->inv_d = (double *)p_alloc(P, sizeof(double) * cells, alloc, actx);
   P->edge = (double *)p_alloc(P, sizeof(double) * P->edge_len, alloc, actx);
-  if (!P->d_l0 || !P->d_order || !P->d_sync || !P->inv_d || !P->edge) {
+  // run-vectorised sweep geometry (FWD and BWD share the tile grid: the larger one)
+  P->koff_f = sweep4_koff(G.np, false);
+  P->koff_b = sweep4_koff(G.np, true);
+  P->ntj4 = (G.nt + SWJ - 1) / SWJ;
+  P->ntk4 = std::max((G.np - P->koff_f + SWK - 1) / SWK, (G.np - P->koff_b + SWK - 1) / SWK);
+  P->ntiles4 = P->ntj4 * P->ntk4;
+  P->edge4_len = (long long)P->nblk * P->ntiles4 * P->nbmax * (SNR * SV + SWJ * 2);
+  P->d_order4 = (int2 *)p_alloc(P, sizeof(int2) * P->ntiles4, alloc, actx);
+  P->edge4 = (double *)p_alloc(P, sizeof(double) * P->edge4_len, alloc, actx);
+  if (!P->d_l0 || !P->d_order || !P->d_sync || !P->inv_d || !P->edge || !P->d_order4 || !P->edge4) {
+    *out = P;
+    return -1;
+  }
+  if (cudaFuncSetAttribute(k_sweep4<SW_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(Sw4<SW_FWD>::SMEM + 16 * P->nbmax)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_sweep4<SW_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(Sw4<SW_BWD>::SMEM + 16 * P->nbmax)) != cudaSuccess) {
     *out = P;
     return -1;
   }
@@ -321,8 +657,18 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
     const int sx = x.x * WJ + x.y * WK, sy = y.x * WJ + y.y * WK;
     return sx != sy ? sx < sy : x.x < y.x;
   });
+  std::vector<int2> order4;
+  order4.reserve(P->ntiles4);
+  for (int a = 0; a < P->ntj4; a++)
+    for (int c = 0; c < P->ntk4; c++) order4.push_back(make_int2(a, c));
+  std::stable_sort(order4.begin(), order4.end(), [](const int2 &x, const int2 &y) {
+    const int sx = x.x * SWJ + x.y * SNR, sy = y.x * SWJ + y.y * SNR;
+    return sx != sy ? sx < sy : x.x < y.x;
+  });
   // everything on the context stream (the factor kernel runs there too)
   cudaMemcpyAsync(P->d_order, order.data(), sizeof(int2) * P->ntiles, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(P->d_order4, order4.data(), sizeof(int2) * P->ntiles4, cudaMemcpyHostToDevice, s);
+  k_fill_u64<<<1024, 256, 0, s>>>(reinterpret_cast<unsigned long long *>(P->edge4), P->edge4_len, SENT);
   cudaMemcpyAsync(P->d_l0, block_l0, sizeof(int) * (nblocks_local + 1), cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(P->inv_d, 0, sizeof(double) * cells, s);
   k_fill_u64<<<1024, 256, 0, s>>>(reinterpret_cast<unsigned long long *>(P->edge), P->edge_len, SENT);
@@ -375,11 +721,15 @@ int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, 
   const int pred = iteration ? 1 : 0;
   SweepArgs a = sweep_args(P, M, S, r, z, partials, pred, finalize, local_sum);
   a.peers = iteration ? peers : nullptr;
-  cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);  // ticket only (flags accumulate)
-  k_sweep<SW_FWD><<<P->nblk * P->ntiles, WT, 0, s>>>(a);
-  cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);
   if (!iteration) a.finalize = 0, a.local_sum = local_sum;
-  k_sweep<SW_BWD><<<P->nblk * P->ntiles, WT, 0, s>>>(a);
+  // run-vectorised sweeps: their own tile order and edge slots
+  a.order = P->d_order4;
+  a.edge = P->edge4;
+  a.ntiles = P->ntiles4;
+  cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);  // ticket only (flags accumulate)
+  k_sweep4<SW_FWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_FWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_f, P->ntk4);
+  cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);
+  k_sweep4<SW_BWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_BWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_b, P->ntk4);
   const Grid &G = P->G;
   k_pc2_ghost<<<(unsigned)std::min<long long>(((long long)G.nr_loc * G.nt + 255) / 256, 4096), 256, 0,
                 s>>>(G, z, S, pred);
@@ -395,6 +745,7 @@ int pc2_status(Pc2 *P, cudaStream_t s) {
   cudaStreamSynchronize(s);
   if (f & 2) {
     k_fill_u64<<<1024, 256, 0, s>>>(reinterpret_cast<unsigned long long *>(P->edge), P->edge_len, SENT);
+    k_fill_u64<<<1024, 256, 0, s>>>(reinterpret_cast<unsigned long long *>(P->edge4), P->edge4_len, SENT);
     cudaMemsetAsync(P->d_sync + 1, 0, sizeof(int), s);
     cudaStreamSynchronize(s);
   }

@@ -6,9 +6,11 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "base": [],
-    "r1m2": ["POT3D_RPW=1", "POT3D_MINB=2"],
-    "r1m1": ["POT3D_RPW=1", "POT3D_MINB=1"],
+    "s8p44": [],
+    "s8p22": ["POT3D_SPD_F=2", "POT3D_SPD_B=2"],
+    "s16p42": ["POT3D_SWJ=16", "POT3D_SPD_F=4", "POT3D_SPD_B=2"],
+    "s16p22": ["POT3D_SWJ=16", "POT3D_SPD_F=2", "POT3D_SPD_B=2"],
+    "s4p44": ["POT3D_SWJ=4"],
 }
 out = Path(build.PKG) / "variants"
 out.mkdir(exist_ok=True)
