@@ -459,9 +459,11 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     // chunk touches a ghost shell (scheduled last); the rank sums go straight into
     // every rank's mailbox from the reductions' last blocks
     const PeerTab *pt = ctx->peers;
+    // PC1: the previous iteration's beta finalisation lives in edge_p (fold)
+    const int fold = pc2 ? 0 : 1;
     CK(launch_k(ctx->pdl, k_edge_p, dim3(148 * 4), dim3(256), 0, ctx->stream, G, ctx->M, ctx->S,
                 (const double *)(pc2 ? ctx->z : ctx->r), (const double *)ctx->P[parity],
-                ctx->P[parity ^ 1], pc2 ? 1 : 0, pt, parity ^ 1));
+                ctx->P[parity ^ 1], pc2 ? 1 : 0, pt, parity ^ 1, ctx->hist, fold));
     MARK("edge_p");
     PassArgs ax = a;
     ax.G.part = 3;
@@ -474,13 +476,17 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     MARK("finalize_alpha");
     PassArgs bx = ab;
     bx.peers = pt;
+    bx.fold = fold;  // pass B only posts its sums and marks them pending
     CK(launch_k(ctx->pdl, pc2 ? k_pass_b_pc2 : k_pass_b_pc1, grdb, dim3(NTHREADS), SMEM_B,
                 ctx->stream, ctx->tmaps, bx, parity));
     MARK("passB");
-    CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_B,
-                pc2 ? 2 : 1, ctx->hist));
-    MARK("finalize_beta");
-    ctx->n_enq += 5;
+    ctx->n_enq += 4;
+    if (!fold) {
+      CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_B,
+                  2, ctx->hist));
+      MARK("finalize_rr");
+      ctx->n_enq++;
+    }
     if (pc2) {
       int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
                          ctx->stream, true, pt);
@@ -497,7 +503,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     // covers the interior shells, then pass A finishes the two edge shells
     k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
                                                 ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0,
-                                                nullptr, 0);
+                                                nullptr, 0, nullptr, 0);
     CK(cudaGetLastError());
     ctx->n_enq++;
     MARK("edge_p");
@@ -535,7 +541,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     if (multi) {
       k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
                                                   ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0,
-                                                nullptr, 0);
+                                                nullptr, 0, nullptr, 0);
       CK(cudaGetLastError());
       ctx->n_enq++;
       TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
@@ -677,7 +683,7 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   info->pc = ctx->pc;
   info->pc2_blocks_total = ctx->pc2_blocks * ctx->nranks;
   int64_t k = 2;
-  if (ctx->nranks > 1) k += 3;
+  if (ctx->nranks > 1) k += (ctx->xfer && ctx->pc == 1) ? 2 : 3;
   if (ctx->pc == 2 && ctx->pc2) k += pc2_kernels_per_apply(ctx->pc2) + (ctx->nranks > 1 ? 1 : 0);
   info->graph_kernels_per_iter = k;
   // algorithmic bytes: PC1 64 B/cell (pass A 24 + pass B 40), PC2 + 56 B sweeps
@@ -1254,7 +1260,7 @@ int pot3d_precond(pot3d_ctx *ctx, const double *rin, double *zout) {
     // PC1: the edge-plane kernel computes z = D^-1 r (beta = 0) over any planes
     Scalars h0{};
     CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
-    k_edge_p<<<148 * 8, 256, 0, s>>>(G, ctx->M, ctx->S, rr, nullptr, zz, -1, nullptr, 0);
+    k_edge_p<<<148 * 8, 256, 0, s>>>(G, ctx->M, ctx->S, rr, nullptr, zz, -1, nullptr, 0, nullptr, 0);
     CK(cudaGetLastError());
     ctx->n_launch++;
   }

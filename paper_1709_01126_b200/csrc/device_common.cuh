@@ -181,15 +181,24 @@ __device__ __forceinline__ bool xfer_wait(const unsigned long long *flag, unsign
   return true;
 }
 
-// every rank's entry of `kind` for seq, summed in rank order (bit-identical on all ranks)
+// every rank's entry of `kind` for seq, summed in rank order (bit-identical on all ranks);
+// the first pass issues all ranks' acquire loads back to back (one round trip when
+// every rank has already posted), stragglers are then waited for one by one
 __device__ __forceinline__ bool mail_collect(const PeerTab *T, int kind, unsigned long long seq,
                                              Scalars *S, double &s0, double &s1) {
   const Mailbox *mb = T->mail[T->rank];
+  const int n = T->nranks;
+  unsigned long long got[MAXR];
+#pragma unroll
+  for (int r = 0; r < MAXR; r++)
+    if (r < n) got[r] = ld_acquire_sys(&mb->e[kind][r].seq);
   s0 = 0.0;
   s1 = 0.0;
-  for (int r = 0; r < T->nranks; r++) {
+#pragma unroll
+  for (int r = 0; r < MAXR; r++) {
+    if (r >= n) break;
     const MailEntry *e = &mb->e[kind][r];
-    if (!xfer_wait(&e->seq, seq, S)) return false;
+    if (got[r] != seq && !xfer_wait(&e->seq, seq, S)) return false;
     s0 += *reinterpret_cast<const volatile double *>(&e->v0);
     s1 += *reinterpret_cast<const volatile double *>(&e->v1);
   }

@@ -139,13 +139,47 @@ __global__ void k_finalize_rho(Scalars *S, const double *gathered, int nranks) {
 // Edge shells / whole-slab PC1 apply (see pot3d_internal.cuh for the modes).
 // ---------------------------------------------------------------------------
 __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const double *p_old,
-                         double *p_new, int mode, const PeerTab *peers, int parity_new) {
+                         double *p_new, int mode, const PeerTab *peers, int parity_new,
+                         double *hist, int fold) {
   pdl_trigger();
   pdl_wait();
   if (mode >= 0 && S->stop) return;
-  const double beta = (mode >= 0) ? S->beta : 0.0;
+  // fold (peer memory, PC1): finalise the previous pass B here -- every block sums
+  // the ranks' (r.z, r.r) from the mailbox in rank order and takes the same
+  // decisions; only the last block (after every block has read S) writes S
+  __shared__ double s_beta, s_rz, s_rr;
+  __shared__ int s_stop, s_status;
+  const bool pend = fold && S->pend_b;
+  const long long iter0 = S->iter;
+  if (threadIdx.x == 0) {
+    s_stop = 0;
+    s_status = 0;
+    s_beta = (mode >= 0) ? S->beta : 0.0;
+    if (pend) {
+      double rz, rr;
+      if (!mail_collect(peers, MAIL_B, mail_seq(S->epoch, iter0 + 1), S, rz, rr)) {
+        s_stop = 1;
+        s_status = -5;
+      } else {
+        s_rz = rz;
+        s_rr = rr;
+        const double rn = sqrt(rr);
+        if (rn <= S->rtol * S->bnorm) {
+          s_stop = 1;
+          s_status = 0;
+        } else if (iter0 + 1 >= S->maxit) {
+          s_stop = 1;
+          s_status = 1;
+        }
+        s_beta = rz / S->rho;
+      }
+    }
+  }
+  __syncthreads();
+  const double beta = s_beta;
+  const long long iter = pend ? iter0 + 1 : iter0;  // the iteration p_k belongs to
   const long long per = (long long)G.nt * G.np;
-  const long long n = (mode < 0) ? per * G.nr_loc : 2 * per;
+  const long long n = (mode < 0) ? per * G.nr_loc : (s_stop ? 0 : 2 * per);
   // peer memory: shell 0 also lands in rank-1's top ghost shell, shell nr_loc-1
   // in rank+1's bottom ghost shell (same [il+1][j][c] layout, shifted by whole planes)
   double *lo = nullptr, *hi = nullptr;
@@ -193,10 +227,31 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
       S->counter[4] = 0u;
-      __threadfence_system();
-      const unsigned long long seq = mail_seq(S->epoch, S->iter + 1);
-      if (peers->rank > 0) st_release_sys(&peers->mail[peers->rank - 1]->halo[1], seq);
-      if (peers->rank < peers->nranks - 1) st_release_sys(&peers->mail[peers->rank + 1]->halo[0], seq);
+      if (pend) {  // finalize_beta of the previous iteration
+        S->pend_b = 0;
+        if (s_status == -5) {
+          S->status = -5;
+          S->stop = 1;
+        } else {
+          S->iter = iter;
+          S->rr = s_rr;
+          if (hist) hist[iter] = sqrt(s_rr) / S->bnorm;
+          S->alpha_prev = S->alpha;
+          if (s_stop) {
+            S->status = s_status;
+            S->stop = 1;
+          } else {
+            S->beta = beta;
+            S->rho = s_rz;
+          }
+        }
+      }
+      if (!s_stop) {
+        __threadfence_system();
+        const unsigned long long seq = mail_seq(S->epoch, iter + 1);
+        if (peers->rank > 0) st_release_sys(&peers->mail[peers->rank - 1]->halo[1], seq);
+        if (peers->rank < peers->nranks - 1) st_release_sys(&peers->mail[peers->rank + 1]->halo[0], seq);
+      }
     }
   }
 }

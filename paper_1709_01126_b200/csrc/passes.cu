@@ -509,6 +509,9 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
         finalize_rr(S, tot[1], A.hist);  // PC2: rho' comes from the sweeps
       else
         finalize_beta(S, tot[0], tot[1], A.hist);
+    } else if (A.fold) {
+      mail_post(A.peers, MAIL_B, tot[0], tot[1], mail_seq(S->epoch, S->iter + 1));
+      S->pend_b = 1;  // finalised by the next edge-shell kernel
     } else if (A.peers) {
       mail_post(A.peers, MAIL_B, tot[0], tot[1], mail_seq(S->epoch, S->iter + 1));
     } else {

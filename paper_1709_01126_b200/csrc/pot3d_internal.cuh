@@ -88,7 +88,8 @@ struct Scalars {
   unsigned int counter[6]; // last-block counters
   unsigned long long epoch;  // solve number (peer-memory sequence numbers)
   int xfer_error;    // peer-memory wait expired
-  int pad1;
+  int pend_b;        // peer-memory PC1: pass B posted its sums; the next edge-shell kernel
+                     // finalises them (convergence test, beta) before it builds p_k
 };
 
 // ---- peer-memory exchange between the rank processes (CUDA IPC over NVLink) ----
@@ -169,6 +170,8 @@ struct PassArgs {
   int finalize;         // 1: single rank, finalise scalars in the last block
   double *local_sum;    // nranks > 1: this rank's sums for the all-gather
   const PeerTab *peers; // nranks > 1 with peer memory: mailbox / ghost-shell exchange
+  int fold;             // peer memory, PC1: pass B posts its sums and leaves their
+                        // finalisation (convergence, beta) to the next edge-shell kernel
 };
 
 // Arguments of the field kernels (a11).
@@ -223,7 +226,8 @@ __global__ void k_pole_avg(Grid G, const double *x, const double *dp, double per
 // mode -1: z = D^-1 src on every plane (PC1 apply); 0: p_new = D^-1 src + beta p_old on the
 // two edge shells (PC1); 1: p_new = src + beta p_old on the edge shells (PC2, src = z)
 __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const double *p_old,
-                         double *p_new, int mode, const PeerTab *peers, int parity_new);
+                         double *p_new, int mode, const PeerTab *peers, int parity_new,
+                         double *hist, int fold);
 // peer-memory finalisation: poll every rank's mailbox entry of `kind` for this
 // iteration, sum in rank order, update the scalars (what = 0 alpha, 1 beta, 2 rr, 3 rho)
 __global__ void k_finalize_mail(Scalars *S, const PeerTab *peers, int kind, int what, double *hist);
