@@ -420,6 +420,14 @@ PassArgs make_args(pot3d_ctx *ctx, int parity) {
   return a;
 }
 
+using PassKernel = void (*)(const TMaps, PassArgs, int);
+PassKernel kern_a(const pot3d_ctx *ctx) {
+  return ctx->pc == 2 ? k_pass_a_pc2 : k_pass_a_pc1;
+}
+PassKernel kern_b(const pot3d_ctx *ctx) {
+  return ctx->pc == 2 ? k_pass_b_pc2 : k_pass_b_pc1;
+}
+
 // One PCG iteration (a3-a10) enqueued on ctx->stream; parity = iteration & 1.
 //   [multi-rank] edge shells of p_new -> NCCL halo
 //   pass A  (p_new, q = A p_new, sigma partial, lazy x update) -> alpha
@@ -468,7 +476,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     PassArgs ax = a;
     ax.G.part = 3;
     ax.peers = pt;
-    CK(launch_k(ctx->pdl, pc2 ? k_pass_a_pc2 : k_pass_a_pc1, grd, dim3(NTHREADS), SMEM_A,
+    CK(launch_k(ctx->pdl, kern_a(ctx), grd, dim3(NTHREADS), SMEM_A,
                 ctx->stream, ctx->tmaps, ax, parity));
     MARK("passA");
     CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_A, 0,
@@ -477,7 +485,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     PassArgs bx = ab;
     bx.peers = pt;
     bx.fold = fold;  // pass B only posts its sums and marks them pending
-    CK(launch_k(ctx->pdl, pc2 ? k_pass_b_pc2 : k_pass_b_pc1, grdb, dim3(NTHREADS), SMEM_B,
+    CK(launch_k(ctx->pdl, kern_b(ctx), grdb, dim3(NTHREADS), SMEM_B,
                 ctx->stream, ctx->tmaps, bx, parity));
     MARK("passB");
     ctx->n_enq += 4;
@@ -521,20 +529,14 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     ae.G.part = 2;
     ae.G.blk_off = ntl * nci;
     ae.G.blk_total = ntl * (nci + 2);
-    if (pc2)
-      k_pass_a_pc2<<<dim3(ntl, nci), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ai, parity);
-    else
-      k_pass_a_pc1<<<dim3(ntl, nci), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ai, parity);
-    CK(cudaGetLastError());
+    CK(launch_k(false, kern_a(ctx), dim3(ntl, nci), dim3(NTHREADS), SMEM_A, ctx->stream, ctx->tmaps, ai,
+                parity));
     ctx->n_enq++;
     MARK("passA_interior");
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
     MARK("halo_wait");
-    if (pc2)
-      k_pass_a_pc2<<<dim3(ntl, 2), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ae, parity);
-    else
-      k_pass_a_pc1<<<dim3(ntl, 2), NTHREADS, SMEM_A, ctx->stream>>>(ctx->tmaps, ae, parity);
-    CK(cudaGetLastError());
+    CK(launch_k(false, kern_a(ctx), dim3(ntl, 2), dim3(NTHREADS), SMEM_A, ctx->stream, ctx->tmaps, ae,
+                parity));
     ctx->n_enq++;
     MARK("passA_edge");
   } else {
@@ -546,7 +548,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
       ctx->n_enq++;
       TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
     }
-    CK(launch_k(ctx->pdl && !multi, pc2 ? k_pass_a_pc2 : k_pass_a_pc1, grd, dim3(NTHREADS), SMEM_A,
+    CK(launch_k(ctx->pdl && !multi, kern_a(ctx), grd, dim3(NTHREADS), SMEM_A,
                 ctx->stream, ctx->tmaps, a, parity));
     ctx->n_enq++;
   }
@@ -558,7 +560,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     ctx->n_enq++;
     MARK("finalize_alpha");
   }
-  CK(launch_k(ctx->pdl && !multi, pc2 ? k_pass_b_pc2 : k_pass_b_pc1, grdb, dim3(NTHREADS), SMEM_B,
+  CK(launch_k(ctx->pdl && !multi, kern_b(ctx), grdb, dim3(NTHREADS), SMEM_B,
               ctx->stream, ctx->tmaps, ab, parity));
     ctx->n_enq++;
   MARK("passB");
@@ -890,6 +892,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   }
   ctx->M = Metrics{ctx->m_arp, ctx->m_arm, ctx->m_dr, ctx->m_ss, ctx->m_g, ctx->m_atp,
                    ctx->m_atm, ctx->m_q, ctx->m_dp, ctx->m_app, ctx->m_apm};
+
 
   // vectors with ghost shells
   const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
@@ -1299,14 +1302,12 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
     a.hist = nullptr;
     a.finalize = 1;
     CK(cudaEventRecord(ev[0], s));
-    if (pc2) k_pass_a_pc2<<<grd, NTHREADS, SMEM_A, s>>>(ctx->tmaps, a, par); else k_pass_a_pc1<<<grd, NTHREADS, SMEM_A, s>>>(ctx->tmaps, a, par);
-    CK(cudaGetLastError());
+    CK(launch_k(false, kern_a(ctx), grd, dim3(NTHREADS), SMEM_A, s, ctx->tmaps, a, par));
     CK(cudaEventRecord(ev[1], s));
     PassArgs ab = a;
     ab.G.nchunks = ctx->nchunks_b;
     dim3 grdb(G.ntj * G.ntk, ctx->nchunks_b);
-    if (pc2) k_pass_b_pc2<<<grdb, NTHREADS, SMEM_B, s>>>(ctx->tmaps, ab, par); else k_pass_b_pc1<<<grdb, NTHREADS, SMEM_B, s>>>(ctx->tmaps, ab, par);
-    CK(cudaGetLastError());
+    CK(launch_k(false, kern_b(ctx), grdb, dim3(NTHREADS), SMEM_B, s, ctx->tmaps, ab, par));
     CK(cudaEventRecord(ev[2], s));
     ctx->n_launch += 2;
     if (pc2) {

@@ -243,6 +243,11 @@ __device__ __forceinline__ DiagRow diag_row(const PlaneC &P, const RowC &R) {
 }
 
 
+// The Jacobi diagonal of a cell, in one fixed evaluation order for every kernel
+// (pass A, pass B, the edge-shell kernel, the init dots): diag = dp_k a + b (app_k + apm_k).
+__device__ __forceinline__ double diag_at(double dpk, const DiagRow &d, double appk, double apmk) {
+  return fma(dpk, d.a, d.b * (appk + apmk));
+}
 // r / d for d > 0 (normal): approximate reciprocal (MUFU.RCP64H, ~2^-20), one
 // Newton step (~2^-40), product, then one remainder correction
 // q1 = q0 + y (r - d q0), which leaves the quotient within ~1 ulp of the
@@ -256,6 +261,10 @@ __device__ __forceinline__ double fdiv(double r, double d) {
   double rem = fma(-d, q, r);
   return fma(y, rem, q);
 }
+
+// z = D^-1 r, the same corrected quotient in every kernel (pass A, pass B, the
+// edge-shell kernel, the init dots), so a ghost copy equals the owner's value bitwise
+__device__ __forceinline__ double jacobi(double r, double dk) { return fdiv(r, dk); }
 
 // cp.async (LDGSTS) with zero-fill: copies src_bytes of 16 (8) and fills the
 // rest of the destination with zeros; src_bytes = 0 reads nothing.

@@ -203,9 +203,10 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
       const PlaneC P = plane_c(M, G.i0 + il);
       const RowC R = row_c(M, j);
       const DiagRow d = diag_row(P, R);
-      zv = src[o] / (__ldg(M.dp + k) * d.a + d.b * (__ldg(M.app + k) + __ldg(M.apm + k)));
+      zv = jacobi(src[o], diag_at(__ldg(M.dp + k), d, __ldg(M.app + k), __ldg(M.apm + k)));
     }
-    const double v = (mode < 0) ? zv : zv + beta * p_old[o];
+    // same arithmetic as pass A, so the ghost copy equals the owner's value bitwise
+    const double v = (mode < 0) ? zv : fma(beta, p_old[o], zv);
     p_new[o] = v;
     if (k == 0) p_new[o + G.np] = v;           // periodic ghost columns
     if (k == G.np - 1) p_new[o - G.np] = v;
@@ -304,7 +305,7 @@ __global__ void k_init_dots(Grid G, Metrics M, Scalars *S, const double *r, doub
       const PlaneC P = plane_c(M, G.i0 + il);
       const RowC R = row_c(M, j);
       const DiagRow d = diag_row(P, R);
-      zv = rv / (__ldg(M.dp + k) * d.a + d.b * (__ldg(M.app + k) + __ldg(M.apm + k)));
+      zv = jacobi(rv, diag_at(__ldg(M.dp + k), d, __ldg(M.app + k), __ldg(M.apm + k)));
     }
     a0 += rv * zv;
     a1 += rv * rv;

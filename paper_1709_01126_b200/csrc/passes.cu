@@ -323,8 +323,10 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
         pn.y = ghost ? rv.y : fma(beta, pv.y, rv.y);
       } else {
         const DiagRow d = diag_row(P, rw[e]);
-        pn.x = selp(rv.x, fdiv(rv.x, dp.x * d.a + d.b * (ap.x + am.x)) + beta * pv.x, ghost);
-        pn.y = selp(rv.y, fdiv(rv.y, dp.y * d.a + d.b * (ap.y + am.y)) + beta * pv.y, ghost);
+        const double z0 = jacobi(rv.x, diag_at(dp.x, d, ap.x, am.x));
+        const double z1 = jacobi(rv.y, diag_at(dp.y, d, ap.y, am.y));
+        pn.x = selp(rv.x, fma(beta, pv.x, z0), ghost);
+        pn.y = selp(rv.y, fma(beta, pv.y, z1), ghost);
       }
       R[u][e] = pn;
       *reinterpret_cast<double2 *>(&sm.pn[u][r][cs]) = pn;
@@ -475,8 +477,8 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
           acc_rr += (t.st0 ? rn.x * rn.x : 0.0) + (t.st1 ? rn.y * rn.y : 0.0);
         } else {
           const DiagRow d = diag_row(P, rw[e]);
-          const double z0 = fdiv(rn.x, dp.x * d.a + d.b * (ap.x + am.x));
-          const double z1 = fdiv(rn.y, dp.y * d.a + d.b * (ap.y + am.y));
+          const double z0 = jacobi(rn.x, diag_at(dp.x, d, ap.x, am.x));
+          const double z1 = jacobi(rn.y, diag_at(dp.y, d, ap.y, am.y));
           acc_rz += (t.st0 ? rn.x * z0 : 0.0) + (t.st1 ? rn.y * z1 : 0.0);
           acc_rr += (t.st0 ? rn.x * rn.x : 0.0) + (t.st1 ? rn.y * rn.y : 0.0);
         }
