@@ -23,6 +23,7 @@
 // neighbour terms is fixed (r, theta, phi), so the sweep equals the
 // sequential ILU0 solve up to rounding.
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -30,6 +31,9 @@
 #include "device_common.cuh"
 
 namespace pot3d {
+
+template <int V>
+using IC2 = std::integral_constant<int, V>;
 
 constexpr int WJ = 8;            // tile rows (theta)
 constexpr int WK = 32;           // tile columns (phi): one warp per row
@@ -295,21 +299,16 @@ constexpr int SWK = SV * SNR;    // 128 phi columns per tile
 #ifndef POT3D_SWJ
 #define POT3D_SWJ 8
 #endif
-#ifndef POT3D_SPD_F
-#define POT3D_SPD_F 4
-#endif
-#ifndef POT3D_SPD_B
-#define POT3D_SPD_B 4
-#endif
 constexpr int SWJ = POT3D_SWJ;   // tile rows
 constexpr int SWT = SWJ * SNR;   // 256 threads
+#ifndef POT3D_SPD
+#define POT3D_SPD 2
+#endif
+constexpr int SPD = POT3D_SPD;   // register prefetch depth (steps)
 
 template <int MODE> struct Sw4 {
-  static constexpr int NA = (MODE == SW_FWD) ? 2 : 3;  // FWD: r, 1/d; BWD: w, 1/d, r
-  static constexpr int PD = (MODE == SW_FWD) ? POT3D_SPD_F : POT3D_SPD_B;  // prefetch depth (power of 2)
-  static constexpr int RING = PD * NA * SWT * SV;      // doubles
-  static constexpr int JR = PD * SNR * SV, KR = PD * SWJ * 2, XW = 2 * SWJ * SNR * SV;
-  static constexpr size_t SMEM = (size_t)(RING + JR + KR + XW) * sizeof(double);
+  static constexpr int XW = 2 * SWJ * SNR * SV;        // doubles of the step exchange
+  static constexpr size_t SMEM = (size_t)XW * sizeof(double);
 };
 
 // virtual phi offset of the first run so that every run starts on a 32-B
@@ -320,36 +319,39 @@ __host__ __device__ inline int sweep4_koff(int np, bool rev) {
   return o > 0 ? o - 4 : o;
 }
 
-__device__ __forceinline__ double2 lds2(unsigned a) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
-  return v;
+// 256-bit global accesses (one L1TEX wavefront per lane and run)
+__device__ __forceinline__ void ldg4(const double *p, double (&v)[4]) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p) : "memory");
 }
-__device__ __forceinline__ double lds1(unsigned a) {
+__device__ __forceinline__ void ldg4_cg(const double *p, double (&v)[4]) {  // L2 only (edge slots)
+  asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void stg4(double *p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+__device__ __forceinline__ void stg4_cg(double *p, double a, double b, double c, double d) {
+  asm volatile("st.global.cg.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+__device__ __forceinline__ double ldg_cg(const double *p) {
   double v;
-  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
+  asm volatile("ld.global.cg.f64 %0, [%1];\n" : "=d"(v) : "l"(p) : "memory");
   return v;
-}
-__device__ __forceinline__ void sts2(unsigned a, double x, double y) {
-  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(x), "d"(y) : "memory");
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(SWT, 1) k_sweep4(SweepArgs A, int koff, int ntk4) {
-  using C = Sw4<MODE>;
-  constexpr int PD = C::PD, NA = C::NA;
   constexpr bool rev = (MODE == SW_BWD);
-  constexpr unsigned ASTR = SWT * SV * 8, SLOT = NA * ASTR;        // ring: array / slot strides
-  constexpr unsigned XB = SWJ * SNR * SV * 8;                      // xw buffer stride
+  constexpr int PD = SPD;
   const Grid &G = A.G;
   const Metrics &M = A.M;
   if (A.predicated && A.S->stop) return;
   extern __shared__ __align__(16) double sm4[];
-  double *ring = sm4;                       // [PD][NA][SWT][SV]
-  double *jring = ring + C::RING;           // [PD][SNR][SV]
-  double *kring = jring + C::JR;            // [PD][SWJ][2]
-  double *xw = kring + C::KR;               // [2][SWJ][SNR][SV]
-  double *crs = xw + C::XW;                 // [nbmax] r coupling factor of virtual shell iv
+  double *xw = sm4;                         // [2][SWJ][SNR][SV] step exchange
+  double *crs = xw + Sw4<MODE>::XW;         // [nbmax] r coupling factor of virtual shell iv
   double *drs = crs + A.nbmax;              // [nbmax] dr of virtual shell iv
   __shared__ int s_ticket;
   __shared__ double sred[SWT / 32];
@@ -416,108 +418,80 @@ __global__ void __launch_bounds__(SWT, 1) k_sweep4(SweepArgs A, int koff, int nt
   const double *src0 = (MODE == SW_FWD) ? A.r : A.z;  // FWD: r; BWD: w (forward output)
   const double *src1 = A.inv_d;
   const double *src2 = A.r;                          // BWD: r for the r.z partial
-  // shared addresses (32-bit)
-  const unsigned ring_me = smem_u32(ring) + (unsigned)(tid * SV * 8);
-  const unsigned jr_me = smem_u32(jring) + (unsigned)(m * SV * 8);
-  const unsigned kr_me = smem_u32(kring) + (unsigned)(jj * 2 * 8);
-  const unsigned xw0 = smem_u32(xw);
-  const unsigned xo_me = xw0 + (unsigned)((jj * SNR + m) * SV * 8);
-  const unsigned xj_me = xw0 + (unsigned)(((jj > 0 ? jj - 1 : 0) * SNR + m) * SV * 8);
-  const unsigned xk_me = xw0 + (unsigned)((jj * SNR + (m > 0 ? m - 1 : 0)) * SV * 8 + (SV - 1) * 8);
-  const unsigned crs_a = smem_u32(crs), drs_a = smem_u32(drs);
-  const int ts_lo = jj + m, ts_hi = jj + m + nb;     // steps with a cell of this thread
-  auto prefetch = [&](int ts) {
-    const bool ok = any && ts >= ts_lo && ts < ts_hi;
-    const long long o = ok ? o0 + (long long)ts * ostep : 0;
-    const int sb = ok ? 16 : 0;
-    const unsigned sl = (unsigned)(ts & (PD - 1));
-    const unsigned d = ring_me + sl * SLOT;
-    cp_async16s(d, src0 + o, sb);
-    cp_async16s(d + 16, src0 + o + 2, sb);
-    cp_async16s(d + ASTR, src1 + o, sb);
-    cp_async16s(d + ASTR + 16, src1 + o + 2, sb);
-    if (NA == 3) {
-      cp_async16s(d + 2 * ASTR, src2 + o, sb);
-      cp_async16s(d + 2 * ASTR + 16, src2 + o + 2, sb);
+  const int ts_lo = jj + m;                          // first step with a cell of this thread
+  double *xo_me = xw + (jj * SNR + m) * SV;
+  const double *xj_me = xw + ((jj > 0 ? jj - 1 : 0) * SNR + m) * SV;
+  const double *xk_me = xw + (jj * SNR + (m > 0 ? m - 1 : 0)) * SV + SV - 1;
+  constexpr int XB = SWJ * SNR * SV;
+
+  // register prefetch ring (PD steps ahead), slot = step mod PD (compile-time by unrolling)
+  double ra[PD][SV], rb[PD][SV], rc[PD][SV], rj[PD][SV], rk[PD];
+  int pf_t = 0;
+  long long pf_o = o0;
+  auto prefetch = [&](auto U) {
+    constexpr int u = decltype(U)::value;
+    const int iv = pf_t - ts_lo;
+    if (any && (unsigned)iv < (unsigned)nb) {
+      ldg4(src0 + pf_o, ra[u]);
+      ldg4(src1 + pf_o, rb[u]);
+      if (MODE == SW_BWD) ldg4(src2 + pf_o, rc[u]);
+      if (need_j) ldg4_cg(up_bot + iv * SV, rj[u]);
+      if (need_k) rk[u] = ldg_cg(lf_rgt + iv * 2);
     }
-    if (need_j) {
-      const double *g0 = up_bot + (ok ? (long long)(ts - ts_lo) * SV : 0);
-      cp_async16s(jr_me + sl * (SNR * SV * 8), g0, sb);
-      cp_async16s(jr_me + sl * (SNR * SV * 8) + 16, g0 + 2, sb);
-    }
-    if (need_k)
-      cp_async16s(kr_me + sl * (SWJ * 2 * 8), lf_rgt + (ok ? (long long)(ts - ts_lo) * 2 : 0), sb);
-    cp_async_commit();
+    ++pf_t;
+    pf_o += ostep;
   };
 
-  const int nsteps = nb + SWJ + SNR - 2;
-#pragma unroll 1
-  for (int u = 0; u < PD; u++) prefetch(u);
   double wprev[SV];
 #pragma unroll
   for (int e = 0; e < SV; e++) wprev[e] = 0.0;
   double acc = 0.0;
   bool proto = false;
-#pragma unroll 1
-  for (int t = 0; t < nsteps; t++) {
-    cp_async_wait<PD - 1>();  // this thread's operands of step t have landed
-    __syncthreads();          // step t-1 of the neighbouring threads is in xw; crs/drs staged
+  double *zr = A.z + o0;  // the run at step t (advanced every step)
+
+  auto step = [&](auto U, int t) {
+    constexpr int u = decltype(U)::value;
+    __syncthreads();  // step t-1 of the neighbouring threads is in xw; crs/drs staged
     const int ivt = t - ts_lo;
-    if (any && ivt >= 0 && ivt < nb) {
-      const unsigned sl = (unsigned)(t & (PD - 1));
-      const unsigned rs = ring_me + sl * SLOT;
+    if (any && (unsigned)ivt < (unsigned)nb) {
       double a0[SV], b0[SV], c0[SV];
-      {
-        const double2 x0 = lds2(rs), x1 = lds2(rs + 16);
-        const double2 y0 = lds2(rs + ASTR), y1 = lds2(rs + ASTR + 16);
-        // the ring holds physical column order
-        a0[0] = rev ? x1.y : x0.x; a0[1] = rev ? x1.x : x0.y; a0[2] = rev ? x0.y : x1.x; a0[3] = rev ? x0.x : x1.y;
-        b0[0] = rev ? y1.y : y0.x; b0[1] = rev ? y1.x : y0.y; b0[2] = rev ? y0.y : y1.x; b0[3] = rev ? y0.x : y1.y;
-        if (NA == 3) {
-          const double2 w0 = lds2(rs + 2 * ASTR), w1 = lds2(rs + 2 * ASTR + 16);
-          c0[0] = w1.y; c0[1] = w1.x; c0[2] = w0.y; c0[3] = w0.x;
-        } else {
-          c0[0] = c0[1] = c0[2] = c0[3] = 0.0;
-        }
+#pragma unroll
+      for (int e = 0; e < SV; e++) {  // registers hold physical column order
+        const int pe = rev ? SV - 1 - e : e;
+        a0[e] = ra[u][pe];
+        b0[e] = rb[u][pe];
+        c0[e] = (MODE == SW_BWD) ? rc[u][pe] : 0.0;
       }
-      const unsigned xb_prev = ((t - 1) & 1) ? XB : 0u;
+      const double *xp = (t & 1) ? xw : xw + XB;  // buffer of step t-1
       double vj[SV], vk;
       if (jj > 0) {
-        const double2 u0 = lds2(xj_me + xb_prev), u1 = lds2(xj_me + xb_prev + 16);
+        const double2 u0 = *reinterpret_cast<const double2 *>(xp + (xj_me - xw));
+        const double2 u1 = *reinterpret_cast<const double2 *>(xp + (xj_me - xw) + 2);
         vj[0] = u0.x; vj[1] = u0.y; vj[2] = u1.x; vj[3] = u1.y;
-      } else {
-        const unsigned jr = jr_me + sl * (SNR * SV * 8);
-        const double2 u0 = lds2(jr), u1 = lds2(jr + 16);
-        vj[0] = u0.x; vj[1] = u0.y; vj[2] = u1.x; vj[3] = u1.y;
-        if (need_j) {
-          double *slot = up_bot + (long long)ivt * SV;
+      } else if (need_j) {
+        double *slot = up_bot + (long long)ivt * SV;
 #pragma unroll
-          for (int e = 0; e < SV; e++) {
-            if (ve[e]) {
-              if (is_sent(vj[e])) vj[e] = poll_slot(slot + e, vj[e], A.sync + 1, proto);
-            } else {
-              vj[e] = 0.0;
-            }
-          }
-          // re-arm all four slots: the producer stores whole runs, and FWD / BWD
-          // (different run offsets) share the slots
-          const ulonglong2 s2 = make_ulonglong2(SENT, SENT);
-          __stcg(reinterpret_cast<ulonglong2 *>(slot), s2);
-          __stcg(reinterpret_cast<ulonglong2 *>(slot + 2), s2);
-        } else {
-          vj[0] = vj[1] = vj[2] = vj[3] = 0.0;
+        for (int e = 0; e < SV; e++) {
+          double v = rj[u][e];
+          if (ve[e] && is_sent(v)) v = poll_slot(slot + e, v, A.sync + 1, proto);
+          vj[e] = ve[e] ? v : 0.0;
         }
+        // re-arm all four slots: the producer stores whole runs, FWD / BWD share them
+        stg4_cg(slot, __longlong_as_double((long long)SENT), __longlong_as_double((long long)SENT),
+                __longlong_as_double((long long)SENT), __longlong_as_double((long long)SENT));
+      } else {
+        vj[0] = vj[1] = vj[2] = vj[3] = 0.0;
       }
       if (m > 0) {
-        vk = lds1(xk_me + xb_prev);
+        vk = xp[xk_me - xw];
       } else if (need_k) {
-        vk = lds1(kr_me + sl * (SWJ * 2 * 8));
+        vk = rk[u];
         if (is_sent(vk)) vk = poll_slot(lf_rgt + (long long)ivt * 2, vk, A.sync + 1, proto);
         __stcg(reinterpret_cast<unsigned long long *>(lf_rgt + (long long)ivt * 2), SENT);
       } else {
         vk = 0.0;
       }
-      const double cr = lds1(crs_a + ivt * 8), dr = lds1(drs_a + ivt * 8);
+      const double cr = crs[ivt], dr = drs[ivt];
       double val[SV];
 #pragma unroll
       for (int e = 0; e < SV; e++) {
@@ -533,32 +507,41 @@ __global__ void __launch_bounds__(SWT, 1) k_sweep4(SweepArgs A, int koff, int nt
         vk = v;
       }
       // results: z (w for FWD), physical order col_lo .. col_lo+3
-      double *zr = A.z + o0 + (long long)t * ostep;
-      const double2 p0 = rev ? make_double2(val[3], val[2]) : make_double2(val[0], val[1]);
-      const double2 p1 = rev ? make_double2(val[1], val[0]) : make_double2(val[2], val[3]);
       if (full) {
-        *reinterpret_cast<double2 *>(zr) = p0;
-        *reinterpret_cast<double2 *>(zr + 2) = p1;
+        if (rev)
+          stg4(zr, val[3], val[2], val[1], val[0]);
+        else
+          stg4(zr, val[0], val[1], val[2], val[3]);
       } else {
-        if (rev ? ve[3] : ve[0]) zr[0] = p0.x;
-        if (rev ? ve[2] : ve[1]) zr[1] = p0.y;
-        if (rev ? ve[1] : ve[2]) zr[2] = p1.x;
-        if (rev ? ve[0] : ve[3]) zr[3] = p1.y;
+        if (rev ? ve[3] : ve[0]) zr[0] = rev ? val[3] : val[0];
+        if (rev ? ve[2] : ve[1]) zr[1] = rev ? val[2] : val[1];
+        if (rev ? ve[1] : ve[2]) zr[2] = rev ? val[1] : val[2];
+        if (rev ? ve[0] : ve[3]) zr[3] = rev ? val[0] : val[3];
       }
-      if (put_bot) {
-        __stcg(reinterpret_cast<double2 *>(my_bot + (long long)ivt * SV), make_double2(val[0], val[1]));
-        __stcg(reinterpret_cast<double2 *>(my_bot + (long long)ivt * SV + 2), make_double2(val[2], val[3]));
-      }
+      if (put_bot) stg4_cg(my_bot + (long long)ivt * SV, val[0], val[1], val[2], val[3]);
       if (put_rgt) __stcg(my_rgt + (long long)ivt * 2, val[SV - 1]);
-      const unsigned xb = (t & 1) ? XB : 0u;
-      sts2(xo_me + xb, val[0], val[1]);
-      sts2(xo_me + xb + 16, val[2], val[3]);
+      double *xo = ((t & 1) ? xw + XB : xw) + (xo_me - xw);
+      *reinterpret_cast<double2 *>(xo) = make_double2(val[0], val[1]);
+      *reinterpret_cast<double2 *>(xo + 2) = make_double2(val[2], val[3]);
 #pragma unroll
       for (int e = 0; e < SV; e++) wprev[e] = val[e];
     }
-    prefetch(t + PD);  // into the ring slot this step has just consumed
+    zr += ostep;
+    prefetch(U);  // step t + PD into this slot
+  };
+
+  const int nsteps = nb + SWJ + SNR - 2;
+  prefetch(IC2<0>{});
+  if (PD > 1) prefetch(IC2<(PD > 1 ? 1 : 0)>{});
+  if (PD > 2) prefetch(IC2<(PD > 2 ? 2 : 0)>{});
+  if (PD > 3) prefetch(IC2<(PD > 3 ? 3 : 0)>{});
+#pragma unroll 1
+  for (int t = 0; t < nsteps; t += PD) {
+    step(IC2<0>{}, t);
+    if (PD > 1) { if (t + 1 >= nsteps) break; step(IC2<(PD > 1 ? 1 : 0)>{}, t + 1); }
+    if (PD > 2) { if (t + 2 >= nsteps) break; step(IC2<(PD > 2 ? 2 : 0)>{}, t + 2); }
+    if (PD > 3) { if (t + 3 >= nsteps) break; step(IC2<(PD > 3 ? 3 : 0)>{}, t + 3); }
   }
-  cp_async_wait<0>();
   if (__syncthreads_or(proto) && tid == 0) atomicOr(&A.sync[1], 2);  // protocol error
   if (MODE == SW_BWD) {
     double v[1] = {acc}, tot[1];

@@ -6,11 +6,11 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "s8p44": [],
-    "s8p22": ["POT3D_SPD_F=2", "POT3D_SPD_B=2"],
-    "s16p42": ["POT3D_SWJ=16", "POT3D_SPD_F=4", "POT3D_SPD_B=2"],
-    "s16p22": ["POT3D_SWJ=16", "POT3D_SPD_F=2", "POT3D_SPD_B=2"],
-    "s4p44": ["POT3D_SWJ=4"],
+    "pd3": [],
+    "pd2": ["POT3D_SPD=2"],
+    "pd4": ["POT3D_SPD=4"],
+    "j4pd3": ["POT3D_SWJ=4"],
+    "j16pd2": ["POT3D_SWJ=16", "POT3D_SPD=2"],
 }
 out = Path(build.PKG) / "variants"
 out.mkdir(exist_ok=True)
