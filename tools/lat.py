@@ -11,7 +11,11 @@ world = int(os.environ.get("WORLD_SIZE", "1")); rank = int(os.environ.get("RANK"
 local = int(os.environ.get("LOCAL_RANK", "0")); torch.cuda.set_device(local)
 if world > 1:
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-c = synth.weak_config(world) if cfg == "weak" else synth.CONFIGS[cfg]
+if "x" in cfg:  # nr x nt x np, nonuniform like the BASELINE configs
+    nr, nt, np_ = (int(v) for v in cfg.split("x"))
+    c = synth.Config(cfg, nr, nt, np_)
+else:
+    c = synth.weak_config(world) if cfg == "weak" else synth.CONFIGS[cfg]
 rf, tf, pf = c.faces()
 with Pot3d(rf, tf, pf, c.br0(), rank=rank, nranks=world) as s:
     s.solve(rtol=0.0, maxit=50, true_residual=False, want_phi=False)
