@@ -28,6 +28,7 @@ struct pot3d_ctx {
   int rank = 0, nranks = 1, pc2_blocks = 1, unroll = 8;
   int nchunks_b = 1;  // r-chunks of pass B (G.nchunks: pass A)
   bool pdl = true;    // programmatic dependent launch for the loop kernels (POT3D_PDL=0: off)
+  int edge_blocks = 148 * 4;  // grid of the edge-shell kernel (POT3D_EDGE_BLOCKS)
   int device = 0;
   double r0 = 1.0;
   Grid G{};
@@ -68,6 +69,7 @@ struct pot3d_ctx {
   PeerTab *peers = nullptr;           // device copy
   std::vector<void *> ipc_own, ipc_open;
   unsigned long long epoch = 0;       // solves (and profile runs) so far
+  unsigned long long *trace = nullptr;  // POT3D_TRACE diagnostics (kernel timestamps)
   // graphs
   cudaGraphExec_t gexec = nullptr;
   int graph_unroll = 0;
@@ -469,7 +471,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     const PeerTab *pt = ctx->peers;
     // PC1: the previous iteration's beta finalisation lives in edge_p (fold)
     const int fold = pc2 ? 0 : 1;
-    CK(launch_k(ctx->pdl, k_edge_p, dim3(148 * 4), dim3(256), 0, ctx->stream, G, ctx->M, ctx->S,
+    CK(launch_k(ctx->pdl, k_edge_p, dim3(ctx->edge_blocks), dim3(256), 0, ctx->stream, G, ctx->M, ctx->S,
                 (const double *)(pc2 ? ctx->z : ctx->r), (const double *)ctx->P[parity],
                 ctx->P[parity ^ 1], pc2 ? 1 : 0, pt, parity ^ 1, ctx->hist, fold));
     MARK("edge_p");
@@ -799,6 +801,8 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   {
     const char *e = getenv("POT3D_PDL");
     ctx->pdl = !(e && atoi(e) == 0);
+    const char *eb = getenv("POT3D_EDGE_BLOCKS");
+    if (eb && atoi(eb) > 0) ctx->edge_blocks = atoi(eb);
   }
   pot3d_runtime R{};
   R.nranks = 1;
@@ -1018,6 +1022,11 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
   }
   Scalars h0{};
   h0.epoch = ++ctx->epoch;
+  if (getenv("POT3D_TRACE") && !ctx->trace) {
+    TRY(dalloc(ctx, &ctx->trace, 64 * 16));
+  }
+  if (ctx->trace) CK(cudaMemsetAsync(ctx->trace, 0, 64 * 16 * sizeof(unsigned long long), s));
+  h0.trace = ctx->trace;
   h0.rtol = rtol;
   h0.maxit = (long long)std::min<int64_t>(maxit, hlen - 1);
   CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
@@ -1084,6 +1093,25 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
   CK(cudaStreamSynchronize(s));
   const Scalars hs = *ctx->hS;
   ctx->last_iters = hs.iter;
+  if (ctx->trace) {  // mean per-iteration timeline relative to the edge-shell kernel's start
+    std::vector<unsigned long long> t(64 * 16);
+    cudaMemcpy(t.data(), ctx->trace, t.size() * 8, cudaMemcpyDeviceToHost);
+    const char *nm[10] = {"edge0", "edge1", "A0", "Ahalo", "A1", "fin0", "fin1", "B0", "B1", "edgeM"};
+    double sum[10] = {0}, n = 0, per = 0;
+    for (int it = 0; it < 64; it++) {
+      const unsigned long long *r = &t[it * 16];
+      if (!r[0] || !r[8]) continue;
+      for (int q = 0; q < 10; q++) sum[q] += r[q] ? (double)(long long)(r[q] - r[0]) : 0.0;
+      const unsigned long long *nx = &t[((it + 1) % 64) * 16];
+      if (nx[0] > r[0]) per += (double)(nx[0] - r[0]);
+      n++;
+    }
+    if (n > 0) {
+      fprintf(stderr, "POT3D_TRACE rank %d (us after edge0, mean of %.0f iterations):", ctx->rank, n);
+      for (int q = 0; q < 10; q++) fprintf(stderr, " %s %.1f", nm[q], sum[q] / n / 1e3);
+      fprintf(stderr, " | iteration %.1f\n", per / n / 1e3);
+    }
+  }
   if (ctx->pc == 2 && (pc2_status(ctx->pc2, s) & 2)) {
     ctx->err = "PC2 sweep handoff protocol error (bounded wait expired)";
     return POT3D_ERR_CUDA;

@@ -154,7 +154,13 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// this rank's (v0, v1) of `kind` into every rank's mailbox
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// this rank's (v0, v1) of `kind` into every rank's mailbox: all value stores, ONE
+// system-scope fence, then the sequence numbers (fence + relaxed store = release);
+// one NVLink round trip on the critical path instead of one per rank
 __device__ __forceinline__ void mail_post(const PeerTab *T, int kind, double v0, double v1,
                                           unsigned long long seq) {
   const int me = T->rank;
@@ -162,8 +168,9 @@ __device__ __forceinline__ void mail_post(const PeerTab *T, int kind, double v0,
     MailEntry *e = &T->mail[r]->e[kind][me];
     *reinterpret_cast<volatile double *>(&e->v0) = v0;
     *reinterpret_cast<volatile double *>(&e->v1) = v1;
-    st_release_sys(&e->seq, seq);
   }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int r = 0; r < T->nranks; r++) st_relaxed_sys(&T->mail[r]->e[kind][me].seq, seq);
 }
 
 // spin until *flag == seq; false (and S->xfer_error set) when the wait expired
@@ -179,6 +186,15 @@ __device__ __forceinline__ bool xfer_wait(const unsigned long long *flag, unsign
     }
   }
   return true;
+}
+
+// diagnostics (POT3D_TRACE): %globaltimer of an event of the current iteration
+enum TraceSlot { TR_EDGE0 = 0, TR_EDGE1, TR_A0, TR_AHALO, TR_A1, TR_F0, TR_F1, TR_B0, TR_B1, TR_EDGEM };
+__device__ __forceinline__ void trace_mark(Scalars *S, int slot) {
+  if (S->trace) S->trace[(S->iter & 63) * 16 + slot] = global_ns();
+}
+__device__ __forceinline__ void trace_max(Scalars *S, int slot) {
+  if (S->trace) atomicMax(&S->trace[(S->iter & 63) * 16 + slot], global_ns());
 }
 
 // every rank's entry of `kind` for seq, summed in rank order (bit-identical on all ranks);

@@ -144,6 +144,7 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
   pdl_trigger();
   pdl_wait();
   if (mode >= 0 && S->stop) return;
+  const unsigned long long t_start = (S->trace && blockIdx.x == 0 && threadIdx.x == 0) ? global_ns() : 0ull;
   // fold (peer memory, PC1): finalise the previous pass B here -- every block sums
   // the ranks' (r.z, r.r) from the mailbox in rank order and takes the same
   // decisions; only the last block (after every block has read S) writes S
@@ -178,6 +179,10 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
   __syncthreads();
   const double beta = s_beta;
   const long long iter = pend ? iter0 + 1 : iter0;  // the iteration p_k belongs to
+  if (t_start) {
+    S->trace[(iter & 63) * 16 + TR_EDGE0] = t_start;
+    S->trace[(iter & 63) * 16 + TR_EDGEM] = global_ns();  // mailbox collected
+  }
   const long long per = (long long)G.nt * G.np;
   const long long n = (mode < 0) ? per * G.nr_loc : (s_stop ? 0 : 2 * per);
   // peer memory: shell 0 also lands in rank-1's top ghost shell, shell nr_loc-1
@@ -228,6 +233,7 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
       S->counter[4] = 0u;
+      if (S->trace) S->trace[(iter & 63) * 16 + TR_EDGE1] = global_ns();  // iteration of p_k
       if (pend) {  // finalize_beta of the previous iteration
         S->pend_b = 0;
         if (s_status == -5) {
@@ -248,10 +254,10 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
         }
       }
       if (!s_stop) {
-        __threadfence_system();
+        __threadfence_system();  // + relaxed stores = release of every block's ghost stores
         const unsigned long long seq = mail_seq(S->epoch, iter + 1);
-        if (peers->rank > 0) st_release_sys(&peers->mail[peers->rank - 1]->halo[1], seq);
-        if (peers->rank < peers->nranks - 1) st_release_sys(&peers->mail[peers->rank + 1]->halo[0], seq);
+        if (peers->rank > 0) st_relaxed_sys(&peers->mail[peers->rank - 1]->halo[1], seq);
+        if (peers->rank < peers->nranks - 1) st_relaxed_sys(&peers->mail[peers->rank + 1]->halo[0], seq);
       }
     }
   }
@@ -263,6 +269,7 @@ __global__ void k_finalize_mail(Scalars *S, const PeerTab *peers, int kind, int 
   pdl_trigger();
   pdl_wait();
   if (S->stop) return;
+  if (what == 0) trace_mark(S, TR_F0);
   // kinds A/B belong to iteration iter+1 (iter not yet advanced); C follows finalize_rr
   const unsigned long long seq = mail_seq(S->epoch, what == 3 ? S->iter : S->iter + 1);
   double s0, s1;
@@ -271,9 +278,10 @@ __global__ void k_finalize_mail(Scalars *S, const PeerTab *peers, int kind, int 
     S->stop = 1;
     return;
   }
-  if (what == 0)
+  if (what == 0) {
     finalize_alpha(S, s0);
-  else if (what == 1)
+    trace_mark(S, TR_F1);
+  } else if (what == 1)
     finalize_beta(S, s0, s1, hist);
   else if (what == 2)
     finalize_rr(S, s1, hist);

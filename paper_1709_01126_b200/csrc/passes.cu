@@ -237,6 +237,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
           if (side == 0 ? A.peers->rank > 0 : A.peers->rank < A.peers->nranks - 1) {
             xfer_wait(&A.peers->mail[A.peers->rank]->halo[side], mail_seq(S->epoch, S->iter + 1), S);
             fence_proxy_async_global();
+            trace_max(S, TR_AHALO);
           }
         }
         mbar_arrive_expect_tx(&sm.bar[st], STAGE_BYTES / 2);
@@ -264,6 +265,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   pdl_trigger();
   pdl_wait();
   if (S->stop) return;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_mark(S, TR_A0);
   const double beta = S->beta;
   if (threadIdx.x == 0) {
     issue(0, 0);
@@ -368,6 +370,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   double v[1] = {acc}, tot[1];
   if (grid_sum<1>(v, A.partials, &S->counter[0], sred, tot, pass_bid(G), pass_nb(G)) &&
       threadIdx.x == 0) {
+    trace_mark(S, TR_A1);
     if (A.finalize)
       finalize_alpha(S, tot[0]);
     else if (A.peers)
@@ -429,6 +432,7 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   pdl_trigger();
   pdl_wait();
   if (S->stop) return;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_mark(S, TR_B0);
   const double alpha = S->alpha;
   if (threadIdx.x == 0)
     for (int s = 0; s < NS_B - 2; s++) issue();
@@ -506,6 +510,7 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   double v[2] = {acc_rz, acc_rr}, tot[2];
   if (grid_sum<2>(v, A.partials, &S->counter[1], sred, tot, pass_bid(G), pass_nb(G)) &&
       threadIdx.x == 0) {
+    trace_mark(S, TR_B1);
     if (A.finalize) {
       if (USE_Z)
         finalize_rr(S, tot[1], A.hist);  // PC2: rho' comes from the sweeps

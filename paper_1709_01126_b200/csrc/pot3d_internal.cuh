@@ -90,6 +90,7 @@ struct Scalars {
   int xfer_error;    // peer-memory wait expired
   int pend_b;        // peer-memory PC1: pass B posted its sums; the next edge-shell kernel
                      // finalises them (convergence test, beta) before it builds p_k
+  unsigned long long *trace;  // POT3D_TRACE: [64 iterations][16] %globaltimer marks, or null
 };
 
 // ---- peer-memory exchange between the rank processes (CUDA IPC over NVLink) ----
