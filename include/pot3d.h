@@ -160,6 +160,15 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
  * their ';'-separated names.  Invalidates the last solution. */
 int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *names, int32_t nmax);
 
+/* In-situ kernel timing of the solve loop itself (no extra launches): with
+ * tracing enabled before pot3d_solve, every fused pass records %globaltimer when
+ * its first block starts (after its dependency wait) and when its last block
+ * finishes, in a ring of the last 64 iterations.  pot3d_kernel_times returns the
+ * mean pass A and pass B durations (microseconds) over the ring and the number
+ * of iterations averaged (n).  POT3D_ERR_STATE if tracing was not enabled. */
+int pot3d_trace_enable(pot3d_ctx *ctx, int32_t on);
+int pot3d_kernel_times(pot3d_ctx *ctx, double *us_pass_a, double *us_pass_b, int32_t *n);
+
 /* Rank 0 creates the 128-byte NCCL unique id that every rank passes in
  * pot3d_runtime.nccl_unique_id (the caller broadcasts it, e.g. with
  * torch.distributed).  Returns 0 or POT3D_ERR_NCCL. */

@@ -69,7 +69,8 @@ struct pot3d_ctx {
   PeerTab *peers = nullptr;           // device copy
   std::vector<void *> ipc_own, ipc_open;
   unsigned long long epoch = 0;       // solves (and profile runs) so far
-  unsigned long long *trace = nullptr;  // POT3D_TRACE diagnostics (kernel timestamps)
+  unsigned long long *trace = nullptr;  // kernel timestamps (pot3d_trace_enable / POT3D_TRACE)
+  bool trace_on = false;
   // graphs
   cudaGraphExec_t gexec = nullptr;
   int graph_unroll = 0;
@@ -1022,7 +1023,7 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
   }
   Scalars h0{};
   h0.epoch = ++ctx->epoch;
-  if (getenv("POT3D_TRACE") && !ctx->trace) {
+  if ((ctx->trace_on || getenv("POT3D_TRACE")) && !ctx->trace) {
     TRY(dalloc(ctx, &ctx->trace, 64 * 16));
   }
   if (ctx->trace) CK(cudaMemsetAsync(ctx->trace, 0, 64 * 16 * sizeof(unsigned long long), s));
@@ -1093,7 +1094,7 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
   CK(cudaStreamSynchronize(s));
   const Scalars hs = *ctx->hS;
   ctx->last_iters = hs.iter;
-  if (ctx->trace) {  // mean per-iteration timeline relative to the edge-shell kernel's start
+  if (ctx->trace && getenv("POT3D_TRACE")) {  // mean per-iteration timeline after the edge-shell kernel
     std::vector<unsigned long long> t(64 * 16);
     cudaMemcpy(t.data(), ctx->trace, t.size() * 8, cudaMemcpyDeviceToHost);
     const char *nm[10] = {"edge0", "edge1", "A0", "Ahalo", "A1", "fin0", "fin1", "B0", "B1", "edgeM"};
@@ -1412,6 +1413,39 @@ int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *nam
   names[1023] = 0;
   ctx->solved = false;
   return n;
+}
+
+int pot3d_trace_enable(pot3d_ctx *ctx, int32_t on) {
+  if (!ctx) return POT3D_ERR_INVALID;
+  ctx->trace_on = on != 0;
+  return 0;
+}
+
+int pot3d_kernel_times(pot3d_ctx *ctx, double *us_pass_a, double *us_pass_b, int32_t *n) {
+  if (!ctx || !us_pass_a || !us_pass_b || !n) return POT3D_ERR_INVALID;
+  *n = 0;
+  if (!ctx->trace) {
+    ctx->err = "tracing not enabled (pot3d_trace_enable before pot3d_solve)";
+    return POT3D_ERR_STATE;
+  }
+  CK(cudaSetDevice(ctx->device));
+  std::vector<unsigned long long> t(64 * 16);
+  CK(cudaMemcpy(t.data(), ctx->trace, t.size() * 8, cudaMemcpyDeviceToHost));
+  double sa = 0, sb = 0;
+  int cnt = 0;
+  for (int it = 0; it < 64; it++) {
+    const unsigned long long *r = &t[it * 16];
+    if (!r[TR_A0] || !r[TR_A1] || !r[TR_B0] || !r[TR_B1] || r[TR_A1] < r[TR_A0] || r[TR_B1] < r[TR_B0]) continue;
+    sa += (double)(r[TR_A1] - r[TR_A0]);
+    sb += (double)(r[TR_B1] - r[TR_B0]);
+    cnt++;
+  }
+  if (cnt) {
+    *us_pass_a = sa / cnt / 1e3;
+    *us_pass_b = sb / cnt / 1e3;
+  }
+  *n = cnt;
+  return 0;
 }
 
 int pot3d_destroy(pot3d_ctx *ctx) {

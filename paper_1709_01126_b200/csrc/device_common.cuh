@@ -189,7 +189,6 @@ __device__ __forceinline__ bool xfer_wait(const unsigned long long *flag, unsign
 }
 
 // diagnostics (POT3D_TRACE): %globaltimer of an event of the current iteration
-enum TraceSlot { TR_EDGE0 = 0, TR_EDGE1, TR_A0, TR_AHALO, TR_A1, TR_F0, TR_F1, TR_B0, TR_B1, TR_EDGEM };
 __device__ __forceinline__ void trace_mark(Scalars *S, int slot) {
   if (S->trace) S->trace[(S->iter & 63) * 16 + slot] = global_ns();
 }

@@ -33,7 +33,8 @@ STATUS_NAMES = {0: "ok", 1: "not_converged", 2: "pc2_fell_back", -1: "invalid", 
 
 EXPORTS = ["pot3d_setup", "pot3d_set_br0", "pot3d_solve", "pot3d_field", "pot3d_apply",
            "pot3d_precond", "pot3d_history", "pot3d_info", "pot3d_profile",
-           "pot3d_profile_iteration", "pot3d_nccl_unique_id",
+           "pot3d_profile_iteration", "pot3d_trace_enable", "pot3d_kernel_times",
+           "pot3d_nccl_unique_id",
            "pot3d_destroy", "pot3d_last_error"]
 
 _ALLOC = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
@@ -102,6 +103,8 @@ def library(build_if_missing: bool = True):
     L.pot3d_info.argtypes = [vp, ctypes.POINTER(_Info)]
     L.pot3d_profile.argtypes = [vp, ctypes.c_int32, d, d, d]
     L.pot3d_profile_iteration.argtypes = [vp, ctypes.c_int32, d, ctypes.c_char_p, ctypes.c_int32]
+    L.pot3d_trace_enable.argtypes = [vp, ctypes.c_int32]
+    L.pot3d_kernel_times.argtypes = [vp, d, d, ctypes.POINTER(ctypes.c_int32)]
     L.pot3d_nccl_unique_id.argtypes = [vp]
     L.pot3d_destroy.argtypes = [vp]
     L.pot3d_last_error.argtypes = [vp]
@@ -300,6 +303,17 @@ class Pot3d:
         z = self._out((self.np, self.nt, self.nr_loc), out)
         self._check(self._L.pot3d_precond(self._ctx, pr, _ptr(z)[0]))
         return z
+
+    def trace(self, on=True):
+        """Record in-situ pass durations in the solve loop (see kernel_times)."""
+        self._check(self._L.pot3d_trace_enable(self._ctx, 1 if on else 0))
+
+    def kernel_times(self):
+        """Mean device microseconds of pass A and pass B over the last <= 64 loop
+        iterations of the last solve (first block start -> last block end)."""
+        a, b, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+        self._check(self._L.pot3d_kernel_times(self._ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
+        return a.value, b.value, n.value
 
     def history(self, n):
         h = np.empty(int(n), dtype=np.float64)
