@@ -279,3 +279,17 @@ def test_large_config_fixed_iterations():
     assert res.iters == 5
     scale = np.abs(ref["x"]).max()
     assert np.abs(res.phi - ref["x"]).max() <= 1e-9 * scale
+
+
+def test_kernel_times_live_trace():
+    """pot3d_trace_enable / pot3d_kernel_times: in-solve pass durations (bench roofline)."""
+    c = synth.CONFIGS["small"]
+    rf, tf, pf = c.faces()
+    with solver(rf, tf, pf, c.br0()) as s:
+        with pytest.raises(RuntimeError):
+            s.kernel_times()  # not enabled
+        s.trace(True)
+        res = s.solve(rtol=1e-9)
+        a, b, n = s.kernel_times()
+    assert n == min(64, res.iters)
+    assert 0.0 < a < 1e4 and 0.0 < b < 1e4
