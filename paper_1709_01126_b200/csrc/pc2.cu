@@ -88,7 +88,6 @@ struct SweepArgs {
 // (a signalling-NaN bit pattern arithmetic never produces) until the producer
 // stores the value; the single consumer prefetches the slot PD steps ahead with
 // ld.global.cv, polls only while it still reads the sentinel, and re-arms it.
-constexpr unsigned SENT32 = 0x7FF57FF5u;
 constexpr unsigned long long SENT = 0x7FF57FF57FF57FF5ull;
 #ifndef POT3D_SWEEP_D
 #define POT3D_SWEEP_D 8
@@ -132,14 +131,14 @@ __device__ __forceinline__ double poll_slot(const double *p, double v, int *flag
 #ifndef POT3D_SWEEP_MINB
 #define POT3D_SWEEP_MINB 1
 #endif
-template <int MODE>
-__global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
+// D-ILU factorisation (setup only): d_m = diag_m - sum_{N-} A_mn^2 / d_n as a
+// one-cell-per-thread wavefront over 8 x 32 tiles; writes 1/d.
+__global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_factor(SweepArgs A) {
   const Grid &G = A.G;
   const Metrics &M = A.M;
   if (A.predicated && A.S->stop) return;
   __shared__ double sw[2][WJ][WK];
   __shared__ int s_ticket;
-  __shared__ double sred[WT / 32];
   const int tid = threadIdx.x;
   const int jj = tid / WK, kk = tid % WK;
   if (tid == 0) s_ticket = atomicAdd(&A.sync[0], 1);
@@ -150,12 +149,11 @@ __global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
   const int2 tl = A.order[pos];  // virtual tile (tj, tk)
   const int l0 = A.l0[b], l1 = A.l0[b + 1];
   const int nb = l1 - l0;
-  const bool rev = (MODE == SW_BWD);
-  // virtual coordinates (dependencies on iv-1, jv-1, kv-1); real = mirrored for BWD
+  // dependencies on i-1, j-1, k-1 (the factor runs in natural order)
   const int jv = tl.x * WJ + jj, kv = tl.y * WK + kk;
   const bool valid = (jv < G.nt) && (kv < G.np);
-  const int j = rev ? G.nt - 1 - jv : jv;
-  const int k = rev ? G.np - 1 - kv : kv;
+  const int j = jv;
+  const int k = kv;
   const int jc = valid ? j : 0, kc = valid ? k : 0;
   const int nsteps = nb + WJ + WK - 2;
   // edge buffers of this tile (producer) and of its up / left neighbours (consumer)
@@ -176,39 +174,29 @@ __global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
   const double g = __ldg(M.g + jc), q = __ldg(M.q + jc);
   const double atp = __ldg(M.atp + jc), atm = __ldg(M.atm + jc);
   const double dpk = __ldg(M.dp + kc), app = __ldg(M.app + kc), apm = __ldg(M.apm + kc);
-  // couplings to the virtual predecessors (zero across the pole / the dropped wrap)
-  const double ct = rev ? atp : atm;                                              // x dr_i dp_k
-  const double cp = rev ? ((k < G.np - 1) ? app : 0.0) : ((k > 0) ? apm : 0.0);  // x dr_i q_j
-  const long long o_base = cidx(G, rev ? l1 - 1 : l0, jc, kc);
-  const long long o_step = rev ? -G.plane : G.plane;  // one virtual shell
-  const int ig_base = G.i0 + (rev ? l1 - 1 : l0), ig_step = rev ? -1 : 1;
+  // couplings to the predecessors (zero across the pole / the dropped wrap)
+  const double ct = atm;                         // x dr_i dp_k
+  const double cp = (k > 0) ? apm : 0.0;         // x dr_i q_j
+  const long long o_base = cidx(G, l0, jc, kc);
+  const long long o_step = G.plane;
+  const int ig_base = G.i0 + l0;
 
-  // prefetch ring: operands of the cell this thread handles at step t+PD
-  double ra[PD], rb[PD], rc[PD], rnj[PD], rnk[PD];
-  auto fetch = [&](int ts, double &xa, double &xb, double &xc, double &xj, double &xk) {
+  // prefetch ring of the neighbour-tile values this thread needs PD steps ahead
+  double rnj[PD], rnk[PD];
+  auto fetch = [&](int ts, double &xj, double &xk) {
     const int iv = ts - jj - kk;
-    xa = xb = xc = 0.0;
     xj = xk = 0.0;
     if (valid && iv >= 0 && iv < nb) {
-      const long long o = o_base + (long long)iv * o_step;
-      if (MODE == SW_FWD) {
-        xa = __ldg(A.r + o);
-        xb = __ldg(A.inv_d + o);
-      } else if (MODE == SW_BWD) {
-        xa = __ldcg(A.z + o);   // w of this cell (forward sweep output)
-        xb = __ldg(A.inv_d + o);
-        xc = __ldg(A.r + o);    // r of this cell for the r.z partial
-      }
-      // neighbour-tile values: prefetched, re-polled at use if still the sentinel
+      // re-polled at use while still the sentinel
       if (need_j) xj = ld_poll(up_bot + iv);
       if (need_k) xk = ld_poll(lf_rgt + iv);
     }
   };
   bool proto = false;
 #pragma unroll
-  for (int u = 0; u < PD; u++) fetch(u, ra[u], rb[u], rc[u], rnj[u], rnk[u]);
+  for (int u = 0; u < PD; u++) fetch(u, rnj[u], rnk[u]);
 
-  double wprev = 0.0, acc = 0.0;
+  double wprev = 0.0;
   bool bad = false;
   for (int t0 = 0; t0 < nsteps; t0 += PD) {
 #pragma unroll
@@ -216,9 +204,8 @@ __global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
       const int t = t0 + u;
       if (t >= nsteps) break;
       __syncthreads();  // step t-1 complete in this CTA (shared double buffer)
-      const double a0 = ra[u], b0 = rb[u], c0 = rc[u];
       double nj = rnj[u], nk = rnk[u];
-      fetch(t + PD, ra[u], rb[u], rc[u], rnj[u], rnk[u]);
+      fetch(t + PD, rnj[u], rnk[u]);
       const int ivt = t - jj - kk;  // virtual local shell of this thread at step t
       if (valid && ivt >= 0 && ivt < nb) {
         if (need_j) {  // value of the tile above (virtual), produced at its step t+WJ-1
@@ -230,31 +217,21 @@ __global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
           __stcg(reinterpret_cast<unsigned long long *>(lf_rgt + ivt), SENT);
         }
         const long long o = o_base + (long long)ivt * o_step;
-        const int ig = ig_base + ivt * ig_step;
+        const int ig = ig_base + ivt;
         const double dr = __ldg(M.dr + ig);
         const double vi = (ivt > 0) ? wprev : 0.0;
         const double vj = (jj > 0) ? sw[(t - 1) & 1][jj - 1][kk] : (need_j ? nj : 0.0);
         const double vk = (kk > 0) ? sw[(t - 1) & 1][jj][kk - 1] : (need_k ? nk : 0.0);
-        const double cr = (ivt > 0) ? (rev ? __ldg(M.arp + ig) : __ldg(M.arm + ig)) : 0.0;
+        const double cr = (ivt > 0) ? __ldg(M.arm + ig) : 0.0;
         const double Ar = cr * g * dpk, At = dr * ct * dpk, Ap = dr * q * cp;
-        double val;
-        if (MODE == SW_FACTOR) {
-          const double diag = dpk * (g * (__ldg(M.arp + ig) + __ldg(M.arm + ig) + __ldg(M.ss + ig)) +
-                                     dr * (atp + atm)) + dr * q * (app + apm);
-          // the wrap coupling and the inter-block couplings are dropped from L/U,
-          // the full diagonal is kept (A11)
-          const double d = diag - Ar * Ar * vi - At * At * vj - Ap * Ap * vk;
-          bad |= !(d > 1e-300);
-          val = 1.0 / d;
-          A.inv_d[o] = val;
-        } else if (MODE == SW_FWD) {
-          val = (a0 + Ar * vi + At * vj + Ap * vk) * b0;
-          A.z[o] = val;
-        } else {
-          val = a0 + b0 * (Ar * vi + At * vj + Ap * vk);
-          A.z[o] = val;
-          acc += c0 * val;
-        }
+        const double diag = dpk * (g * (__ldg(M.arp + ig) + __ldg(M.arm + ig) + __ldg(M.ss + ig)) +
+                                   dr * (atp + atm)) + dr * q * (app + apm);
+        // the wrap coupling and the inter-block couplings are dropped from L/U,
+        // the full diagonal is kept (A11); vi, vj, vk hold 1/d of the predecessors
+        const double d = diag - Ar * Ar * vi - At * At * vj - Ap * Ap * vk;
+        bad |= !(d > 1e-300);
+        const double val = 1.0 / d;
+        A.inv_d[o] = val;
         if (put_bot) __stcg(my_bot + ivt, val);
         if (put_rgt) __stcg(my_rgt + ivt, val);
         wprev = val;
@@ -263,26 +240,12 @@ __global__ void __launch_bounds__(WT, POT3D_SWEEP_MINB) k_sweep(SweepArgs A) {
     }
   }
   if (__syncthreads_or(proto) && tid == 0) atomicOr(&A.sync[1], 2);  // protocol error
-  if (MODE == SW_FACTOR) {
-    if (__syncthreads_or(bad) && tid == 0) atomicOr(&A.sync[1], 1);
-  }
-  if (MODE == SW_BWD) {
-    double v[1] = {acc}, tot[1];
-    // partials indexed by ticket (tile identity), not blockIdx: a fixed summation order
-    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket) && tid == 0) {
-      if (A.finalize)
-        finalize_rho(A.S, tot[0]);
-      else if (A.peers)
-        mail_post(A.peers, MAIL_C, tot[0], 0.0, mail_seq(A.S->epoch, A.S->iter));
-      else
-        A.local_sum[0] = tot[0];
-    }
-  }
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(&A.sync[1], 1);      // pivot breakdown
 }
 
 // ---------------------------------------------------------------------------
 // Run-vectorised forward / backward sweeps.  Same wavefront and handoff
-// protocol as k_sweep, but a thread owns SV = 4 phi-consecutive cells of one
+// protocol as k_factor, but a thread owns SV = 4 phi-consecutive cells of one
 // row (a "run", one 32-B sector per array) instead of one cell: step t of
 // thread (jj, m) handles shell t - jj - m of run m, so the lanes of a warp read
 // and write whole sectors (the one-cell mapping used a quarter of every sector
@@ -687,7 +650,7 @@ static SweepArgs sweep_args(Pc2 *P, const Metrics &M, Scalars *S, const double *
 int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host) {
   cudaMemsetAsync(P->d_sync, 0, sizeof(int) * P->nsync, s);
   SweepArgs a = sweep_args(P, M, nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr);
-  k_sweep<SW_FACTOR><<<P->nblk * P->ntiles, WT, 0, s>>>(a);
+  k_factor<<<P->nblk * P->ntiles, WT, 0, s>>>(a);
   if (cudaGetLastError() != cudaSuccess) return -1;
   int flags[2];
   cudaMemcpyAsync(flags, P->d_sync, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
