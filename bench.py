@@ -340,7 +340,8 @@ def main():
     line = {
         "metric": "fp64 PCG iters/s", "value": value, "unit": "iters/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if args.config == "weak" else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {
             "workload": workload_desc(c, args),
