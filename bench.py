@@ -176,7 +176,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "fp64 PCG iters/s", "value": value, "unit": "iters/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
+        "scaling": "weak" if args.config == "weak" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_desc(c, args),
                    "step": f"{iters} oracle PCG iterations (bounded sample)"},
