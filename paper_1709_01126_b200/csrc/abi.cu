@@ -622,10 +622,11 @@ int build_graph(pot3d_ctx *ctx) {
 // large 75-100 / 27-38, weak 69 / 35 shells -> Lcap 100 for A and 32 for B.
 int pick_chunks(const Grid &G, double slots, int Lcap) {
   const int cmin = std::max(1, (G.nr_loc + Lcap - 1) / Lcap);
-  // thin slabs (multi-GPU r-slabs of <= 24 shells): the two halo planes of a chunk
-  // cost more than idle slots -- one chunk (measured on 19 shells: 57.8 us per
-  // iteration with 1 chunk per pass vs 66.0 us with 4, tools/lat.py)
-  if (G.nr_loc <= 24) return cmin;
+  // thin slabs (multi-GPU r-slabs of <= 24 shells) whose tiles alone already cover
+  // every SM: the two halo planes of a chunk cost more than idle slots -- one chunk
+  // (19 x 301 x 601: 57.8 us per iteration with 1 chunk per pass vs 66.0 us with 4,
+  // tools/lat.py); small grids with few tiles still need the chunks for parallelism
+  if (G.nr_loc <= 24 && (double)G.ntj * G.ntk >= slots / 2) return cmin;
   const long long tiles = (long long)G.ntj * G.ntk;
   double best = -1;
   int bestc = cmin;
