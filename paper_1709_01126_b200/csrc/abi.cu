@@ -29,6 +29,7 @@ struct pot3d_ctx {
   int nchunks_b = 1;  // r-chunks of pass B (G.nchunks: pass A)
   bool pdl = true;    // programmatic dependent launch for the loop kernels (POT3D_PDL=0: off)
   int edge_blocks = 148 * 4;  // grid of the edge-shell kernel (POT3D_EDGE_BLOCKS)
+  bool edge_in_a = true;      // pass A's first block row builds the edge shells (POT3D_EDGE_IN_A=0: kernel)
   int device = 0;
   double r0 = 1.0;
   Grid G{};
@@ -470,6 +471,29 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     // chunk touches a ghost shell (scheduled last); the rank sums go straight into
     // every rank's mailbox from the reductions' last blocks
     const PeerTab *pt = ctx->peers;
+    if (ctx->edge_in_a && !pc2) {
+      // pass A's first block row builds and sends the edge shells beside the interior
+      // chunks; beta is finalised by its own kernel after pass B
+      PassArgs ax = a;
+      ax.G.part = 3;
+      ax.G.role_rows = 1;
+      ax.peers = pt;
+      CK(launch_k(ctx->pdl, kern_a(ctx), dim3(G.ntj * G.ntk, G.nchunks + 1), dim3(NTHREADS), SMEM_A,
+                  ctx->stream, ctx->tmaps, ax, parity));
+      MARK("passA");
+      CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_A, 0,
+                  (double *)nullptr));
+      MARK("finalize_alpha");
+      PassArgs bx = ab;
+      bx.peers = pt;
+      CK(launch_k(ctx->pdl, kern_b(ctx), grdb, dim3(NTHREADS), SMEM_B, ctx->stream, ctx->tmaps, bx, parity));
+      MARK("passB");
+      CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_B, 1,
+                  ctx->hist));
+      MARK("finalize_beta");
+      ctx->n_enq += 4;
+      return 0;
+    }
     // PC1: the previous iteration's beta finalisation lives in edge_p (fold)
     const int fold = pc2 ? 0 : 1;
     CK(launch_k(ctx->pdl, k_edge_p, dim3(ctx->edge_blocks), dim3(256), 0, ctx->stream, G, ctx->M, ctx->S,
@@ -805,6 +829,8 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
     ctx->pdl = !(e && atoi(e) == 0);
     const char *eb = getenv("POT3D_EDGE_BLOCKS");
     if (eb && atoi(eb) > 0) ctx->edge_blocks = atoi(eb);
+    const char *ea = getenv("POT3D_EDGE_IN_A");
+    ctx->edge_in_a = !(ea && atoi(ea) == 0);
   }
   pot3d_runtime R{};
   R.nranks = 1;
@@ -923,7 +949,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   DA(ctx->bshell, G.plane + 16); DA(ctx->br_dev, G.plane + 16); DA(ctx->mean2, 2);
   DA(ctx->S, 1);
   ctx->partials_len = 4 * (size_t)std::max<long long>(
-      (long long)G.ntj * G.ntk * (std::max(G.nchunks, ctx->nchunks_b) + 2), 65536);
+      (long long)G.ntj * G.ntk * (std::max(G.nchunks, ctx->nchunks_b) + 3), 65536);
   DA(ctx->partials, ctx->partials_len);
   DA(ctx->local_sum, 2);
   DA(ctx->gathered, 2 * (size_t)ctx->nranks + 2);

@@ -347,4 +347,70 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// The two edge shells of p_k = z + beta p_{k-1} by aligned column pairs (physical
+// 2m, 2m+1 = logical k = 2m-1, 2m; 16-B loads and stores), stored locally and into
+// the neighbours' ghost shells (peer memory, same [il+1][j][c] layout shifted by
+// whole planes); the ghost columns (k = -1, np) are computed like cells from their
+// duplicated inputs, exactly as pass A does.  Block-wide call over blocks
+// bid = 0 .. nblocks-1; returns true in the block that completed last (after every
+// block's stores were released system-wide), which then raises the halo flags.
+__device__ __forceinline__ bool edge_shells(const Grid &G, const Metrics &M, Scalars *S,
+                                            const double *src, const double *p_old, double *p_new,
+                                            bool use_z, const PeerTab *peers, int parity_new,
+                                            double beta, int bid, int nblocks, bool work = true) {
+  // peers == nullptr (NCCL exchange): local stores only, the caller sends the shells
+  double *lo = peers ? peers->p_lo[parity_new] : nullptr, *hi = peers ? peers->p_hi[parity_new] : nullptr;
+  if (lo) lo += (long long)peers->nr_lo * G.plane;
+  if (hi) hi -= (long long)G.nr_loc * G.plane;
+  const int npair = (G.np + 2 + 1) / 2;  // pairs covering physical columns 0 .. np+1
+  const long long rows = (long long)G.nt * npair;
+  const long long npairs = work ? 2 * rows : 0;
+  for (long long c = bid * (long long)blockDim.x + threadIdx.x; c < npairs;
+       c += (long long)nblocks * blockDim.x) {
+    const int sidx = (int)(c / rows);
+    const long long t = c - sidx * rows;
+    const int j = (int)(t / npair), m = (int)(t - (long long)j * npair);
+    const int il = sidx == 0 ? 0 : G.nr_loc - 1;
+    const long long o = (long long)(il + 1) * G.plane + (long long)j * G.PK + 2 * m;  // physical 2m
+    const PlaneC P = plane_c(M, G.i0 + il);
+    const RowC R = row_c(M, j);
+    const DiagRow d = diag_row(P, R);
+    const double2 sv = *reinterpret_cast<const double2 *>(src + o);
+    const double2 pv = *reinterpret_cast<const double2 *>(p_old + o);
+    double v[2];
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      int k = 2 * m - 1 + e;  // logical column, wrapped for the ghost copies
+      k = (k < 0) ? k + G.np : (k >= G.np ? k - G.np : k);
+      const double s = e ? sv.y : sv.x, p = e ? pv.y : pv.x;
+      const double zv = use_z ? s : jacobi(s, diag_at(__ldg(M.dp + k), d, __ldg(M.app + k), __ldg(M.apm + k)));
+      v[e] = fma(beta, p, zv);  // the same arithmetic as pass A
+    }
+    const bool both = 2 * m + 1 <= G.np + 1;  // physical 2m+1 still a ghost or a cell
+    double *rem = sidx == 0 ? lo : hi;
+    if (both) {
+      *reinterpret_cast<double2 *>(p_new + o) = make_double2(v[0], v[1]);
+      if (rem) *reinterpret_cast<double2 *>(rem + o) = make_double2(v[0], v[1]);
+    } else {
+      p_new[o] = v[0];
+      if (rem) rem[o] = v[0];
+    }
+  }
+  if (!peers) return false;
+  __shared__ bool s_edge_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // this block's peer stores, before the count
+    s_edge_last = atomicAdd(&S->counter[4], 1u) == (unsigned)nblocks - 1;
+  }
+  __syncthreads();
+  return s_edge_last;
+}
+// neighbours' halo flags for seq (caller: the last block of edge_shells, one thread)
+__device__ __forceinline__ void raise_halo_flags(const PeerTab *peers, unsigned long long seq) {
+  __threadfence_system();  // + relaxed stores = release of every block's ghost stores
+  if (peers->rank > 0) st_relaxed_sys(&peers->mail[peers->rank - 1]->halo[1], seq);
+  if (peers->rank < peers->nranks - 1) st_relaxed_sys(&peers->mail[peers->rank + 1]->halo[0], seq);
+}
+
 }  // namespace pot3d

@@ -194,45 +194,10 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
     if (lo) lo += (long long)peers->nr_lo * G.plane;
     if (hi) hi -= (long long)G.nr_loc * G.plane;
   }
-  if (mode >= 0) {
-    // the two edge shells by aligned column pairs (physical 2m, 2m+1 = logical k = 2m-1, 2m):
-    // 16-B loads and stores, local and remote; the ghost columns (k = -1, k = np) are
-    // computed like cells from their duplicated inputs, exactly as pass A does
-    const int npair = (G.np + 2 + 1) / 2;  // pairs covering physical columns 0 .. np+1
-    const long long rows = (long long)G.nt * npair;
-    const long long npairs = s_stop ? 0 : 2 * rows;
-    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < npairs;
-         c += (long long)gridDim.x * blockDim.x) {
-      const int sidx = (int)(c / rows);
-      const long long t = c - sidx * rows;
-      const int j = (int)(t / npair), m = (int)(t - (long long)j * npair);
-      const int il = sidx == 0 ? 0 : G.nr_loc - 1;
-      const long long o = (long long)(il + 1) * G.plane + (long long)j * G.PK + 2 * m;  // physical 2m
-      const PlaneC P = plane_c(M, G.i0 + il);
-      const RowC R = row_c(M, j);
-      const DiagRow d = diag_row(P, R);
-      const double2 sv = *reinterpret_cast<const double2 *>(src + o);
-      const double2 pv = *reinterpret_cast<const double2 *>(p_old + o);
-      double v[2];
-#pragma unroll
-      for (int e = 0; e < 2; e++) {
-        int k = 2 * m - 1 + e;  // logical column, wrapped for the ghost copies
-        k = (k < 0) ? k + G.np : (k >= G.np ? k - G.np : k);
-        const double s = e ? sv.y : sv.x, p = e ? pv.y : pv.x;
-        const double zv = (mode == 1) ? s : jacobi(s, diag_at(__ldg(M.dp + k), d, __ldg(M.app + k), __ldg(M.apm + k)));
-        v[e] = fma(beta, p, zv);
-      }
-      const bool both = 2 * m + 1 <= G.np + 1;  // physical 2m+1 still a ghost or a cell
-      double *rem = sidx == 0 ? lo : hi;
-      if (both) {
-        *reinterpret_cast<double2 *>(p_new + o) = make_double2(v[0], v[1]);
-        if (rem) *reinterpret_cast<double2 *>(rem + o) = make_double2(v[0], v[1]);
-      } else {
-        p_new[o] = v[0];
-        if (rem) rem[o] = v[0];
-      }
-    }
-  }
+  bool last_edge = false;  // every block counts in, also when the loop stops here
+  if (mode >= 0)
+    last_edge = edge_shells(G, M, S, src, p_old, p_new, mode == 1, peers, parity_new, beta, blockIdx.x,
+                            gridDim.x, !s_stop);
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < (mode < 0 ? n : 0);
        c += (long long)gridDim.x * blockDim.x) {
     long long t = c % per;
@@ -262,15 +227,7 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
     }
   }
   if (peers && mode >= 0) {
-    // all blocks' peer stores are released before the neighbours' flags
-    __shared__ bool s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      s_last = atomicAdd(&S->counter[4], 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x == 0) {
+    if (last_edge && threadIdx.x == 0) {
       S->counter[4] = 0u;
       if (S->trace) S->trace[(iter & 63) * 16 + TR_EDGE1] = global_ns();  // iteration of p_k
       if (pend) {  // finalize_beta of the previous iteration
@@ -292,12 +249,7 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
           }
         }
       }
-      if (!s_stop) {
-        __threadfence_system();  // + relaxed stores = release of every block's ghost stores
-        const unsigned long long seq = mail_seq(S->epoch, iter + 1);
-        if (peers->rank > 0) st_relaxed_sys(&peers->mail[peers->rank - 1]->halo[1], seq);
-        if (peers->rank < peers->nranks - 1) st_relaxed_sys(&peers->mail[peers->rank + 1]->halo[0], seq);
-      }
+      if (!s_stop) raise_halo_flags(peers, mail_seq(S->epoch, iter + 1));
     }
   }
 }

@@ -142,7 +142,7 @@ __device__ __forceinline__ TileThread tile_thread(const Grid &G) {
   t.k0 = (tile / G.ntj) * TK;
   // part 3: all shells, the two chunks touching a ghost shell scheduled last (their
   // blocks wait for the neighbours' halo, which meanwhile arrives in peer memory)
-  int cy = blockIdx.y;
+  int cy = blockIdx.y - G.role_rows;
   if (G.part == 3 && G.nchunks >= 3)
     cy = (cy < G.nchunks - 2) ? cy + 1 : (cy == G.nchunks - 2 ? 0 : G.nchunks - 1);
   chunk_bounds(G, cy, t.c0, t.c1);
@@ -203,6 +203,27 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   const Grid &G = A.G;
   const Metrics &M = A.M;
   Scalars *S = A.S;
+  if (G.role_rows && blockIdx.y == 0) {
+    // edge role (peer memory): p_k on the two edge shells, locally and into the
+    // neighbours' ghost shells, then the halo flags -- scheduled first, beside the
+    // interior chunks; these blocks add nothing to sigma
+    __shared__ double sred_e[NTHREADS / 32];
+    pdl_trigger();
+    pdl_wait();
+    if (S->stop) return;
+    const bool last = edge_shells(G, M, S, USE_Z ? A.z : A.r, A.p_old, A.p_new, USE_Z, A.peers, parity ^ 1,
+                                  S->beta, blockIdx.x, gridDim.x);
+    if (last && threadIdx.x == 0) {
+      S->counter[4] = 0u;
+      raise_halo_flags(A.peers, mail_seq(S->epoch, S->iter + 1));
+    }
+    double v[1] = {0.0}, tot[1];
+    if (grid_sum<1>(v, A.partials, &S->counter[0], sred_e, tot, pass_bid(G), pass_nb(G)) && threadIdx.x == 0) {
+      trace_mark(S, TR_A1);
+      mail_post(A.peers, MAIL_A, tot[0], 0.0, mail_seq(S->epoch, S->iter + 1));
+    }
+    return;
+  }
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemA &sm = *reinterpret_cast<SmemA *>(smem_raw);
   __shared__ double sred[NTHREADS / 32];

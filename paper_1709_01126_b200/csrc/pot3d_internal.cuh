@@ -130,6 +130,8 @@ struct Grid {
   //   as part 0 with the two chunks next to the ghost shells scheduled last.
   int part;
   int blk_off, blk_total;  // this launch's blocks within a reduction spanning launches
+  int role_rows;           // pass A, peer memory: the first block row builds the edge shells
+                           // of p_k and sends them to the neighbours (no edge-shell kernel)
 };
 
 // Physical column of logical phi index k is k + COFF: physical 0 is the
