@@ -39,7 +39,10 @@ namespace pot3d {
 #endif
 constexpr int TK = 62;          // interior phi columns per tile: lane l owns logical
                                 // columns k0-1+2l, k0+2l (lanes 0/31 hold the halo columns)
-constexpr int TJ = 14;          // interior theta rows per tile
+#ifndef POT3D_TJ
+#define POT3D_TJ 14
+#endif
+constexpr int TJ = POT3D_TJ;    // interior theta rows per tile
 constexpr int TR = TJ + 2;      // haloed rows
 // chunks of the fused passes stage their r-metric factors for at most
 // POT3D_PLMAX planes (chunk length + 2) in shared memory
