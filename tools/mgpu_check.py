@@ -23,8 +23,11 @@ fails = 0
 cases = [("tiny", 1, 1, synth.SOURCE_SURFACE), ("small", 1, 1, synth.SOURCE_SURFACE),
          ("small", 1, 1, synth.CLOSED_WALL), ("small", 2, 1, synth.SOURCE_SURFACE),
          ("small", 2, 2, synth.SOURCE_SURFACE), ("small", 2, 1, synth.CLOSED_WALL)]
+# the thinnest legal slabs: 2 shells per rank
+cases.append(("thin", 1, 1, synth.SOURCE_SURFACE))
+cases.append(("thin", 2, 1, synth.SOURCE_SURFACE))
 for name, pc, blocks, bc in cases:
-    c = synth.CONFIGS[name]
+    c = synth.Config("thin", 2 * world, 17, 33, lmax=4) if name == "thin" else synth.CONFIGS[name]
     rf, tf, pf = c.faces()
     br = c.br0()
     t0 = time.time()
