@@ -26,6 +26,10 @@
 
 // pass A code-generation switches (tuning variants)
 
+#ifndef POT3D_A_FLUX   // pass A shares the r flux between consecutive stencil planes
+#define POT3D_A_FLUX 1
+#endif
+
 namespace pot3d {
 
 static_assert(NS_A == 3, "pass A is unrolled by its stage count");
@@ -119,6 +123,17 @@ __device__ __forceinline__ double stencil7(double c, double ip, double im, doubl
                                            double apmk, const PlaneC &P, const RowC &R) {
   return dpk * (R.g * (P.arp * (c - ip) + P.arm * (c - im) + P.ss * c) +
                 P.dr * (R.atp * (c - jp) + R.atm * (c - jm))) +
+         P.dr * R.q * (appk * (c - kp) + apmk * (c - km));
+}
+
+// stencil7 with the r flux shared between consecutive planes: Fu = arp (c - ip) is
+// returned for the next plane, whose lower term arm (c - im) is exactly -Fu
+// (arm_{i+1} == arp_i bitwise, a - b == -(b - a) exactly); Fd = arm (c - im).
+__device__ __forceinline__ double stencil7f(double c, double ip, double Fd, double jp, double jm,
+                                            double kp, double km, double dpk, double appk,
+                                            double apmk, const PlaneC &P, const RowC &R, double &Fu) {
+  Fu = P.arp * (c - ip);
+  return dpk * (R.g * (Fu + Fd + P.ss * c) + P.dr * (R.atp * (c - jp) + R.atm * (c - jm))) +
          P.dr * R.q * (appk * (c - kp) + apmk * (c - km));
 }
 
@@ -319,9 +334,14 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   // One plane step.  STENCIL = false only for q = 0, 1 (peeled), so the steady
   // state is one basic block: the transform's fp64 chains (plane q) and the
   // stencil of plane q-1 are independent and can be interleaved by the scheduler.
-  auto step = [&](auto U, auto STENCIL, int q) {
+#if POT3D_A_FLUX
+  double2 fl[RPW];  // upper r flux arp (c - ip) of the last stencil plane, per row and cell
+#endif
+  auto step = [&](auto U, auto STENCIL, int q, auto FIRST) {
     constexpr int u = decltype(U)::value;       // stage, slot and register set of plane q
     constexpr bool do_st = decltype(STENCIL)::value;
+    constexpr bool first = decltype(FIRST)::value;  // first stencil plane of the chunk
+    (void)first;
     constexpr int um = (u + 2) % 3, umm = (u + 1) % 3;
     __syncthreads();  // stage um and slot u are free
     if (threadIdx.x == 0) issue(q + 2, um);
@@ -367,25 +387,35 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
         const double2 up = (RPW == 2 && e == 1) ? R[um][0] : *reinterpret_cast<const double2 *>(so + up_off[e]);
         const double2 dn = (RPW == 2 && e == 0) ? R[um][RPW - 1] : *reinterpret_cast<const double2 *>(so + dn_off[e]);
         const double lf = so[-1], rt = so[2];
+#if POT3D_A_FLUX
+        // lower r flux: computed on the chunk's first stencil plane, then the negated
+        // upper flux of the previous plane
+        const double fdx = first ? Ps.arm * (c.x - R[umm][e].x) : -fl[e].x;
+        const double fdy = first ? Ps.arm * (c.y - R[umm][e].y) : -fl[e].y;
+        const double q0 = stencil7f(c.x, R[u][e].x, fdx, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e], fl[e].x);
+        const double q1 = stencil7f(c.y, R[u][e].y, fdy, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e], fl[e].y);
+#else
         const double q0 = stencil7(c.x, R[u][e].x, R[umm][e].x, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e]);
         const double q1 = stencil7(c.y, R[u][e].y, R[umm][e].y, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e]);
+#endif
         acc += (m0[e] ? c.x * q0 : 0.0) + (m1[e] ? c.y * q1 : 0.0);
       }
     }
   };
 
   const int last = L + 1;  // >= 2
-  step(IC<0>{}, std::false_type{}, 0);
-  step(IC<1>{}, std::false_type{}, 1);
+  step(IC<0>{}, std::false_type{}, 0, std::false_type{});
+  step(IC<1>{}, std::false_type{}, 1, std::false_type{});
+  step(IC<2>{}, std::true_type{}, 2, std::true_type{});
+  ph ^= 1u;
 #pragma unroll 1
-  for (int q = 2;; q += 3) {
-    step(IC<2>{}, std::true_type{}, q);
-    ph ^= 1u;
+  for (int q = 3; q <= last; q += 3) {
+    step(IC<0>{}, std::true_type{}, q, std::false_type{});
     if (q + 1 > last) break;
-    step(IC<0>{}, std::true_type{}, q + 1);
+    step(IC<1>{}, std::true_type{}, q + 1, std::false_type{});
     if (q + 2 > last) break;
-    step(IC<1>{}, std::true_type{}, q + 2);
-    if (q + 3 > last) break;
+    step(IC<2>{}, std::true_type{}, q + 2, std::false_type{});
+    ph ^= 1u;
   }
 
   double v[1] = {acc}, tot[1];
