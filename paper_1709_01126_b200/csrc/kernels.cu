@@ -1,25 +1,21 @@
-// kernels.cu -- sm_100a kernels of the fp64 PCG hot path.
+// kernels.cu -- the sm_100a kernels around the two fused passes;
+// the passes themselves are in passes.cu, the PC2 sweeps in pc2.cu.
 //
-//   k_metrics        a1  1-D metric factors from the faces (A1-A7)
-//   k_rhs            a2  b on the photosphere shell (Eq.2)
-//   k_pass_a         a3  p = z + beta p_old (z = D^-1 r on the fly, PC1 P:88),
-//                        q = A p, partial p.q, lazy x += alpha_prev p_old
-//   k_pass_b         a7  q = A p (recomputed), r -= alpha q, z = D^-1 r,
-//                        partials r.z and r.r
-//   k_init_dots      a10 rho_0 = b.D^-1 b, ||b||
-//   finalize_*       a6/a10 deterministic second-level reduction, alpha, beta,
-//                        convergence test, on the device
-//   k_apply          unfused 7-point apply (diagnostics, true residual)
-//   k_finish         a11 x += alpha_last p_last
-//   k_field_*        a11 B = grad Phi on staggered faces (A16)
-//   k_transpose      user layout (r fastest) <-> device layout (phi fastest)
-//
-// The two fused passes march along r through a theta x phi tile (2.5-D
-// blocking): each thread owns two phi-adjacent cells
-// (one 128-bit fp64 load per array), the current plane of p is staged in a
-// 3-slot shared-memory ring for the theta/phi neighbours, the r neighbours
-// stay in registers, and the next plane is prefetched into registers while
-// the stencil of the current plane runs.
+//   k_metrics         a1  1-D metric factors from the faces (A1-A7)
+//   k_br_mean, k_rhs  a2  closed-wall mean removal (A8); b on the photosphere shell
+//                         (Eq.2)
+//   k_init_dots       a10 rho_0 = b.M^-1 b and ||b|| (deterministic grid reduction)
+//   k_edge_p          a5  p_k on the two edge shells (NCCL path, PC2, or
+//                         POT3D_EDGE_IN_A=0), stored locally and -- peer memory --
+//                         into the neighbours' ghost shells; can finalise the
+//                         previous pass B's beta from the mailbox (fold)
+//   k_finalize_*      a6  multi-rank scalar updates: rank-order sums of the NCCL
+//                         all-gather (k_finalize_alpha/beta/rr/rho, k_init_finalize)
+//                         or of the peer mailbox (k_finalize_mail)
+//   k_apply           unfused 7-point apply (diagnostics, true residual)
+//   k_gauge_*         closed-wall zero volume-weighted-mean gauge
+//   k_pole_avg, k_field_r/t/p   a11 Eq.3 pole rings, B = grad Phi on staggered faces (A16)
+//   k_transpose       user layout (r fastest) <-> device layout (phi fastest)
 #include "device_common.cuh"
 
 namespace pot3d {
