@@ -418,18 +418,6 @@ __global__ void k_rhs(Grid G, Metrics M, double r0, const double *br, const doub
   bshell[o] = -r0 * r0 * __ldg(M.g + j) * __ldg(M.dp + k) * (br[o] - mean);
 }
 
-// ---------------------------------------------------------------------------
-// a11 finish: x += alpha_prev * p_last over owned cells (vectorised rows).
-// ---------------------------------------------------------------------------
-__global__ void k_axpy_cells(Grid G, double *x, const double *p, const Scalars *S) {
-  const double a = S->alpha_prev;
-  const long long n = (long long)G.nr_loc * G.plane;
-  double *xo = x + G.plane;
-  const double *po = p + G.plane;
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
-       c += (long long)gridDim.x * blockDim.x)
-    xo[c] += a * po[c];
-}
 
 // Closed-wall gauge: sums of V x and V over this rank (V = vr_i g_j dp_k).
 __global__ void k_gauge_sums(Grid G, Metrics M, const double *vr, const double *x, Scalars *S,

@@ -220,7 +220,6 @@ __global__ void k_apply(Grid G, Metrics M, const double *x, double *y, const dou
 __global__ void k_br_mean(Grid G, Metrics M, const double *br, double *out2);
 __global__ void k_rhs(Grid G, Metrics M, double r0, const double *br, const double *mean2,
                       double *bshell);
-__global__ void k_axpy_cells(Grid G, double *x, const double *p, const Scalars *S);
 __global__ void k_gauge_sums(Grid G, Metrics M, const double *vr, const double *x, Scalars *S,
                              double *partials, double *local_sum);
 __global__ void k_gauge_shift(Grid G, double *x, const double *gathered, int nranks);
