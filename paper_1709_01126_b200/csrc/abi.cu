@@ -433,10 +433,12 @@ PassKernel kern_b(const pot3d_ctx *ctx) {
 }
 
 // One PCG iteration (a3-a10) enqueued on ctx->stream; parity = iteration & 1.
-//   [multi-rank] edge shells of p_new -> NCCL halo
-//   pass A  (p_new, q = A p_new, sigma partial, lazy x update) -> alpha
-//   pass B  (r -= alpha q, PC1: rho', ||r||^2)                 -> convergence, beta
-//   [PC2]   forward + backward D-ILU sweeps (z, rho')           -> beta
+//   pass A  (p_new = z + beta p_old, q = A p_new, sigma partial)      -> alpha
+//   pass B  (q again, r -= alpha q, x += alpha p_new; PC1: rho', ||r||^2) -> convergence, beta
+//   [PC2]   forward + backward D-ILU sweeps (z, rho')                 -> beta
+//   [N > 1] edge shells of p_new to the neighbours (peer memory: pass A's first block
+//           row or k_edge_p; NCCL: k_edge_p + send/recv) and rank sums through the
+//           mailboxes (or an NCCL all-gather) before each finalisation
 // optional timing hook: records an event on the main stream after each sub-step
 struct StepTimer {
   std::vector<cudaEvent_t> ev;
