@@ -293,3 +293,26 @@ def test_kernel_times_live_trace():
         a, b, n = s.kernel_times()
     assert n == min(64, res.iters)
     assert 0.0 < a < 1e4 and 0.0 < b < 1e4
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_grids_apply_precond_parity(seed):
+    """Seeded random ragged grids (tile remainders in theta and phi, 2-shell slabs,
+    odd phi counts): operator, PC1 and PC2 applies against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    dims = (int(rng.integers(2, 24)), int(rng.integers(2, 40)), int(rng.integers(2, 140)))
+    rf, tf, pf = synth.grid(*dims, uniform=bool(seed % 2))
+    n = int(np.prod(dims))
+    x = synth.random_vector(n, seed).reshape(dims[::-1])
+    S = oracle.System(rf, tf, pf, SS)
+    with solver(rf, tf, pf, synth.br0_map(tf, pf, 0)) as s:
+        y = s.apply(x)
+        z1 = s.precond(x)
+    assert np.abs(y - S.apply(x)).max() <= 1e-13 * np.abs(S.apply(x)).max()
+    z1_ref = oracle.precond(rf, tf, pf, x, pc=1)
+    assert np.abs(z1 - z1_ref).max() <= 1e-14 * np.abs(z1_ref).max()
+    blocks = 1 + seed % min(2, dims[0])
+    with solver(rf, tf, pf, synth.br0_map(tf, pf, 0), pc=2, pc2_blocks=blocks) as s:
+        z2 = s.precond(x)
+    z2_ref = oracle.precond(rf, tf, pf, x, pc=2, pc2_blocks=blocks)
+    assert np.abs(z2 - z2_ref).max() <= 1e-12 * np.abs(z2_ref).max()
