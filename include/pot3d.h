@@ -38,11 +38,15 @@
  * before the call returns; the caller keeps ownership of every buffer.
  *
  * Multi-GPU: one process per GPU.  The grid is split into contiguous r-slabs
- * (leading ranks take the remainder shells); the halo of one
- * theta-phi shell per face is exchanged with NCCL send/recv and the dot
- * products are combined with an NCCL all-gather followed by a fixed-order
- * sum, so every rank holds bit-identical scalars.  Every call is
- * collective: all ranks call it with identical scalar arguments.
+ * (leading ranks take the remainder shells).  pot3d_setup maps the
+ * neighbours' p buffers and every rank's 1-KB mailbox through CUDA IPC (handles
+ * exchanged over NCCL): the kernels store the halo of one theta-phi shell per
+ * face straight into the neighbours' ghost shells over NVLink and post each
+ * rank's dot-product partials into every mailbox; all ranks sum them in rank
+ * order, so every rank holds bit-identical scalars.  If any rank cannot
+ * map the peers, the same steps run over NCCL (send/recv, all-gather).  Peer
+ * waits are bounded (20 s; the solve then fails with POT3D_ERR_CUDA).  Every call
+ * is collective: all ranks call it with identical scalar arguments.
  *
  * Errors: functions return a pot3d_status; on a negative status
  * pot3d_last_error(ctx) describes the failure.  No function aborts.
