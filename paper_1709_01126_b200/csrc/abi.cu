@@ -480,7 +480,11 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
       ax.G.part = 3;
       ax.G.role_rows = 1;
       ax.peers = pt;
-      CK(launch_k(ctx->pdl, kern_a(ctx), dim3(G.ntj * G.ntk, G.nchunks + 1), dim3(NTHREADS), SMEM_A,
+      // at least 3 chunks, so an interior chunk runs while the halo travels (the two
+      // chunks touching the ghost shells are scheduled last): 4 GPUs x 19 shells,
+      // 84.9 us per iteration with 3 chunks vs 89.1 with the single-GPU choice of 1
+      if (ax.G.nchunks < 3 && G.nr_loc >= 6) ax.G.nchunks = 3;
+      CK(launch_k(ctx->pdl, kern_a(ctx), dim3(G.ntj * G.ntk, ax.G.nchunks + 1), dim3(NTHREADS), SMEM_A,
                   ctx->stream, ctx->tmaps, ax, parity));
       MARK("passA");
       CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_A, 0,
