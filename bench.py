@@ -209,7 +209,7 @@ def main():
     rf, tf, pf = c.faces()
     br_np = c.br0((rf, tf, pf))
     s = Pot3d(rf, tf, pf, br_np, bc=c.bc, pc=c.pc, rank=rank, nranks=world,
-              pc2_blocks=args.pc2_blocks, unroll=8)  # fresh NCCL id broadcast inside
+              pc2_blocks=args.pc2_blocks, unroll=32)  # fresh NCCL id broadcast inside
     s.trace(True)  # in-situ pass durations of the timed solves (%globaltimer, no extra launches)
     info = s.info()
     fixed_iters = args.weak_iters if args.config == "weak" else 0

@@ -94,7 +94,7 @@ typedef struct {
   void *alloc_ctx;
   int32_t pc2_blocks;            /* PC2 ILU0 blocks per rank (r sub-slabs); 0 -> 1 (A11) */
   int32_t device;                /* CUDA ordinal; -1 = current device */
-  int32_t unroll;                /* PCG iterations per captured CUDA graph; 0 -> 8 */
+  int32_t unroll;                /* PCG iterations per captured CUDA graph; 0 -> 32 */
 } pot3d_runtime;
 
 typedef struct {

@@ -25,7 +25,7 @@ using namespace pot3d;
 struct pot3d_ctx {
   // problem
   int nr = 0, nt = 0, np = 0, bc = 0, pc_req = 1, pc = 1;
-  int rank = 0, nranks = 1, pc2_blocks = 1, unroll = 8;
+  int rank = 0, nranks = 1, pc2_blocks = 1, unroll = 32;
   int nchunks_b = 1;  // r-chunks of pass B (G.nchunks: pass A)
   bool pdl = true;    // programmatic dependent launch for the loop kernels (POT3D_PDL=0: off)
   int edge_blocks = 148 * 4;  // grid of the edge-shell kernel (POT3D_EDGE_BLOCKS)
@@ -845,7 +845,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   ctx->rank = R.rank;
   ctx->nranks = R.nranks < 1 ? 1 : R.nranks;
   ctx->pc2_blocks = R.pc2_blocks < 1 ? 1 : R.pc2_blocks;
-  ctx->unroll = R.unroll > 0 ? (R.unroll + 1) / 2 * 2 : 8;
+  ctx->unroll = R.unroll > 0 ? (R.unroll + 1) / 2 * 2 : 32;
   ctx->ualloc = R.alloc;
   ctx->ufree = R.free;
   ctx->actx = R.alloc_ctx;

@@ -189,7 +189,7 @@ class Pot3d:
 
     def __init__(self, r_faces, t_faces, p_faces, br0, bc=SOURCE_SURFACE, pc=PC1, *, rank=0,
                  nranks=1, nccl_id: bytes | None = None, stream=None, pc2_blocks=1, device=None,
-                 unroll=8, torch_allocator=True):
+                 unroll=32, torch_allocator=True):
         import torch
 
         if not torch.cuda.is_available():
