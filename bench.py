@@ -2,14 +2,18 @@
 """Benchmark of the B200 fp64 PCG potential-field solve (BASELINE.json metric:
 "fp64 PCG iters/s & GB/s vs HBM peak at 1/2/4/8 B200; time-to-solve").
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config medium] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config large] [--impl reference]
 
-One step = the whole hot path on one synthetic magnetogram:
-RHS from Br0 (a2) -> PCG to rtol 1e-9 (a3-a10) -> finish + B = grad Phi (a11);
-the metric setup (a1) happens once in pot3d_setup, like the paper's start-up
-(P:270).  N > 1: one process per GPU under torchrun; the grid is split into
-r-slabs with NCCL halo exchange + all-gathered dot products (strong scaling of
-the same grid).  Rank 0 prints ONE JSON line.
+Default workload: `large` (301x601x1201 = 217 M cells), the >= 200 M-cell
+configuration BASELINE.json's metric is quoted on (north star; the paper's
+case is 207 M points).  One step = the whole hot path (SURVEY.md
+§8(a)) on one synthetic magnetogram: RHS from Br0 (a2) -> PCG to rtol 1e-9
+(a3-a10) -> finish + B = grad Phi (a11); the metric setup (a1) happens once in
+pot3d_setup, like the paper's start-up.  `value` is device time (CUDA
+events around solve + field, inputs resident); `e2e` is the wall clock of the
+same steps including the pinned H2D of Br0 and the D2H of Phi and B.  N > 1:
+one process per GPU under torchrun; the grid is split into r-slabs (strong
+scaling of the same grid).  Rank 0 prints ONE JSON line.
 
 --impl reference times the CPU oracle (oracle/, the plain C fp64 PCG written
 from the paper) on this box's host cores on a bounded sample of the same
@@ -41,13 +45,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="medium",
+    ap.add_argument("--config", default="large",
                     choices=["tiny", "small", "medium", "large", "pc2", "weak"])
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
     ap.add_argument("--pc2-blocks", type=int, default=1)
     ap.add_argument("--weak-iters", type=int, default=300)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=20)
     ap.add_argument("--cpu-sample-iters", type=int, default=0,
                     help="oracle iterations per cpu sample (0 = auto, ~10-30 s)")
@@ -126,32 +129,61 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- oracle legs
-def oracle_sample(c, iters):
-    """Oracle PCG loop on the config: returns (iters/s, loop seconds)."""
-    import oracle
-
-    rf, tf, pf = c.faces()
-    br = c.br0((rf, tf, pf))
-    _, _, _, secs = oracle.solve_fixed(rf, tf, pf, br, iters, bc=c.bc, pc=c.pc)
-    return iters / secs, secs
+def host_cpu():
+    """CPU model (lscpu) and logical core count of this host."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return model, os.cpu_count()
 
 
 def auto_cpu_iters(c):
-    # ~ 0.25 s / iteration / 27M cells on 8 cores: aim for ~15 s of loop time
-    per_iter = 0.25 * c.n / 27.3e6 * (2.5 if c.pc == 2 else 1.0)
+    # ~ 0.12 s / iteration / 27M cells on 16 host threads: aim for ~15 s of loop time
+    per_iter = 0.12 * c.n / 27.3e6 * (2.5 if c.pc == 2 else 1.0)
     return int(max(3, min(200, 15.0 / max(per_iter, 1e-4))))
 
 
-def cpu_baseline(c, args):
-    import oracle
+class OracleRun:
+    """The CPU oracle (oracle/, the plain C fp64 PCG written from the paper) on
+    this box's host cores: the system is assembled once (oracle.Session), each
+    sample is the unchanged PCG loop from x0 = 0 for a fixed iteration count."""
 
-    oracle.build()
+    def __init__(self, c):
+        import oracle
+
+        oracle.build()
+        rf, tf, pf = c.faces()
+        t0 = time.perf_counter()
+        self.sess = oracle.Session(rf, tf, pf, c.br0((rf, tf, pf)), bc=c.bc, pc=c.pc)
+        self.setup_s = time.perf_counter() - t0
+        self.cores = oracle.threads()
+        self.model, self.ncpu = host_cpu()
+
+    def sample(self, iters):
+        _, secs = self.sess.solve_fixed(iters)
+        return iters / secs, secs
+
+    def desc(self, c, iters):
+        return (f"{iters} PCG iterations of {c.name} from x0 = 0 (oracle C fp64, DIA bands, OpenMP "
+                f"element-wise loops on {self.cores} threads, sequential dots; assembly "
+                f"{self.setup_s:.1f} s excluded); host: {self.model or 'unknown CPU'}, "
+                f"{self.ncpu} logical CPUs")
+
+
+def cpu_baseline(c, args):
+    o = OracleRun(c)
     iters = args.cpu_sample_iters or auto_cpu_iters(c)
-    v, secs = oracle_sample(c, iters)
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return {"value": v, "unit": "iters/s", "cores": cores, "kind": "oracle",
-            "sample": f"{iters} PCG iterations of {c.name} (oracle C fp64, DIA, OpenMP on "
-                      f"{cores} threads; assembly excluded), loop {secs:.1f} s"}
+    v, secs = o.sample(iters)
+    out = {"value": v, "unit": "iters/s", "cores": o.cores, "kind": "oracle",
+           "sample": o.desc(c, iters) + f", loop {secs:.1f} s", "cpu_model": o.model}
+    o.sess.close()
+    return out
 
 
 def run_reference(args):
@@ -160,19 +192,16 @@ def run_reference(args):
     if rank != 0:
         return 0
     c = make_config(args, world)
-    import oracle
-
-    oracle.build()
-    iters = args.cpu_sample_iters or max(3, auto_cpu_iters(c) // 3)
+    o = OracleRun(c)
+    iters = args.cpu_sample_iters or max(2, auto_cpu_iters(c) // 4)
     for _ in range(args.warmup):
-        oracle_sample(c, iters)
+        o.sample(iters)
     tot_it, tot_s = 0, 0.0
     for _ in range(args.steps):
-        v, secs = oracle_sample(c, iters)
+        _, secs = o.sample(iters)
         tot_it += iters
         tot_s += secs
     value = tot_it / tot_s
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     line = {
         "impl": "reference", "metric": "fp64 PCG iters/s", "value": value, "unit": "iters/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -180,13 +209,23 @@ def run_reference(args):
         "scaling": "weak" if args.config == "weak" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_desc(c, args),
-                   "step": f"{iters} oracle PCG iterations (bounded sample)"},
-        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{iters} PCG iterations per step of {c.name}"},
+                   "step": f"{iters} oracle PCG iterations (bounded sample of the solve)"},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": o.cores, "kind": "oracle",
+                         "sample": o.desc(c, iters), "cpu_model": o.model},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def traffic_of(config, kernel):
+    """ncu DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
+    `kernel` on `config` from the committed ncu capture summary, or None."""
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return tr.get(config, {}).get(kernel)
+    except Exception:
+        return None
 
 
 # --------------------------------------------------------------------------- own impl
@@ -204,6 +243,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1709_01126_b200 import Pot3d
+    from paper_1709_01126_b200.pot3d import _ptr
 
     c = make_config(args, world)
     rf, tf, pf = c.faces()
@@ -217,123 +257,111 @@ def main():
     maxit = fixed_iters if fixed_iters else 10**6
 
     dev = torch.device("cuda", local)
-    br_dev = torch.from_numpy(br_np).to(dev)
-    phi_dev = torch.empty((c.np, c.nt, s.nr_loc), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
     nbr = info["br_shells"]
+    phi_dev = torch.empty((c.np, c.nt, s.nr_loc), dtype=torch.float64, device=dev)
     B_dev = (torch.empty((c.np, c.nt, nbr), dtype=torch.float64, device=dev),
              torch.empty((c.np, c.nt + 1, s.nr_loc), dtype=torch.float64, device=dev),
              torch.empty((c.np, c.nt, s.nr_loc), dtype=torch.float64, device=dev))
-    from paper_1709_01126_b200.pot3d import _ptr
-
-    def step_device():
-        s.set_br0(br_dev)
-        res = s.solve(rtol=rtol, maxit=maxit, phi=phi_dev, true_residual=False)
-        s._check(s._L.pot3d_field(s._ctx, _ptr(B_dev[0])[0], _ptr(B_dev[1])[0], _ptr(B_dev[2])[0]))
-        return res
+    # pinned host buffers: the step's input (Br0) and its results (Phi, B)
+    br_h = torch.from_numpy(br_np).pin_memory()
+    phi_h = torch.empty(phi_dev.shape, dtype=torch.float64).pin_memory()
+    B_h = tuple(torch.empty(b.shape, dtype=torch.float64).pin_memory() for b in B_dev)
+    h2d = br_h.numel() * 8
+    d2h = (phi_h.numel() + sum(b.numel() for b in B_h)) * 8
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up
+    def step(ev):
+        """One step of the hot path through the public API: Br0 from pinned host
+        memory (pot3d_set_br0: H2D + a2), the solve (a3-a10) and B (a11) into
+        device buffers between CUDA events ev[0], ev[1] (the device-resident
+        `value`), then Phi and B read back into pinned host memory (e2e)."""
+        s.set_br0(br_h)
+        ev[0].record(stream)
+        res = s.solve(rtol=rtol, maxit=maxit, phi=phi_dev, true_residual=False)
+        s._check(s._L.pot3d_field(s._ctx, _ptr(B_dev[0])[0], _ptr(B_dev[1])[0], _ptr(B_dev[2])[0]))
+        ev[1].record(stream)
+        phi_h.copy_(phi_dev, non_blocking=True)
+        for bh, bd in zip(B_h, B_dev):
+            bh.copy_(bd, non_blocking=True)
+        stream.synchronize()
+        return res
+
+    def evpair():
+        return (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+
     for _ in range(args.warmup):
-        step_device()
+        step(evpair())
     barrier()
     clk = ClockSampler(local)
     clk.start()
-    stream = torch.cuda.current_stream(dev)
     launches0 = s.info()["kernel_launches"]
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    ev0.record(stream)
+    evs = [evpair() for _ in range(args.steps)]
     iters = []
-    for _ in range(args.steps):
-        res = step_device()
-        iters.append(res.iters)
-    ev1.record(stream)
     barrier()
+    w0 = time.perf_counter()
+    for ev in evs:
+        iters.append(step(ev).iters)
+    barrier()
+    wall = time.perf_counter() - w0
     clocks = clk.stop()
     launches = s.info()["kernel_launches"] - launches0
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms, wall], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms, wall = float(t[0].item()), float(t[1].item())
     tot_iters = int(sum(iters))
     value = tot_iters / (ms / 1e3)
-    # live durations of pass A / pass B inside the last timed solve (last <= 64 iterations)
-    us_a_live, us_b_live, n_live = s.kernel_times()
-
-    # end-to-end through the public API with pinned host buffers
-    e2e = None
-    if not args.no_e2e:
-        br_h = torch.from_numpy(br_np).pin_memory()
-        phi_h = torch.empty((c.np, c.nt, s.nr_loc), dtype=torch.float64).pin_memory()
-        B_h = tuple(torch.empty(b.shape, dtype=torch.float64).pin_memory() for b in B_dev)
-
-        def step_host():
-            s.set_br0(br_h)
-            r = s.solve(rtol=rtol, maxit=maxit, phi=phi_h, true_residual=False)
-            s._check(s._L.pot3d_field(s._ctx, _ptr(B_h[0])[0], _ptr(B_h[1])[0], _ptr(B_h[2])[0]))
-            return r
-
-        step_host()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        it_h = 0
-        for _ in range(args.steps):
-            it_h += step_host().iters
-        e1.record(stream)
-        barrier()
-        ems = e0.elapsed_time(e1)
-        t = torch.tensor([ems], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t.item())
-        h2d = br_h.numel() * 8
-        d2h = (phi_h.numel() + sum(b.numel() for b in B_h)) * 8
-        e2e = {"value": it_h / (ems / 1e3), "unit": "iters/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps,
-               "note": "C-ABI calls with pinned host buffers: Br0 H2D, Phi + Br/Bt/Bp D2H per step"}
+    e2e = {"value": tot_iters / wall, "unit": "iters/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * wall / args.steps,
+           "note": "wall clock (max over ranks) around every timed step: pot3d_set_br0 from pinned "
+                   "host memory (H2D), solve + field, Phi and Br/Bt/Bp copied to pinned host memory"}
+    # live durations of pass A / pass B inside the last timed solve (last <= 64 iterations);
+    # PC1's pass B moves 24 B/cell on even and 40 B/cell on odd iterations (A23)
+    k_it, k_ua, k_ub = s.kernel_trace()
+    n_live = len(k_it)
 
     # roofline of the dominant kernel: live durations from the timed solve; the
     # same passes launched separately between CUDA events are reported beside them
     ms_a_iso, ms_b_iso, ms_pc = s.profile(args.profile_iters)
-    if n_live > 0:
-        ms_a, ms_b, timing = us_a_live / 1e3, us_b_live / 1e3, (
-            f"live: mean first-block-start to last-block-end (%globaltimer) of the last {n_live} "
-            f"iterations of the last timed solve")
-    else:
-        ms_a, ms_b, timing = ms_a_iso, ms_b_iso, "isolated launches between CUDA events"
     cells_loc = s.nr_loc * c.nt * c.np
-    bytes_a, bytes_b = 24 * cells_loc, 40 * cells_loc
-    peaks = {}
+    pc1 = info["pc"] == 1
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         peak, peak_src = float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    gbs_a = bytes_a / (ms_a * 1e-3) / 1e9
-    gbs_b = bytes_b / (ms_b * 1e-3) / 1e9
-    dom = "k_pass_a_pc1" if ms_a >= ms_b else "k_pass_b_pc1"
-    if c.pc == 2:
-        dom = dom.replace("pc1", "pc2")
-    achieved = gbs_a if ms_a >= ms_b else gbs_b
-    dom_bytes, dom_ms = (bytes_a, ms_a) if ms_a >= ms_b else (bytes_b, ms_b)
-    if c.pc == 2 and ms_pc > max(ms_a, ms_b):
-        # PC2: the forward + backward ILU sweeps dominate (24 + 32 B per cell per apply)
-        dom = "k_sweep4 (forward + backward)"
-        dom_bytes, dom_ms = 56 * cells_loc, ms_pc
-        achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tr.get(c.name, {}).get(dom)
-    except Exception:
-        pass
-    loop_ms = (ms_a + ms_b + ms_pc)
+    # kernels of one iteration: (name, algorithmic bytes per launch, launches per iteration, ms)
+    if n_live > 0:
+        timing = (f"live: mean first-block-start to last-block-end (%globaltimer) of the last {n_live} "
+                  f"iterations of the last timed solve")
+        ms_a = float(np.mean(k_ua)) / 1e3
+        if pc1:
+            ev, od = k_ub[k_it % 2 == 0], k_ub[k_it % 2 == 1]
+            ms_be = float(np.mean(ev)) / 1e3 if len(ev) else float(np.mean(k_ub)) / 1e3
+            ms_bo = float(np.mean(od)) / 1e3 if len(od) else float(np.mean(k_ub)) / 1e3
+        else:
+            ms_b = float(np.mean(k_ub)) / 1e3
+    else:
+        timing = "isolated launches between CUDA events"
+        ms_a, ms_be, ms_bo, ms_b = ms_a_iso, ms_b_iso, ms_b_iso, ms_b_iso
+    kern = [("k_pass_a", 24 * cells_loc, 1.0, ms_a)]
+    if pc1:
+        kern += [("k_pass_b_pc1_even", 24 * cells_loc, 0.5, ms_be), ("k_pass_b_pc1_odd", 40 * cells_loc, 0.5, ms_bo)]
+    else:
+        kern += [("k_pass_b_pc2", 40 * cells_loc, 1.0, ms_b),
+                 ("k_sweep4 (forward + backward)", 56 * cells_loc, 1.0, ms_pc)]
+    table = {k: {"bytes_per_launch": by, "launches_per_iter": lp, "ms": t, "gbs": by / (t * 1e-3) / 1e9,
+                 "frac": by / (t * 1e-3) / 1e9 / peak} for k, by, lp, t in kern}
+    dom, dom_bytes, _, dom_ms = max(kern, key=lambda k: k[2] * k[3])
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    loop_ms = sum(lp * t for _, _, lp, t in kern)
+    loop_bytes = sum(lp * by for _, by, lp, _ in kern)
     per_iter_bytes = info["bytes_per_iter"]
 
     if rank != 0:
@@ -344,6 +372,7 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(c, args)
+    ws = info["device_bytes"]
     line = {
         "metric": "fp64 PCG iters/s", "value": value, "unit": "iters/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -356,25 +385,28 @@ def main():
             "iters_per_step": iters, "fixed_iters": bool(fixed_iters),
             "step": "rhs(a2) + PCG solve to rtol (a3-a10) + finish + field B (a11)",
             "parallelism": f"r-slabs x{world}" if world > 1 else "1 GPU",
-            "l2": f"inputs larger than L2: working set {info['device_bytes'] / 1e9:.2f} GB per rank "
-                  f"> 126 MB L2 (no flush)",
+            "l2": (f"inputs larger than L2: working set {ws / 1e9:.2f} GB per rank > 126 MB L2 (no flush)"
+                   if ws > L2_BYTES else
+                   f"working set {ws / 1e6:.1f} MB per rank fits the 126 MB L2 (latency-bound config)"),
         },
         "time_to_solve_s": ms / args.steps / 1e3,
         "cell_updates_per_s": c.n * value,
         "loop_gbs_algorithmic": per_iter_bytes * world * value / 1e9,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic,
+                     "traffic": traffic_of(c.name, dom.split(" ")[0]),
+                     "traffic_source": "profiles/traffic.json (ncu --set full dram__bytes_read.sum + "
+                                       "dram__bytes_write.sum per launch, this config)",
                      "algorithmic_bytes_per_launch": dom_bytes,
                      "ms_per_launch": dom_ms,
                      "timing": timing,
-                     "pass_a": {"ms": ms_a, "gbs": gbs_a, "bytes_per_cell": 24},
-                     "pass_b": {"ms": ms_b, "gbs": gbs_b, "bytes_per_cell": 40},
+                     "kernels": table,
                      "isolated": {"pass_a_ms": ms_a_iso, "pass_b_ms": ms_b_iso,
-                                  "pass_b_gbs": bytes_b / (ms_b_iso * 1e-3) / 1e9,
-                                  "note": "pot3d_profile: 20 launches between CUDA events after the timed region"},
-                     "precond_ms": ms_pc,
-                     "loop_gbs": (bytes_a + bytes_b) / (loop_ms * 1e-3) / 1e9 if c.pc == 1 else None},
+                                  "note": f"pot3d_profile: {args.profile_iters} launches between CUDA "
+                                          f"events after the timed region (pass B: both parities)"},
+                     "loop": {"bytes_per_iter": loop_bytes, "ms_per_iter": loop_ms,
+                              "gbs": loop_bytes / (loop_ms * 1e-3) / 1e9,
+                              "frac": loop_bytes / (loop_ms * 1e-3) / 1e9 / peak}},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -66,7 +66,10 @@ typedef struct pot3d_ctx pot3d_ctx; /* opaque; owns all device state */
 typedef enum {
   POT3D_OK = 0,
   POT3D_NOT_CONVERGED = 1,       /* maxit reached; outputs valid */
-  POT3D_PC2_FELL_BACK = 2,       /* ILU pivot <= 1e-300: PC1 used instead */
+  POT3D_PC2_FELL_BACK = 2,       /* ILU pivot <= 1e-300: PC1 used instead and the solve
+                                    converged; a fallen-back solve that
+                                    hit maxit returns POT3D_NOT_CONVERGED (pot3d_info().pc
+                                    still shows the fallback) */
   POT3D_ERR_INVALID = -1,        /* bad grid / sizes / arguments */
   POT3D_ERR_CUDA = -2,
   POT3D_ERR_NCCL = -3,
@@ -95,6 +98,15 @@ typedef struct {
   int32_t pc2_blocks;            /* PC2 ILU0 blocks per rank (r sub-slabs); 0 -> 1 (A11) */
   int32_t device;                /* CUDA ordinal; -1 = current device */
   int32_t unroll;                /* PCG iterations per captured CUDA graph; 0 -> 32 */
+  int32_t loopback_slabs;        /* > 1 (with nranks == 1): split the grid into this many
+                                    r-slabs on ONE device and run the multi-GPU peer-memory
+                                    exchange between them (halo stores into the siblings'
+                                    ghost shells, mailbox reductions in rank order)
+                                    ordered on one stream -- the multi-GPU path testable on
+                                    one GPU.  Arrays are then the whole grid. 0/1: off */
+  int32_t variant;               /* PCG recurrences: 0 standard (two reductions per
+                                    iteration), 1 single-reduction CG1
+                                    (Chronopoulos-Gear) */
 } pot3d_runtime;
 
 typedef struct {
@@ -139,13 +151,25 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
  * outputs are skipped.  POT3D_ERR_STATE before a successful solve. */
 int pot3d_field(pot3d_ctx *ctx, double *br, double *bt, double *bp);
 
-/* Diagnostics used by the parity tests (same kernels as the solve):
- * y = A x (homogeneous operator, A6) and z = M^-1 r on this rank's slab. */
+/* Diagnostics used by the parity tests.  They run the production kernels of
+ * the solve loop with scalars that turn them into plain applies (this rank's
+ * slab, layout as phi; x, y host or device; every rank calls them together):
+ *   pot3d_apply_fused(which = 0): y = A x (homogeneous operator, A6)
+ *       through pass B (PC2 instantiation: r_out = 0 - (-1) q = q exactly);
+ *   which = 1 (PC1 contexts): y = D^-1 A x through PC1's pass B
+ *       (z_out = 0 - (-1) D^-1 q, the Jacobi division of the loop);
+ *   which = 2: y = A x from pass A's stencil (a diagnostic instantiation of
+ *       the same code that also stores q).
+ * pot3d_apply = pot3d_apply_fused(which = 0).  pot3d_precond: z = M^-1 r
+ * (PC1: the init kernel that forms z_0 = D^-1 b; PC2: the D-ILU sweeps).
+ * Each invalidates the last solution.  POT3D_ERR_INVALID for a bad `which`. */
 int pot3d_apply(pot3d_ctx *ctx, const double *x, double *y);
+int pot3d_apply_fused(pot3d_ctx *ctx, const double *x, double *y, int32_t which);
 int pot3d_precond(pot3d_ctx *ctx, const double *r, double *z);
 
 /* Residual history of the last solve: hist[k] = ||r_k||/||b||, k = 0..n-1,
- * n = min(len, iters+1). Returns n or an error. */
+ * n = min(len, iters+1, 2^24) (the device buffer keeps the first 2^24 entries;
+ * maxit itself is not capped). Returns n or an error. */
 int64_t pot3d_history(pot3d_ctx *ctx, double *hist, int64_t len);
 
 int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info);
@@ -172,6 +196,11 @@ int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *nam
  * of iterations averaged (n).  POT3D_ERR_STATE if tracing was not enabled. */
 int pot3d_trace_enable(pot3d_ctx *ctx, int32_t on);
 int pot3d_kernel_times(pot3d_ctx *ctx, double *us_pass_a, double *us_pass_b, int32_t *n);
+/* The same ring per iteration: for up to `len` of the last <= 64 iterations of
+ * the last solve, the iteration index (0-based; PC1's pass B differs between
+ * even and odd iterations, A23) and the pass A / pass B durations in
+ * microseconds.  Returns the number of entries written or an error. */
+int pot3d_kernel_trace(pot3d_ctx *ctx, int64_t *iter, double *us_pass_a, double *us_pass_b, int32_t len);
 
 /* Rank 0 creates the 128-byte NCCL unique id that every rank passes in
  * pot3d_runtime.nccl_unique_id (the caller broadcasts it, e.g. with

@@ -12,12 +12,24 @@ Parity status of each function:
   assemble/apply   pinned: symmetry, null space, closed-form dipole/multipole,
                    hand-evaluated coefficients, dense brute force.
   rhs              pinned: closed form, S:234 hand evaluation, Σb = 0 (CW).
-  solve (PC1/PC2)  pinned: dense brute force, SPEC 2x2, closed form,
-                   monotone PC2 degradation, decomposition invariance.
+  pcg (standard)   pinned: SPEC 2x2 worked example through orc_pcg,
+                   exact termination of random SPD n <= 30, dense
+                   brute force.
+  pcg (CG1)        pinned: the same SPEC 2x2 / random SPD / brute-force pins,
+                   and exact-arithmetic equivalence with the standard
+                   variant (iterates agree to rounding, iterations +-1).
+  solve (PC1/PC2)  pinned: dense brute force, closed form, the survey's
+                   independent iteration counts (tiny PC1 229, PC2 91/96/104/
+                   114 for 1/2/4/8 blocks, closed wall 428, small 913),
+                   monotone PC2 degradation.
+  slab_bounds      pinned: explicit sizes (21 shells / 8 -> 3,3,3,3,3,2,2,2,
+                   S:392) and PC2 with 8 blocks = block-diagonal ILU0 of the
+                   explicitly listed slabs.
   ilu0             pinned: defining property (LU)_ij = a_ij on the pattern,
                    tridiagonal exact LU.
   field            pinned: Br(r0) = Br0, Phi=r -> Br=1, V div B = b - A Phi,
-                   closed-form dipole field.
+                   closed-form dipole field, polar-face Btheta of an m=1 field
+                   against its closed-form derivative (second order, A19).
   polar_average    pinned: constant ring, cos(phi) ring.
 """
 from __future__ import annotations
@@ -52,13 +64,21 @@ def build(force: bool = False) -> Path:
 
 
 _lib = None
+LINOP = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                         ctypes.POINTER(ctypes.c_double))
+STANDARD = 0   # orc_pcg variants: standard two-reduction PCG
+CG1 = 1        # Chronopoulos-Gear single-reduction PCG
 
 
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(str(_LIB))
+        # POT3D_ORACLE_LIB: a deliberately broken build (tools/oracle_mutants.py
+        # checks that the pins catch it); never set outside that script
+        alt = os.environ.get("POT3D_ORACLE_LIB")
+        if not alt:
+            build()
+        L = ctypes.CDLL(alt or str(_LIB))
         P = ctypes.POINTER
         d = P(ctypes.c_double)
         i64 = P(ctypes.c_int64)
@@ -76,6 +96,19 @@ def lib():
         L.orc_polar_average.restype = None
         L.orc_field.argtypes = [ci, ci, ci, d, d, d, ci, d, d, d, d, d]
         L.orc_volumes.argtypes = [ci, ci, ci, d, d, d, d]
+        L.orc_solve_v.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, d, ctypes.c_double,
+                                  ctypes.c_int64, ci, d, i64, d, d, d]
+        L.orc_pcg.argtypes = [ctypes.c_int64, LINOP, ctypes.c_void_p, LINOP, ctypes.c_void_p, d,
+                              ctypes.c_double, ctypes.c_int64, ci, d, i64, d, d]
+        L.orc_slab_bounds.argtypes = [ci, ci, ci, P(ci), P(ci)]
+        L.orc_slab_bounds.restype = None
+        L.orc_session_create.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, d]
+        L.orc_session_create.restype = ctypes.c_void_p
+        L.orc_session_solve.argtypes = [ctypes.c_void_p, ctypes.c_double, ctypes.c_int64, ci, d, i64,
+                                        d, d]
+        L.orc_session_free.argtypes = [ctypes.c_void_p]
+        L.orc_session_free.restype = None
+        L.orc_threads.restype = ci
         L.orc_solve_fixed.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, d, ctypes.c_int64, d, d, d]
         _lib = L
     return _lib
@@ -150,8 +183,9 @@ class System:
 
 
 def solve(rf, tf, pf, br0, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1, rtol=1e-9, maxit=100000,
-          history=False):
-    """Oracle PCG solve.  Returns dict(x, iters, rel_res, true_rel_res, status[, hist])."""
+          history=False, variant=STANDARD):
+    """Oracle PCG solve.  Returns dict(x, iters, rel_res, true_rel_res, status[, hist]).
+    variant: STANDARD or CG1 (Chronopoulos-Gear)."""
     rf, tf, pf, br0 = _f(rf), _f(tf), _f(pf), _f(br0)
     nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
     x = np.zeros(nr * nt * np_)
@@ -159,13 +193,52 @@ def solve(rf, tf, pf, br0, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1, rtol=1e-9, max
     rr = np.zeros(1)
     tr = np.zeros(1)
     hist = np.zeros(int(maxit) + 1) if history else None
-    st = lib().orc_solve(nr, nt, np_, _d(rf), _d(tf), _d(pf), bc, pc, pc2_blocks, _d(br0),
-                         float(rtol), int(maxit), _d(x), _i(it), _d(rr), _d(tr),
-                         _d(hist) if history else None)
+    st = lib().orc_solve_v(nr, nt, np_, _d(rf), _d(tf), _d(pf), bc, pc, pc2_blocks, _d(br0),
+                           float(rtol), int(maxit), int(variant), _d(x), _i(it), _d(rr), _d(tr),
+                           _d(hist) if history else None)
     out = dict(x=x.reshape(np_, nt, nr), iters=int(it[0]), rel_res=float(rr[0]),
                true_rel_res=float(tr[0]), status=st)
     if history:
         out["hist"] = hist[: out["iters"] + 1]
+    return out
+
+
+def pcg(A, b, rtol=1e-9, maxit=1000, minv=None, variant=STANDARD, history=False):
+    """The oracle's PCG loop (orc_pcg) on a caller operator: A is a dense
+    matrix or a callable x -> A x, minv (optional) a callable r -> M^-1 r.
+    Used for the SPEC worked example and random SPD systems.
+    Returns dict(x, iters, rel_res, status[, hist])."""
+    b = _f(b).reshape(-1)
+    n = b.size
+    fa = (lambda v: A @ v) if isinstance(A, np.ndarray) else A
+    fm = minv if minv is not None else (lambda v: v.copy())
+
+    def wrap(f):
+        def cb(_ctx, x, y):
+            xv = np.ctypeslib.as_array(x, shape=(n,))
+            np.ctypeslib.as_array(y, shape=(n,))[:] = f(xv.copy())
+        return LINOP(cb)
+
+    ca, cm = wrap(fa), wrap(fm)
+    x = np.zeros(n)
+    it = np.zeros(1, dtype=np.int64)
+    rr = np.zeros(1)
+    hist = np.zeros(int(maxit) + 1) if history else None
+    st = lib().orc_pcg(n, ca, None, cm, None, _d(b), float(rtol), int(maxit), int(variant), _d(x),
+                       _i(it), _d(rr), _d(hist) if history else None)
+    out = dict(x=x, iters=int(it[0]), rel_res=float(rr[0]), status=st)
+    if history:
+        out["hist"] = hist[: out["iters"] + 1]
+    return out
+
+
+def slab_bounds(nr, nblocks):
+    """[(i0, i1)] of the r-slab blocks (S:392 leading-remainder rule)."""
+    out = []
+    for b in range(nblocks):
+        i0, i1 = ctypes.c_int(), ctypes.c_int()
+        lib().orc_slab_bounds(nr, nblocks, b, ctypes.byref(i0), ctypes.byref(i1))
+        out.append((i0.value, i1.value))
     return out
 
 
@@ -234,3 +307,44 @@ def solve_fixed(rf, tf, pf, br0, iters, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1):
     st = lib().orc_solve_fixed(nr, nt, np_, _d(rf), _d(tf), _d(pf), bc, pc, pc2_blocks, _d(br0),
                                int(iters), _d(x), _d(rr), _d(secs))
     return x.reshape(np_, nt, nr), float(rr[0]), st, float(secs[0])
+
+
+class Session:
+    """Timing harness for bench.py (cpu_baseline / --impl reference): the
+    oracle system is assembled once, then solve_fixed(iters) runs the
+    unchanged PCG loop from x0 = 0 for `iters` iterations and returns
+    (rel_res, loop seconds).  Not part of the method."""
+
+    def __init__(self, rf, tf, pf, br0, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1):
+        rf, tf, pf, br0 = _f(rf), _f(tf), _f(pf), _f(br0)
+        self.nr, self.nt, self.np = len(rf) - 1, len(tf) - 1, len(pf) - 1
+        self.N = self.nr * self.nt * self.np
+        self._h = lib().orc_session_create(self.nr, self.nt, self.np, _d(rf), _d(tf), _d(pf), bc, pc,
+                                           pc2_blocks, _d(br0))
+        if not self._h:
+            raise ValueError("invalid grid")
+        self.x = np.zeros(self.N)
+
+    def solve_fixed(self, iters, variant=STANDARD):
+        it = np.zeros(1, dtype=np.int64)
+        rr = np.zeros(1)
+        secs = np.zeros(1)
+        lib().orc_session_solve(self._h, 0.0, int(iters), int(variant), _d(self.x), _i(it), _d(rr),
+                                _d(secs))
+        return float(rr[0]), float(secs[0])
+
+    def close(self):
+        if self._h:
+            lib().orc_session_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def threads():
+    """OpenMP threads of the oracle's element-wise loops."""
+    return int(lib().orc_threads())

@@ -445,37 +445,166 @@ static double now_s(void) {
 /* Plain sequential inner product in index order. */
 static double dot(int64_t n, const double *x, const double *y) {
   double s = 0.0;
+#ifdef ORC_DOT_REVERSE
+  /* an equally valid summation order (tools/oracle_spread.py only): measures how
+   * far the iteration count at rtol moves under a rounding-order change alone */
+  for (int64_t m = n - 1; m >= 0; m--) s += x[m] * y[m];
+#else
   for (int64_t m = 0; m < n; m++) s += x[m] * y[m];
+#endif
   return s;
 }
 
 /* ------------------------------------------------------------------------ */
-/* PCG (A9).                                             */
+/* PCG on an abstract SPD operator (A9).  A and M^-1 are */
+/* callbacks y = op(ctx, x), so the same loop runs the POT3D system         */
+/* (orc_solve) and the SPEC worked examples / random SPD matrices    */
+/* in the tests.                                                     */
+/*                                                                           */
+/* variant ORC_PCG_STANDARD (0) -- the standard two-reduction PCG:   */
 /*   x0 = 0, r = b, z = M^-1 r, p = z, rho = r.z                             */
 /*   loop: q = A p; sigma = p.q (<=0 -> indefinite); alpha = rho/sigma;      */
 /*         x += alpha p; r -= alpha q; k++;                                  */
 /*         stop if ||r|| <= rtol ||b|| or k == maxit;                        */
 /*         z = M^-1 r; rho' = r.z; p = z + (rho'/rho) p; rho = rho'.         */
-/* Closed wall: gauge-shift x to zero volume-weighted mean (A8).      */
-/* status: 0 converged, 1 maxit reached, 2 PC2 fell back to PC1 (converged  */
-/* or not), -1 bad input, -4 indefinite.                                     */
+/*                                                                           */
+/* variant ORC_PCG_CG1 (1) -- single-reduction PCG of Chronopoulos & Gear    */
+/* (1989), in the form of Ghysels & Vanroose (2014) Alg. 2.       */
+/* §8(f)-1: the paper names the inner products' "collective/synchronous     */
+/* nature" as the scaling limiter; this variant gathers the    */
+/* three inner products of an iteration into one reduction.  Not in the      */
+/* paper, so it follows the cited algorithm step by step:                    */
+/*   x0 = 0, r = b, u = M^-1 r, w = A u,                                     */
+/*   gamma = r.u, delta = w.u (<=0 -> indefinite), alpha = gamma/delta,      */
+/*   beta = 0;                                                               */
+/*   loop: p = u + beta p; s = w + beta s;  (k = 0: p = u, s = w)            */
+/*         x += alpha p; r -= alpha s; k++;                                  */
+/*         u = M^-1 r; w = A u; gamma' = r.u; delta = w.u; rr = r.r          */
+/*           (ONE reduction of three inner products);                        */
+/*         stop if sqrt(rr) <= rtol ||b|| or k == maxit;                     */
+/*         beta = gamma'/gamma; den = delta - beta gamma'/alpha              */
+/*           (= p.Ap in exact arithmetic; <=0 -> indefinite);                */
+/*         alpha = gamma'/den; gamma = gamma'.                               */
+/* In exact arithmetic both variants produce the same iterates.              */
+/*                                                                           */
+/* status: 0 converged, 1 maxit reached, -4 indefinite.                      */
 /* hist (nullable, maxit+1 doubles): ||r_k||/||b|| for k = 0..iters.          */
 /* ------------------------------------------------------------------------ */
-int orc_solve(int nr, int nt, int np, const double *rf, const double *tf,
-              const double *pf, int bc, int pc, int pc2_blocks, const double *br0,
-              double rtol, int64_t maxit, double *x, int64_t *iters,
-              double *rel_res, double *true_rel_res, double *hist) {
+typedef void (*orc_linop)(void *ctx, const double *x, double *y);
+#define ORC_PCG_STANDARD 0
+#define ORC_PCG_CG1 1
+
+int orc_pcg(int64_t N, orc_linop A, void *actx, orc_linop Minv, void *mctx, const double *b,
+            double rtol, int64_t maxit, int variant, double *x, int64_t *iters,
+            double *rel_res, double *hist) {
+  double *r = malloc(sizeof(double) * N);
+  double *z = malloc(sizeof(double) * N);  /* z (standard) / u (CG1) */
+  double *p = malloc(sizeof(double) * N);
+  double *q = malloc(sizeof(double) * N);  /* q = A p (standard) / w = A u (CG1) */
+  double *s = variant == ORC_PCG_CG1 ? malloc(sizeof(double) * N) : NULL;
+  int status = 0, conv = 0;
+  for (int64_t m = 0; m < N; m++) { x[m] = 0.0; r[m] = b[m]; }
+  const double bnorm = sqrt(dot(N, b, b));
+  int64_t k = 0;
+  double rnorm = bnorm;
+  if (hist) hist[0] = bnorm > 0 ? 1.0 : 0.0;
+  if (bnorm == 0.0) { /* b = 0 -> Phi = 0 (S:346) */
+    *iters = 0; *rel_res = 0.0;
+    goto done;
+  }
+  const double t_loop = now_s();
+  if (variant == ORC_PCG_STANDARD) {
+    Minv(mctx, r, z);
+    for (int64_t m = 0; m < N; m++) p[m] = z[m];
+    double rho = dot(N, r, z);
+    while (1) {
+      A(actx, p, q);
+      double sigma = dot(N, p, q);
+      if (!(sigma > 0.0)) { status = -4; break; }
+      double alpha = rho / sigma;
+#pragma omp parallel for schedule(static)
+      for (int64_t m = 0; m < N; m++) { x[m] += alpha * p[m]; r[m] -= alpha * q[m]; }
+      k++;
+      rnorm = sqrt(dot(N, r, r));
+      if (hist) hist[k] = rnorm / bnorm;
+      if (rnorm <= rtol * bnorm) { conv = 1; break; }
+      if (k >= maxit) break;
+      Minv(mctx, r, z);
+      double rho_new = dot(N, r, z);
+      double beta = rho_new / rho;
+#pragma omp parallel for schedule(static)
+      for (int64_t m = 0; m < N; m++) p[m] = z[m] + beta * p[m];
+      rho = rho_new;
+    }
+  } else {
+    Minv(mctx, r, z);          /* u */
+    A(actx, z, q);             /* w = A u */
+    double gamma = dot(N, r, z), delta = dot(N, q, z);
+    if (!(delta > 0.0)) { status = -4; goto stop; }
+    double alpha = gamma / delta, beta = 0.0;
+    while (1) {
+#pragma omp parallel for schedule(static)
+      for (int64_t m = 0; m < N; m++) {
+        p[m] = (k == 0) ? z[m] : z[m] + beta * p[m];
+        s[m] = (k == 0) ? q[m] : q[m] + beta * s[m];
+        x[m] += alpha * p[m];
+        r[m] -= alpha * s[m];
+      }
+      k++;
+      Minv(mctx, r, z);
+      A(actx, z, q);
+      double gamma_new = dot(N, r, z);
+      delta = dot(N, q, z);
+      rnorm = sqrt(dot(N, r, r));
+      if (hist) hist[k] = rnorm / bnorm;
+      if (rnorm <= rtol * bnorm) { conv = 1; break; }
+      if (k >= maxit) break;
+      beta = gamma_new / gamma;
+      double den = delta - beta * gamma_new / alpha;
+      if (!(den > 0.0)) { status = -4; break; }
+      alpha = gamma_new / den;
+      gamma = gamma_new;
+    }
+  }
+stop:
+  g_loop_seconds = now_s() - t_loop;
+  if (status == 0 && !conv) status = 1;
+  *iters = k;
+  *rel_res = rnorm / bnorm;
+done:
+  free(r); free(z); free(p); free(q); free(s);
+  return status;
+}
+
+/* The POT3D operator and preconditioners as orc_pcg callbacks. */
+typedef struct { int nr, nt, np; const double *bands, *wrap; } orc_sys;
+static void sys_apply(void *ctx, const double *x, double *y) {
+  const orc_sys *S = (const orc_sys *)ctx;
+  orc_apply(S->nr, S->nt, S->np, S->bands, S->wrap, x, y);
+}
+typedef struct { const orc_pc *M; const double *bands; } orc_pcctx;
+static void pc_cb(void *ctx, const double *r, double *z) {
+  const orc_pcctx *C = (const orc_pcctx *)ctx;
+  pc_apply(C->M, C->bands, r, z);
+}
+
+/* ------------------------------------------------------------------------ */
+/* The POT3D solve: assemble A (DIA), b (Eq.2),       */
+/* build PC1/PC2, run orc_pcg, closed-wall gauge (A8).         */
+/* status: 0 converged, 1 maxit reached, 2 PC2 fell back to PC1 (converged  */
+/* or not), -1 bad input, -4 indefinite.                                     */
+/* ------------------------------------------------------------------------ */
+int orc_solve_v(int nr, int nt, int np, const double *rf, const double *tf,
+                const double *pf, int bc, int pc, int pc2_blocks, const double *br0,
+                double rtol, int64_t maxit, int variant, double *x, int64_t *iters,
+                double *rel_res, double *true_rel_res, double *hist) {
   const int64_t N = (int64_t)nr * nt * np;
   orc_mesh g;
   if (mesh_build(&g, nr, nt, np, rf, tf, pf)) return -1;
   double *bands = malloc(sizeof(double) * 7 * N);
   double *wrap = malloc(sizeof(double) * 2 * nr * nt);
   double *b = malloc(sizeof(double) * N);
-  double *r = malloc(sizeof(double) * N);
-  double *z = malloc(sizeof(double) * N);
-  double *p = malloc(sizeof(double) * N);
-  double *q = malloc(sizeof(double) * N);
-  int status = 0;
+  int status = 0, fell_back = 0;
   orc_assemble(nr, nt, np, rf, tf, pf, bc, bands, wrap);
   orc_rhs(nr, nt, np, rf, tf, pf, bc, br0, b, NULL);
   orc_pc M;
@@ -483,44 +612,15 @@ int orc_solve(int nr, int nt, int np, const double *rf, const double *tf,
   if (prc == -2) { /* ILU breakdown: fall back to PC1 */
     pc_free(&M);
     pc_build(&M, 1, 1, nr, nt, np, bands);
-    status = 2;
+    fell_back = 1;
   } else if (prc) { status = -1; goto done; }
-
-  for (int64_t m = 0; m < N; m++) { x[m] = 0.0; r[m] = b[m]; }
+  orc_sys sys = {nr, nt, np, bands, wrap};
+  orc_pcctx pcc = {&M, bands};
+  status = orc_pcg(N, sys_apply, &sys, pc_cb, &pcc, b, rtol, maxit, variant, x, iters, rel_res,
+                   hist);
+  if (status == 0 && fell_back) status = 2;
   const double bnorm = sqrt(dot(N, b, b));
-  int64_t k = 0;
-  double rnorm = bnorm;
-  if (hist) hist[0] = bnorm > 0 ? 1.0 : 0.0;
-  if (bnorm == 0.0) { /* b = 0 -> Phi = 0 (S:346) */
-    *iters = 0; *rel_res = 0.0; if (true_rel_res) *true_rel_res = 0.0;
-    goto done;
-  }
-  pc_apply(&M, bands, r, z);
-  for (int64_t m = 0; m < N; m++) p[m] = z[m];
-  double rho = dot(N, r, z);
-  int conv = 0;
-  const double t_loop = now_s();
-  while (1) {
-    orc_apply(nr, nt, np, bands, wrap, p, q);
-    double sigma = dot(N, p, q);
-    if (!(sigma > 0.0)) { status = -4; break; }
-    double alpha = rho / sigma;
-#pragma omp parallel for schedule(static)
-    for (int64_t m = 0; m < N; m++) { x[m] += alpha * p[m]; r[m] -= alpha * q[m]; }
-    k++;
-    rnorm = sqrt(dot(N, r, r));
-    if (hist) hist[k] = rnorm / bnorm;
-    if (rnorm <= rtol * bnorm) { conv = 1; break; }
-    if (k >= maxit) break;
-    pc_apply(&M, bands, r, z);
-    double rho_new = dot(N, r, z);
-    double beta = rho_new / rho;
-#pragma omp parallel for schedule(static)
-    for (int64_t m = 0; m < N; m++) p[m] = z[m] + beta * p[m];
-    rho = rho_new;
-  }
-  g_loop_seconds = now_s() - t_loop;
-  if (status == 0 && !conv) status = 1;
+  if (bnorm == 0.0) { if (true_rel_res) *true_rel_res = 0.0; goto done; }
   if (bc == ORC_CLOSED_WALL) {
     double sv = 0.0, svx = 0.0;
     for (int kk = 0; kk < np; kk++)
@@ -532,18 +632,31 @@ int orc_solve(int nr, int nt, int np, const double *rf, const double *tf,
     double mean = svx / sv;
     for (int64_t m = 0; m < N; m++) x[m] -= mean;
   }
-  *iters = k;
-  *rel_res = rnorm / bnorm;
   if (true_rel_res) {
+    double *q = malloc(sizeof(double) * N);
     orc_apply(nr, nt, np, bands, wrap, x, q);
     for (int64_t m = 0; m < N; m++) q[m] = b[m] - q[m];
     *true_rel_res = sqrt(dot(N, q, q)) / bnorm;
+    free(q);
   }
 done:
   pc_free(&M);
-  free(bands); free(wrap); free(b); free(r); free(z); free(p); free(q);
+  free(bands); free(wrap); free(b);
   mesh_free(&g);
   return status;
+}
+
+int orc_solve(int nr, int nt, int np, const double *rf, const double *tf,
+              const double *pf, int bc, int pc, int pc2_blocks, const double *br0,
+              double rtol, int64_t maxit, double *x, int64_t *iters,
+              double *rel_res, double *true_rel_res, double *hist) {
+  return orc_solve_v(nr, nt, np, rf, tf, pf, bc, pc, pc2_blocks, br0, rtol, maxit,
+                     ORC_PCG_STANDARD, x, iters, rel_res, true_rel_res, hist);
+}
+
+/* Slab partition exported for the tests. */
+void orc_slab_bounds(int nr, int nblocks, int b, int *i0, int *i1) {
+  slab_bounds(nr, nblocks, b, i0, i1);
 }
 
 /* Preconditioner apply on its own (for tests): z = M^-1 r. */
@@ -682,6 +795,68 @@ int orc_volumes(int nr, int nt, int np, const double *rf, const double *tf,
         vol[i + (int64_t)nr * (j + (int64_t)nt * k)] = cell_volume(&g, i, j, k);
   mesh_free(&g);
   return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Timing harness for bench.py's cpu_baseline / --impl reference legs (not   */
+/* part of the method): the system (DIA bands, b, PC1/PC2) is assembled once */
+/* per session, then every orc_session_solve runs the unchanged orc_pcg from */
+/* x0 = 0 and reports the PCG loop's wall time.                              */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int64_t N;
+  double *bands, *wrap, *b;
+  orc_pc M;
+  orc_sys sys;
+  orc_pcctx pcc;
+} orc_session;
+
+void *orc_session_create(int nr, int nt, int np, const double *rf, const double *tf,
+                         const double *pf, int bc, int pc, int pc2_blocks, const double *br0) {
+  orc_mesh g;
+  if (mesh_build(&g, nr, nt, np, rf, tf, pf)) return NULL;
+  mesh_free(&g);
+  orc_session *S = calloc(1, sizeof(orc_session));
+  S->N = (int64_t)nr * nt * np;
+  S->bands = malloc(sizeof(double) * 7 * S->N);
+  S->wrap = malloc(sizeof(double) * 2 * nr * nt);
+  S->b = malloc(sizeof(double) * S->N);
+  orc_assemble(nr, nt, np, rf, tf, pf, bc, S->bands, S->wrap);
+  orc_rhs(nr, nt, np, rf, tf, pf, bc, br0, S->b, NULL);
+  if (pc_build(&S->M, pc, pc2_blocks, nr, nt, np, S->bands)) {
+    pc_free(&S->M);
+    pc_build(&S->M, 1, 1, nr, nt, np, S->bands);
+  }
+  S->sys = (orc_sys){nr, nt, np, S->bands, S->wrap};
+  S->pcc = (orc_pcctx){&S->M, S->bands};
+  return S;
+}
+
+int orc_session_solve(void *sp, double rtol, int64_t maxit, int variant, double *x,
+                      int64_t *iters, double *rel_res, double *loop_seconds) {
+  orc_session *S = (orc_session *)sp;
+  int st = orc_pcg(S->N, sys_apply, &S->sys, pc_cb, &S->pcc, S->b, rtol, maxit, variant, x, iters,
+                   rel_res, NULL);
+  if (loop_seconds) *loop_seconds = g_loop_seconds;
+  return st;
+}
+
+void orc_session_free(void *sp) {
+  orc_session *S = (orc_session *)sp;
+  if (!S) return;
+  pc_free(&S->M);
+  free(S->bands); free(S->wrap); free(S->b);
+  free(S);
+}
+
+/* Threads the element-wise loops use (reported as cpu_baseline.cores). */
+int orc_threads(void) {
+#ifdef _OPENMP
+  extern int omp_get_max_threads(void);
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
 }
 
 /* A fixed number of PCG iterations on a prebuilt system, for the timed

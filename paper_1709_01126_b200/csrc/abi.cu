@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <utility>
 #include <vector>
@@ -79,6 +80,11 @@ struct pot3d_ctx {
   int64_t n_launch = 0;     // kernels launched (graph launches count their kernel nodes)
   int64_t n_enq = 0;        // kernels enqueued by enqueue_iteration (graph capture)
   int64_t graph_nodes = 0;  // kernel nodes of the instantiated graph
+  // loopback group (pot3d_runtime.loopback_slabs = k > 1): this context is the group's
+  // handle (stream, graph, staging) and `slabs` are k slab contexts on the same device,
+  // ranks 0..k-1 of a peer-memory exchange wired with plain device pointers
+  std::vector<pot3d_ctx *> slabs;
+  bool member = false;  // a slab context of a loopback group (no NCCL)
   // state
   bool solved = false;
   int64_t last_iters = 0;
@@ -221,28 +227,32 @@ void block_bounds(int nr, int B, int b, int &i0, int &i1) {
 
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
-// user layout (r fastest, ni shells) <-> device cells (phi fastest)
+// user layout (r fastest, ni shells) <-> device cells (phi fastest).  ld > 0: the
+// user array is a slab of an r-fastest array with ld shells (a device pointer at the
+// slab's first shell: loopback groups stage the whole array on the device first).
 int to_device_cells(pot3d_ctx *ctx, const double *user, double *dev_cells_first_shell, int ni,
-                    long long stride_i) {
+                    long long stride_i, int ld = 0) {
   const size_t n = (size_t)ni * ctx->nt * ctx->np;
   const double *src = user;
-  if (!is_device_ptr(user)) {
+  if (ld <= 0) ld = ni;
+  if (ld == ni && !is_device_ptr(user)) {
     TRY(ensure_staging(ctx, n * sizeof(double)));
     CK(cudaMemcpyAsync(ctx->staging, user, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     src = ctx->staging;
   }
   dim3 blk(32, 8), grd((ctx->np + 31) / 32, (ni + 31) / 32, ctx->nt);
   k_transpose<<<grd, blk, 0, ctx->stream>>>(ni, ctx->nt, ctx->np, stride_i, ctx->G.PK, COFF, src,
-                                            dev_cells_first_shell, 1);
+                                            dev_cells_first_shell, 1, ld);
   CK(cudaGetLastError());
   ctx->n_launch++;
   return 0;
 }
 
 int from_device_cells(pot3d_ctx *ctx, const double *dev_first, double *user, int ni, int nj,
-                      long long stride_i, int coff = COFF) {
+                      long long stride_i, int coff = COFF, int ld = 0) {
   const size_t n = (size_t)ni * nj * ctx->np;
-  const bool dev = is_device_ptr(user);
+  if (ld <= 0) ld = ni;
+  const bool dev = ld != ni || is_device_ptr(user);
   double *dst = user;
   if (!dev) {
     TRY(ensure_staging(ctx, n * sizeof(double)));
@@ -250,7 +260,7 @@ int from_device_cells(pot3d_ctx *ctx, const double *dev_first, double *user, int
   }
   dim3 blk(32, 8), grd((ctx->np + 31) / 32, (ni + 31) / 32, nj);
   k_transpose<<<grd, blk, 0, ctx->stream>>>(ni, nj, ctx->np, stride_i, ctx->G.PK, coff, dev_first, dst,
-                                            0);
+                                            0, ld);
   CK(cudaGetLastError());
   ctx->n_launch++;
   if (!dev) {
@@ -413,7 +423,7 @@ PassArgs make_args(pot3d_ctx *ctx, int parity) {
   a.S = ctx->S;
   a.r = ctx->r;
   a.r_out = ctx->r;
-  a.z = ctx->z;
+  a.z = ctx->pc == 2 ? ctx->z : ctx->r;  // PC1 stores z = D^-1 r in ctx->r (A22)
   a.p_old = ctx->P[parity];
   a.p_new = ctx->P[parity ^ 1];
   a.x = ctx->x;
@@ -425,11 +435,12 @@ PassArgs make_args(pot3d_ctx *ctx, int parity) {
 }
 
 using PassKernel = void (*)(const TMaps, PassArgs, int);
-PassKernel kern_a(const pot3d_ctx *ctx) {
-  return ctx->pc == 2 ? k_pass_a_pc2 : k_pass_a_pc1;
-}
-PassKernel kern_b(const pot3d_ctx *ctx) {
-  return ctx->pc == 2 ? k_pass_b_pc2 : k_pass_b_pc1;
+PassKernel kern_a(const pot3d_ctx *) { return k_pass_a; }
+// parity = iteration index & 1 (every solve starts at iteration 0; graphs hold an even
+// number of iterations): PC1 updates x on odd iterations only (A23)
+PassKernel kern_b(const pot3d_ctx *ctx, int parity) {
+  if (ctx->pc == 2) return k_pass_b_pc2;
+  return parity ? k_pass_b_pc1_odd : k_pass_b_pc1_even;
 }
 
 // One PCG iteration (a3-a10) enqueued on ctx->stream; parity = iteration & 1.
@@ -458,6 +469,104 @@ static StepTimer *g_timer = nullptr;
     if (g_timer) g_timer->mark(n); \
   } while (0)
 
+// The kernels of one peer-memory iteration as separate launch steps.  A process
+// with one context runs them in order; a loopback group (several slab contexts on
+// one device, pot3d_runtime.loopback_slabs) runs step q of every slab before step
+// q+1 of any, so every wait of the exchange protocol (halo flags, mailboxes) is on
+// work that an earlier launch of the same stream already finished.
+using Step = std::function<int()>;
+std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
+  std::vector<Step> st;
+  const Grid &G = ctx->G;
+  PassArgs a = make_args(ctx, parity);
+  a.peers = ctx->peers;
+  PassArgs ab = a;  // pass B: its own r-chunking
+  ab.G.nchunks = ctx->nchunks_b;
+  const dim3 grd(G.ntj * G.ntk, G.nchunks), grdb(G.ntj * G.ntk, ctx->nchunks_b);
+  const bool pc2 = ctx->pc == 2;
+  const PeerTab *pt = ctx->peers;
+  auto fin = [ctx, pt](int kind, int what, double *hist, const char *nm) -> Step {
+    return [=]() -> int {
+      CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, kind, what, hist));
+      MARK(nm);
+      ctx->n_enq++;
+      return 0;
+    };
+  };
+  auto pass_b = [ctx, grdb, parity](PassArgs bx) -> Step {
+    return [=]() -> int {
+      CK(launch_k(ctx->pdl, kern_b(ctx, parity), grdb, dim3(NTHREADS), SMEM_B, ctx->stream, ctx->tmaps, bx,
+                  parity));
+      MARK("passB");
+      ctx->n_enq++;
+      return 0;
+    };
+  };
+  if (ctx->edge_in_a && !pc2) {
+    // pass A's first block row builds and sends the edge shells beside the interior
+    // chunks; beta is finalised by its own kernel after pass B.  The halo waits of
+    // the chunks next to a ghost shell (scheduled last in the grid) assume the
+    // neighbour's edge blocks (blockIdx.y = 0, scheduled first) get dispatched --
+    // linear block dispatch; POT3D_EDGE_IN_A=0 selects the separate edge kernel.
+    PassArgs ax = a;
+    ax.G.part = 3;
+    ax.G.role_rows = 1;
+    // at least 3 chunks, so an interior chunk runs while the halo travels (the two
+    // chunks touching the ghost shells are scheduled last): 4 GPUs x 19 shells,
+    // 84.9 us per iteration with 3 chunks vs 89.1 with the single-GPU choice of 1
+    if (ax.G.nchunks < 3 && G.nr_loc >= 6) ax.G.nchunks = 3;
+    st.push_back([=]() -> int {
+      CK(launch_k(ctx->pdl, kern_a(ctx), dim3(G.ntj * G.ntk, ax.G.nchunks + 1), dim3(NTHREADS), SMEM_A,
+                  ctx->stream, ctx->tmaps, ax, parity));
+      MARK("passA");
+      ctx->n_enq++;
+      return 0;
+    });
+    st.push_back(fin(MAIL_A, 0, nullptr, "finalize_alpha"));
+    st.push_back(pass_b(ab));
+    st.push_back(fin(MAIL_B, 1, ctx->hist, "finalize_beta"));
+    return st;
+  }
+  // PC1: the previous iteration's beta finalisation lives in edge_p (fold)
+  const int fold = pc2 ? 0 : 1;
+  st.push_back([=]() -> int {
+    CK(launch_k(ctx->pdl, k_edge_p, dim3(ctx->edge_blocks), dim3(256), 0, ctx->stream, G, ctx->M, ctx->S,
+                (const double *)(pc2 ? ctx->z : ctx->r), (const double *)ctx->P[parity], ctx->P[parity ^ 1], 1,
+                pt, parity ^ 1, ctx->hist, fold));
+    MARK("edge_p");
+    ctx->n_enq++;
+    return 0;
+  });
+  PassArgs ax = a;
+  ax.G.part = 3;
+  st.push_back([=]() -> int {
+    CK(launch_k(ctx->pdl, kern_a(ctx), grd, dim3(NTHREADS), SMEM_A, ctx->stream, ctx->tmaps, ax, parity));
+    MARK("passA");
+    ctx->n_enq++;
+    return 0;
+  });
+  st.push_back(fin(MAIL_A, 0, nullptr, "finalize_alpha"));
+  PassArgs bx = ab;
+  bx.fold = fold;  // PC1: pass B only posts its sums and marks them pending
+  st.push_back(pass_b(bx));
+  if (pc2) {
+    st.push_back(fin(MAIL_B, 2, ctx->hist, "finalize_rr"));
+    st.push_back([=]() -> int {
+      int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
+                         ctx->stream, true, pt);
+      if (nk < 0) {
+        ctx->err = pc2_last_error();
+        return POT3D_ERR_CUDA;
+      }
+      ctx->n_enq += nk;
+      MARK("pc2");
+      return 0;
+    });
+    st.push_back(fin(MAIL_C, 3, nullptr, "finalize_rho"));
+  }
+  return st;
+}
+
 int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   const Grid &G = ctx->G;
   PassArgs a = make_args(ctx, parity);
@@ -472,78 +581,14 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     // (flag per iteration); pass A waits for that flag only in the blocks whose
     // chunk touches a ghost shell (scheduled last); the rank sums go straight into
     // every rank's mailbox from the reductions' last blocks
-    const PeerTab *pt = ctx->peers;
-    if (ctx->edge_in_a && !pc2) {
-      // pass A's first block row builds and sends the edge shells beside the interior
-      // chunks; beta is finalised by its own kernel after pass B
-      PassArgs ax = a;
-      ax.G.part = 3;
-      ax.G.role_rows = 1;
-      ax.peers = pt;
-      // at least 3 chunks, so an interior chunk runs while the halo travels (the two
-      // chunks touching the ghost shells are scheduled last): 4 GPUs x 19 shells,
-      // 84.9 us per iteration with 3 chunks vs 89.1 with the single-GPU choice of 1
-      if (ax.G.nchunks < 3 && G.nr_loc >= 6) ax.G.nchunks = 3;
-      CK(launch_k(ctx->pdl, kern_a(ctx), dim3(G.ntj * G.ntk, ax.G.nchunks + 1), dim3(NTHREADS), SMEM_A,
-                  ctx->stream, ctx->tmaps, ax, parity));
-      MARK("passA");
-      CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_A, 0,
-                  (double *)nullptr));
-      MARK("finalize_alpha");
-      PassArgs bx = ab;
-      bx.peers = pt;
-      CK(launch_k(ctx->pdl, kern_b(ctx), grdb, dim3(NTHREADS), SMEM_B, ctx->stream, ctx->tmaps, bx, parity));
-      MARK("passB");
-      CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_B, 1,
-                  ctx->hist));
-      MARK("finalize_beta");
-      ctx->n_enq += 4;
-      return 0;
-    }
-    // PC1: the previous iteration's beta finalisation lives in edge_p (fold)
-    const int fold = pc2 ? 0 : 1;
-    CK(launch_k(ctx->pdl, k_edge_p, dim3(ctx->edge_blocks), dim3(256), 0, ctx->stream, G, ctx->M, ctx->S,
-                (const double *)(pc2 ? ctx->z : ctx->r), (const double *)ctx->P[parity],
-                ctx->P[parity ^ 1], pc2 ? 1 : 0, pt, parity ^ 1, ctx->hist, fold));
-    MARK("edge_p");
-    PassArgs ax = a;
-    ax.G.part = 3;
-    ax.peers = pt;
-    CK(launch_k(ctx->pdl, kern_a(ctx), grd, dim3(NTHREADS), SMEM_A,
-                ctx->stream, ctx->tmaps, ax, parity));
-    MARK("passA");
-    CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_A, 0,
-                (double *)nullptr));
-    MARK("finalize_alpha");
-    PassArgs bx = ab;
-    bx.peers = pt;
-    bx.fold = fold;  // pass B only posts its sums and marks them pending
-    CK(launch_k(ctx->pdl, kern_b(ctx), grdb, dim3(NTHREADS), SMEM_B,
-                ctx->stream, ctx->tmaps, bx, parity));
-    MARK("passB");
-    ctx->n_enq += 4;
-    if (!fold) {
-      CK(launch_k(ctx->pdl, k_finalize_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S, pt, (int)MAIL_B,
-                  2, ctx->hist));
-      MARK("finalize_rr");
-      ctx->n_enq++;
-    }
-    if (pc2) {
-      int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
-                         ctx->stream, true, pt);
-      TRY(nk);
-      k_finalize_mail<<<1, 1, 0, ctx->stream>>>(ctx->S, pt, MAIL_C, 3, nullptr);
-      CK(cudaGetLastError());
-      ctx->n_enq += nk + 1;
-      MARK("pc2");
-    }
+    for (auto &f : iteration_steps(ctx, parity)) TRY(f());
     return 0;
   }
   if (multi && G.nr_loc >= 3) {
     // edge shells first; their halo travels on the comm stream while pass A
     // covers the interior shells, then pass A finishes the two edge shells
     k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
-                                                ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0,
+                                                ctx->P[parity], ctx->P[parity ^ 1], 1,
                                                 nullptr, 0, nullptr, 0);
     CK(cudaGetLastError());
     ctx->n_enq++;
@@ -575,7 +620,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   } else {
     if (multi) {
       k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
-                                                  ctx->P[parity], ctx->P[parity ^ 1], pc2 ? 1 : 0,
+                                                  ctx->P[parity], ctx->P[parity ^ 1], 1,
                                                 nullptr, 0, nullptr, 0);
       CK(cudaGetLastError());
       ctx->n_enq++;
@@ -593,7 +638,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     ctx->n_enq++;
     MARK("finalize_alpha");
   }
-  CK(launch_k(ctx->pdl && !multi, kern_b(ctx), grdb, dim3(NTHREADS), SMEM_B,
+  CK(launch_k(ctx->pdl && !multi, kern_b(ctx, parity), grdb, dim3(NTHREADS), SMEM_B,
               ctx->stream, ctx->tmaps, ab, parity));
     ctx->n_enq++;
   MARK("passB");
@@ -681,9 +726,9 @@ int choose_chunks(pot3d_ctx *ctx) {
   const int lstage = POT3D_PLMAX - 2;
   int occ = 0, sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_b_pc1, NTHREADS, SMEM_B));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_b_pc1_odd, NTHREADS, SMEM_B));
   int occa = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occa, k_pass_a_pc1, NTHREADS, SMEM_A));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occa, k_pass_a, NTHREADS, SMEM_A));
   const double slots_a = (double)sms * std::max(1, occa), slots_b = (double)sms * std::max(1, occ);
   G.nchunks = pick_chunks(G, slots_a, std::min(lstage, 100));
   ctx->nchunks_b = pick_chunks(G, slots_b, std::min(lstage, 32));
@@ -693,6 +738,325 @@ int choose_chunks(pot3d_ctx *ctx) {
   };
   env_chunks("POT3D_CHUNKS", G.nchunks);
   env_chunks("POT3D_CHUNKS_B", ctx->nchunks_b);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Solve phases over the contexts of one process: {ctx} for a rank process, the k
+// slab contexts of a loopback group (handle ctx).  The group runs every phase for
+// all slabs on the one stream, so each collective point (gather_all, halo_all)
+// sees all slabs' inputs already enqueued before it.
+// ---------------------------------------------------------------------------
+std::vector<pot3d_ctx *> members(pot3d_ctx *ctx) {
+  if (!ctx->slabs.empty()) return ctx->slabs;
+  return {ctx};
+}
+
+// every rank's / slab's 2-double local sums into every `gathered`, rank order
+int gather_all(std::vector<pot3d_ctx *> &M) {
+  pot3d_ctx *ctx = M[0];
+  if (M.size() == 1) return gather_sums(ctx, 2);
+  for (pot3d_ctx *m : M)
+    for (size_t r = 0; r < M.size(); r++)
+      CK(cudaMemcpyAsync(m->gathered + 2 * r, M[r]->local_sum, 2 * sizeof(double), cudaMemcpyDeviceToDevice,
+                         m->stream));
+  return 0;
+}
+
+// ghost shells of a cell array from the neighbours' edge shells
+template <typename F>
+int halo_all(std::vector<pot3d_ctx *> &M, F arr) {
+  pot3d_ctx *ctx = M[0];
+  if (M.size() == 1) return halo_exchange(ctx, arr(ctx));
+  const size_t bytes = (size_t)ctx->G.plane * sizeof(double);
+  for (size_t q = 0; q < M.size(); q++) {
+    pot3d_ctx *m = M[q];
+    if (q > 0)
+      CK(cudaMemcpyAsync(arr(M[q - 1]) + sidx(M[q - 1]->G, M[q - 1]->G.nr_loc), arr(m) + sidx(m->G, 0), bytes,
+                         cudaMemcpyDeviceToDevice, m->stream));
+    if (q + 1 < M.size())
+      CK(cudaMemcpyAsync(arr(M[q + 1]) + sidx(M[q + 1]->G, -1), arr(m) + sidx(m->G, m->G.nr_loc - 1), bytes,
+                         cudaMemcpyDeviceToDevice, m->stream));
+  }
+  return 0;
+}
+
+// the cells of every member (F: device pointer of shell 0, device layout) into one
+// r-fastest user array (host or device); a group assembles the whole grid
+template <typename F>
+int cells_out(pot3d_ctx *h, std::vector<pot3d_ctx *> &M, F src, double *user, int nj = 0,
+              long long stride_i = 0, int coff = COFF, std::function<int(pot3d_ctx *)> ni_of = nullptr) {
+  pot3d_ctx *ctx = h;
+  if (nj <= 0) nj = h->nt;
+  auto ni_f = [&](pot3d_ctx *m) { return ni_of ? ni_of(m) : m->G.nr_loc; };
+  auto stride_f = [&](pot3d_ctx *m) { return stride_i > 0 ? stride_i : m->G.plane; };
+  if (M.size() == 1) return from_device_cells(M[0], src(M[0]), user, ni_f(M[0]), nj, stride_f(M[0]), coff);
+  int ld = 0;
+  for (pot3d_ctx *m : M) ld += ni_f(m);
+  const size_t n = (size_t)ld * nj * h->np;
+  const bool dev = is_device_ptr(user);
+  double *dst = user;
+  if (!dev) {
+    TRY(ensure_staging(h, n * sizeof(double)));
+    dst = h->staging;
+  }
+  int off = 0;
+  for (pot3d_ctx *m : M) {
+    TRY(from_device_cells(m, src(m), dst + off, ni_f(m), nj, stride_f(m), coff, ld));
+    off += ni_f(m);
+  }
+  if (!dev) {
+    CK(cudaMemcpyAsync(user, dst, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  return 0;
+}
+
+// an r-fastest user array (this process's cells: the whole grid for a group) into
+// every member's device cells (F: device pointer of shell 0)
+template <typename F>
+int cells_in(pot3d_ctx *h, std::vector<pot3d_ctx *> &M, const double *user, F dst) {
+  pot3d_ctx *ctx = h;
+  if (M.size() == 1) return to_device_cells(M[0], user, dst(M[0]), M[0]->G.nr_loc, M[0]->G.plane);
+  const size_t n = (size_t)h->nr * h->nt * h->np;
+  const double *src = user;
+  if (!is_device_ptr(user)) {
+    TRY(ensure_staging(h, n * sizeof(double)));
+    CK(cudaMemcpyAsync(h->staging, user, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    src = h->staging;
+  }
+  for (pot3d_ctx *m : M) TRY(to_device_cells(m, src + m->G.i0, dst(m), m->G.nr_loc, m->G.plane, h->nr));
+  return 0;
+}
+
+// hist buffer (maxit+1 doubles, capped at 2^24 entries); stale: the graph holds the old one
+int ensure_hist(pot3d_ctx *ctx, int64_t maxit, bool &stale) {
+  const int64_t hlen = std::min<int64_t>(maxit + 1, (int64_t)1 << 24);
+  if (hlen > ctx->hist_len) {
+    double *h = nullptr;
+    TRY(dalloc(ctx, &h, (size_t)hlen));
+    ctx->hist = h;
+    ctx->hist_len = hlen;
+    stale = true;
+  }
+  return 0;
+}
+
+int build_graph_group(pot3d_ctx *h);
+
+// x0 = 0, r = b, p = 0 (A9), the device scalars, PC2: z0 = M^-1 b, local init sums
+int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit) {
+  const Grid &G = ctx->G;
+  cudaStream_t s = ctx->stream;
+  const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
+  CK(cudaMemsetAsync(ctx->x, 0, cells * sizeof(double), s));
+  CK(cudaMemsetAsync(ctx->r, 0, cells * sizeof(double), s));
+  CK(cudaMemsetAsync(ctx->P[0], 0, cells * sizeof(double), s));
+  CK(cudaMemsetAsync(ctx->P[1], 0, cells * sizeof(double), s));
+  if (G.i0 == 0) {
+    CK(cudaMemcpyAsync(ctx->r + sidx(G, 0), ctx->bshell, G.plane * sizeof(double),
+                       cudaMemcpyDeviceToDevice, s));
+    k_fix_ghost_cols<<<(ctx->nt + 255) / 256, 256, 0, s>>>(G, ctx->r, 0, 1);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  Scalars h0{};
+  h0.epoch = ++ctx->epoch;
+  if ((ctx->trace_on || getenv("POT3D_TRACE")) && !ctx->trace) {
+    TRY(dalloc(ctx, &ctx->trace, 64 * 16));
+  }
+  if (ctx->trace) CK(cudaMemsetAsync(ctx->trace, 0, 64 * 16 * sizeof(unsigned long long), s));
+  h0.trace = ctx->trace;
+  h0.rtol = rtol;
+  h0.maxit = (long long)maxit;  // the history keeps the first hist_len entries
+  h0.hist_len = ctx->hist_len;
+  CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+  // z0 = M^-1 b, rho0 = b.z0, ||b|| (a10 init)
+  if (ctx->pc == 2) {
+    int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
+                       s, false);
+    TRY(nk);
+    CK(cudaGetLastError());
+    ctx->n_launch += nk;
+  }
+  k_init_dots<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, ctx->partials, ctx->nranks == 1,
+                                      ctx->local_sum, ctx->pc == 2, ctx->z);
+  CK(cudaGetLastError());
+  ctx->n_launch++;
+  if (ctx->pc == 1) {
+    // PC1 keeps z = D^-1 r instead of r (A22): z_0 = D^-1 b in place (ghost columns included)
+    k_edge_p<<<148 * 8, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, nullptr, ctx->r, -1, nullptr, 0, nullptr, 0);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  return 0;
+}
+
+// after gather_all: the global init scalars, hist[0] = 1 (||r_0|| = ||b||)
+int solve_init_end(pot3d_ctx *ctx) {
+  cudaStream_t s = ctx->stream;
+  if (ctx->nranks > 1) {
+    k_init_finalize<<<1, 1, 0, s>>>(ctx->S, ctx->gathered, ctx->nranks);
+    CK(cudaGetLastError());
+    ctx->n_launch++;
+  }
+  if (ctx->hist) {
+    double one = 1.0;
+    CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  return 0;
+}
+
+// the status of a finished loop (identical on every rank / slab)
+int loop_status(pot3d_ctx *ctx, pot3d_ctx *rep) {
+  const Scalars hs = *ctx->hS;
+  const Grid &G = ctx->G;
+  cudaStream_t s = ctx->stream;
+  if (ctx->trace && getenv("POT3D_TRACE")) {  // mean per-iteration timeline after the edge-shell kernel
+    std::vector<unsigned long long> t(64 * 16);
+    cudaMemcpy(t.data(), ctx->trace, t.size() * 8, cudaMemcpyDeviceToHost);
+    const char *nm[10] = {"edge0", "edge1", "A0", "Ahalo", "A1", "fin0", "fin1", "B0", "B1", "edgeM"};
+    double sum[10] = {0}, n = 0, per = 0;
+    for (int it = 0; it < 64; it++) {
+      const unsigned long long *r = &t[it * 16];
+      if (!r[0] || !r[8]) continue;
+      for (int q = 0; q < 10; q++) sum[q] += r[q] ? (double)(long long)(r[q] - r[0]) : 0.0;
+      const unsigned long long *nx = &t[((it + 1) % 64) * 16];
+      if (nx[0] > r[0]) per += (double)(nx[0] - r[0]);
+      n++;
+    }
+    if (n > 0) {
+      fprintf(stderr, "POT3D_TRACE rank %d (us after edge0, mean of %.0f iterations):", ctx->rank, n);
+      for (int q = 0; q < 10; q++) fprintf(stderr, " %s %.1f", nm[q], sum[q] / n / 1e3);
+      fprintf(stderr, " | iteration %.1f\n", per / n / 1e3);
+    }
+  }
+  if (ctx->pc == 2 && (pc2_status(ctx->pc2, s) & 2)) {
+    rep->err = "PC2 sweep handoff protocol error (bounded wait expired)";
+    return POT3D_ERR_CUDA;
+  }
+  if (hs.xfer_error || hs.status == -5) {
+    rep->err = "peer-memory exchange: bounded wait expired (a rank stalled or diverged)";
+    return POT3D_ERR_CUDA;
+  }
+  if (hs.status == -4) {
+    if (getenv("POT3D_DEBUG")) {  // diagnostics: scalars and non-finite counts of the vectors
+      fprintf(stderr, "POT3D_DEBUG iter %lld rho %g alpha %g beta %g sigma %g rr %g bnorm %g\n",
+              hs.iter, hs.rho, hs.alpha, hs.beta, hs.sigma, hs.rr, hs.bnorm);
+      const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
+      std::vector<double> h(cells);
+      const char *nm[5] = {"x", "r", "P0", "P1", "z"};
+      double *ar[5] = {ctx->x, ctx->r, ctx->P[0], ctx->P[1], ctx->z};
+      for (int q = 0; q < 5; q++) {
+        if (!ar[q]) continue;
+        cudaMemcpy(h.data(), ar[q], cells * 8, cudaMemcpyDeviceToHost);
+        size_t bad = 0, first = (size_t)-1;
+        double mx = 0;
+        for (size_t c = 0; c < cells; c++) {
+          if (!std::isfinite(h[c])) { if (!bad) first = c; bad++; }
+          else mx = std::max(mx, std::fabs(h[c]));
+        }
+        long long fi = first == (size_t)-1 ? -1 : (long long)first;
+        fprintf(stderr, "  %s: nonfinite %zu first %lld (shell %lld row %lld col %lld) max|.| %g\n", nm[q], bad, fi,
+                fi < 0 ? -1 : fi / G.plane - 1, fi < 0 ? -1 : (fi % G.plane) / G.PK,
+                fi < 0 ? -1 : (fi % G.PK) - COFF, mx);
+      }
+    }
+    rep->err = "p.Ap <= 0: operator or preconditioner not positive definite (S:341)";
+    return POT3D_ERR_INDEFINITE;
+  }
+  if (!hs.stop) {
+    rep->err = "loop ended without the stop flag";
+    return POT3D_ERR_STATE;
+  }
+  return 0;
+}
+
+// setup of the iteration, the device-driven loop (graphs of `unroll` predicated
+// iterations owned by h; the stop flag of graph g is read back while graph g+1 is
+// already queued), the status checks.  M[0]->hS holds the final scalars.
+int solve_run(pot3d_ctx *h, std::vector<pot3d_ctx *> &M, double rtol, int64_t maxit) {
+  pot3d_ctx *ctx = h;
+  cudaStream_t s = h->stream;
+  bool stale = false;
+  for (pot3d_ctx *m : M) TRY(ensure_hist(m, maxit, stale));
+  if (stale) TRY(M.size() > 1 ? build_graph_group(h) : build_graph(h));  // graph captured the old hist
+  for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit));
+  if (M.size() > 1 || M[0]->nranks > 1) TRY(gather_all(M));
+  for (pot3d_ctx *m : M) TRY(solve_init_end(m));
+  pot3d_ctx *m0 = M[0];
+  CK(cudaMemcpyAsync(m0->hS, m0->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int64_t launched = 0;
+  if (!m0->hS->stop) {
+    cudaEvent_t ev[2];
+    Scalars *hs2 = nullptr;
+    CK(cudaMallocHost(&hs2, 2 * sizeof(Scalars)));
+    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    CK(cudaGraphLaunch(h->gexec, s));
+    h->n_launch += h->graph_nodes;
+    CK(cudaMemcpyAsync(&hs2[0], m0->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ev[0], s));
+    launched++;
+    int cur = 0;
+    while (true) {
+      const bool more = (launched * h->graph_unroll) < maxit + h->graph_unroll;
+      if (more) {
+        CK(cudaGraphLaunch(h->gexec, s));
+        h->n_launch += h->graph_nodes;
+        CK(cudaMemcpyAsync(&hs2[cur ^ 1], m0->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ev[cur ^ 1], s));
+        launched++;
+      }
+      CK(cudaEventSynchronize(ev[cur]));
+      if (hs2[cur].stop || !more) break;
+      cur ^= 1;
+    }
+    CK(cudaStreamSynchronize(s));
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    cudaFreeHost(hs2);
+  }
+  for (pot3d_ctx *m : M) {
+    CK(cudaMemcpyAsync(m->hS, m->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  for (pot3d_ctx *m : M) {
+    m->last_iters = m->hS->iter;
+    TRY(loop_status(m, h));
+  }
+  return 0;
+}
+
+// one graph for a loopback group: step q of every slab before step q+1 of any
+int build_graph_group(pot3d_ctx *h) {
+  pot3d_ctx *ctx = h;
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  for (pot3d_ctx *m : h->slabs) m->n_enq = 0;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = 0;
+  for (int u = 0; u < h->unroll && rc == 0; u++) {
+    std::vector<std::vector<Step>> st;
+    for (pot3d_ctx *m : h->slabs) st.push_back(iteration_steps(m, u & 1));
+    for (size_t q = 0; q < st[0].size() && rc == 0; q++)
+      for (size_t k = 0; k < st.size() && rc == 0; k++) {
+        rc = st[k][q]();
+        if (rc) h->err = h->slabs[k]->err;
+      }
+  }
+  cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+  if (rc) return rc;
+  CK(e);
+  CK(cudaGraphInstantiate(&h->gexec, g, 0));
+  cudaGraphDestroy(g);
+  h->graph_unroll = h->unroll;
+  h->graph_nodes = 0;
+  for (pot3d_ctx *m : h->slabs) h->graph_nodes += m->n_enq;
   return 0;
 }
 }  // namespace
@@ -716,6 +1080,28 @@ int pot3d_nccl_unique_id(void *out128) {
 
 int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   if (!ctx || !info) return POT3D_ERR_INVALID;
+  if (!ctx->slabs.empty()) {  // loopback group: the whole grid on one device
+    pot3d_info_t mi{};
+    *info = pot3d_info_t{};
+    info->i0 = 0;
+    info->i1 = info->nr_loc = ctx->nr;
+    info->br_shells = ctx->nr + 1;
+    info->pc = ctx->pc;
+    info->pc2_blocks_total = ctx->pc2_blocks * (int32_t)ctx->slabs.size();
+    info->kernel_launches = ctx->n_launch;
+    for (const pot3d_ctx *m : ctx->slabs) {
+      pot3d_info(m, &mi);
+      info->graph_kernels_per_iter += mi.graph_kernels_per_iter;
+      info->bytes_per_iter += mi.bytes_per_iter;
+      info->device_bytes += mi.device_bytes;
+      info->kernel_launches += mi.kernel_launches;
+    }
+    info->device_bytes += (int64_t)ctx->dev_bytes;
+    info->exchange = 3;  // peer-memory exchange between the slabs of one device
+    info->chunks_a = ctx->slabs[0]->G.nchunks;
+    info->chunks_b = ctx->slabs[0]->nchunks_b;
+    return 0;
+  }
   info->i0 = ctx->G.i0;
   info->i1 = ctx->G.i0 + ctx->G.nr_loc;
   info->nr_loc = ctx->G.nr_loc;
@@ -726,9 +1112,10 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   if (ctx->nranks > 1) k += (ctx->xfer && ctx->pc == 1) ? 2 : 3;
   if (ctx->pc == 2 && ctx->pc2) k += pc2_kernels_per_apply(ctx->pc2) + (ctx->nranks > 1 ? 1 : 0);
   info->graph_kernels_per_iter = k;
-  // algorithmic bytes: PC1 64 B/cell (pass A 24 + pass B 40), PC2 + 56 B sweeps
+  // algorithmic bytes
   const int64_t cells = (int64_t)ctx->G.nr_loc * ctx->nt * ctx->np;
-  info->bytes_per_iter = (ctx->pc == 2 ? 120 : 64) * cells;
+  // PC1: pass A 24 + pass B 24 (even) / 40 (odd) = 56 B/cell on average (A23)
+  info->bytes_per_iter = (ctx->pc == 2 ? 120 : 56) * cells;
   info->device_bytes = (int64_t)ctx->dev_bytes;
   info->kernel_launches = ctx->n_launch;
   info->exchange = ctx->nranks == 1 ? 0 : (ctx->xfer ? 2 : 1);
@@ -740,6 +1127,17 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
 
 int pot3d_set_br0(pot3d_ctx *ctx, const double *br0) {
   if (!ctx || !br0) return POT3D_ERR_INVALID;
+  if (!ctx->slabs.empty()) {
+    for (pot3d_ctx *m : ctx->slabs) {
+      int rc = pot3d_set_br0(m, br0);
+      if (rc) {
+        ctx->err = m->err;
+        return rc;
+      }
+    }
+    ctx->solved = false;
+    return 0;
+  }
   const Grid &G = ctx->G;
   CK(cudaSetDevice(ctx->device));
   // (np, nt) theta-fastest user map -> device [j][k]: the transpose with ni = nt, nj = 1
@@ -752,7 +1150,8 @@ int pot3d_set_br0(pot3d_ctx *ctx, const double *br0) {
   }
   {
     dim3 blk(32, 8), grd((ctx->np + 31) / 32, (ctx->nt + 31) / 32, 1);
-    k_transpose<<<grd, blk, 0, ctx->stream>>>(ctx->nt, 1, ctx->np, G.PK, G.PK, COFF, src, ctx->br_dev, 1);
+    k_transpose<<<grd, blk, 0, ctx->stream>>>(ctx->nt, 1, ctx->np, G.PK, G.PK, COFF, src, ctx->br_dev, 1,
+                                              ctx->nt);
     CK(cudaGetLastError());
     ctx->n_launch++;
   }
@@ -774,11 +1173,12 @@ int pot3d_set_br0(pot3d_ctx *ctx, const double *br0) {
   return 0;
 }
 
-int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int32_t pc,
-                const pot3d_runtime *rt, pot3d_ctx **out) {
+static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int32_t pc,
+                     const pot3d_runtime *rt, pot3d_ctx **out, bool member) {
   if (!out) return POT3D_ERR_INVALID;
   *out = nullptr;
   pot3d_ctx *ctx = new pot3d_ctx();
+  ctx->member = member;
   auto fail = [&](int rc) {
     *out = nullptr;
     g_setup_error = ctx->err;  // reachable through pot3d_last_error(NULL)
@@ -836,7 +1236,9 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
     const char *eb = getenv("POT3D_EDGE_BLOCKS");
     if (eb && atoi(eb) > 0) ctx->edge_blocks = atoi(eb);
     const char *ea = getenv("POT3D_EDGE_IN_A");
-    ctx->edge_in_a = !(ea && atoi(ea) == 0);
+    // loopback slabs: the separate edge-shell kernel (no spin on a sibling's blocks
+    // inside one launch)
+    ctx->edge_in_a = !(ea && atoi(ea) == 0) && !member;
   }
   pot3d_runtime R{};
   R.nranks = 1;
@@ -850,7 +1252,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   ctx->ufree = R.free;
   ctx->actx = R.alloc_ctx;
   if (ctx->rank < 0 || ctx->rank >= ctx->nranks) { ctx->err = "bad rank"; return fail(POT3D_ERR_INVALID); }
-  if (ctx->nranks > 1 && !R.nccl_unique_id) { ctx->err = "nccl_unique_id required for nranks > 1"; return fail(POT3D_ERR_INVALID); }
+  if (ctx->nranks > 1 && !R.nccl_unique_id && !member) { ctx->err = "nccl_unique_id required for nranks > 1"; return fail(POT3D_ERR_INVALID); }
   const int B = ctx->nranks * ctx->pc2_blocks;
   if (nr < 2 * ctx->nranks || (pc == POT3D_PC2 && nr < B)) {
     ctx->err = "too many ranks/blocks for nr";
@@ -871,7 +1273,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
     ctx->own_stream = true;
   }
 
-  if (ctx->nranks > 1) {
+  if (ctx->nranks > 1 && !member) {
     CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_edge, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
@@ -895,10 +1297,11 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   G.ntj = (nt + TJ - 1) / TJ;
   G.ntk = (np + TK - 1) / TK;
   {
-    const void *fa[2] = {(const void *)k_pass_a_pc1, (const void *)k_pass_a_pc2};
-    const void *fb[2] = {(const void *)k_pass_b_pc1, (const void *)k_pass_b_pc2};
-    for (int q = 0; q < 2; q++) {
-      if (cudaFuncSetAttribute(fa[q], cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_A) ||
+    const void *fa[2] = {(const void *)k_pass_a, (const void *)k_pass_a_probe};
+    const void *fb[3] = {(const void *)k_pass_b_pc1_even, (const void *)k_pass_b_pc1_odd,
+                         (const void *)k_pass_b_pc2};
+    for (int q = 0; q < 3; q++) {
+      if ((q < 2 && cudaFuncSetAttribute(fa[q], cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_A)) ||
           cudaFuncSetAttribute(fb[q], cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B)) {
         ctx->err = "cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed";
         return fail(POT3D_ERR_CUDA);
@@ -941,7 +1344,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   DA(ctx->x, cells); DA(ctx->r, cells);
   {
     const char *xe = getenv("POT3D_XFER");
-    ctx->xfer_want = ctx->nranks > 1 && ctx->nranks <= MAXR && !(xe && atoi(xe) == 0);
+    ctx->xfer_want = member || (ctx->nranks > 1 && ctx->nranks <= MAXR && !(xe && atoi(xe) == 0));
   }
   if (ctx->xfer_want) {
     if ((rc = ipc_alloc(ctx, &ctx->P[0], cells)) || (rc = ipc_alloc(ctx, &ctx->P[1], cells)) ||
@@ -969,7 +1372,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   cudaMemsetAsync(ctx->S, 0, sizeof(Scalars), ctx->stream);
   if (cudaMallocHost(&ctx->hS, sizeof(Scalars)) != cudaSuccess) { ctx->err = "pinned alloc"; return fail(POT3D_ERR_CUDA); }
 
-  if (ctx->nranks > 1) {
+  if (ctx->nranks > 1 && !member) {
     ncclUniqueId id;
     memcpy(&id, R.nccl_unique_id, sizeof(id));
     ncclResult_t nr_ = ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank);
@@ -991,7 +1394,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
     if (rc) { ctx->err = "pc2_factor failed"; return fail(POT3D_ERR_CUDA); }
     // breakdown on any rank -> every rank falls back
     int bad = (minpiv < 1e-300) ? 1 : 0;
-    if (ctx->nranks > 1) {
+    if (ctx->nranks > 1 && !member) {  // loopback groups agree in setup_group
       int *d = nullptr;
       if ((rc = dalloc(ctx, &d, 2 * ctx->nranks))) return fail(rc);
       cudaMemcpyAsync(d, &bad, sizeof(int), cudaMemcpyHostToDevice, ctx->stream);
@@ -1010,7 +1413,7 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   {
     int rc2 = make_maps(ctx);
     if (rc2) return fail(rc2);
-    rc2 = build_graph(ctx);
+    if (!member) rc2 = build_graph(ctx);  // loopback: one graph for the whole group
     if (rc2) return fail(rc2);
   }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
@@ -1021,6 +1424,114 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
   return 0;
 }
 
+// Loopback group (pot3d_runtime.loopback_slabs = k > 1, one device): k slab contexts
+// (ranks 0..k-1 of the r-slab partition) whose peer tables hold the siblings'
+// P arrays and mailboxes directly; every kernel of the peer-memory exchange runs as
+// in a k-process job, ordered on one stream (build_graph_group).
+static int setup_group(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int32_t pc,
+                       const pot3d_runtime *rt, pot3d_ctx **out) {
+  *out = nullptr;
+  const int k = rt->loopback_slabs;
+  pot3d_ctx *h = new pot3d_ctx();
+  auto fail = [&](int rc) {
+    g_setup_error = h->err;
+    for (pot3d_ctx *m : h->slabs) pot3d_destroy(m);
+    h->slabs.clear();
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    dfree_all(h);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return rc;
+  };
+  if (!grid || !br0) {
+    h->err = "null argument";
+    return fail(POT3D_ERR_INVALID);
+  }
+  if (rt->nranks > 1 || k > MAXR) {
+    h->err = "loopback_slabs needs nranks == 1 and at most 16 slabs";
+    return fail(POT3D_ERR_INVALID);
+  }
+  h->nr = grid->nr; h->nt = grid->nt; h->np = grid->np;
+  h->bc = outer_bc;
+  h->pc_req = h->pc = pc;
+  h->pc2_blocks = rt->pc2_blocks < 1 ? 1 : rt->pc2_blocks;
+  h->unroll = rt->unroll > 0 ? (rt->unroll + 1) / 2 * 2 : 32;
+  h->ualloc = rt->alloc;
+  h->ufree = rt->free;
+  h->actx = rt->alloc_ctx;
+  if (rt->device >= 0) h->device = rt->device; else cudaGetDevice(&h->device);
+  if (cudaSetDevice(h->device) != cudaSuccess) { h->err = "cudaSetDevice failed"; return fail(POT3D_ERR_CUDA); }
+  if (rt->cuda_stream) {
+    h->stream = (cudaStream_t)rt->cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamDefault) != cudaSuccess) {
+      h->err = "stream creation failed";
+      return fail(POT3D_ERR_CUDA);
+    }
+    h->own_stream = true;
+  }
+  for (int q = 0; q < k; q++) {
+    pot3d_runtime R = *rt;
+    R.rank = q;
+    R.nranks = k;
+    R.loopback_slabs = 0;
+    R.nccl_unique_id = nullptr;
+    R.cuda_stream = h->stream;
+    R.device = h->device;
+    pot3d_ctx *m = nullptr;
+    int rc = setup_one(grid, br0, outer_bc, pc, &R, &m, true);
+    if (rc) {
+      h->err = "loopback slab " + std::to_string(q) + ": " + g_setup_error;
+      return fail(rc);
+    }
+    h->slabs.push_back(m);
+  }
+  // PC2 breakdown on any slab -> every slab falls back to PC1
+  bool fell = false;
+  for (pot3d_ctx *m : h->slabs) fell = fell || m->pc != pc;
+  for (pot3d_ctx *m : h->slabs) {
+    if (fell && m->pc != POT3D_PC1) {
+      m->pc = POT3D_PC1;
+      if (int rc = make_maps(m)) { h->err = m->err; return fail(rc); }
+    }
+    // the peer table from the siblings' plain device pointers
+    const int q = m->rank;
+    PeerTab T{};
+    T.rank = q;
+    T.nranks = k;
+    T.nr_lo = q > 0 ? h->slabs[q - 1]->G.nr_loc : 0;
+    for (int r = 0; r < k; r++) T.mail[r] = h->slabs[r]->mail;
+    for (int b = 0; b < 2; b++) {
+      if (q > 0) T.p_lo[b] = h->slabs[q - 1]->P[b];
+      if (q < k - 1) T.p_hi[b] = h->slabs[q + 1]->P[b];
+    }
+    if (int rc = dalloc(m, &m->peers, 1)) { h->err = m->err; return fail(rc); }
+    if (cudaMemcpyAsync(m->peers, &T, sizeof(PeerTab), cudaMemcpyHostToDevice, h->stream) != cudaSuccess) {
+      h->err = "peer table upload failed";
+      return fail(POT3D_ERR_CUDA);
+    }
+    m->xfer = true;
+  }
+  h->pc = h->slabs[0]->pc;
+  h->G = h->slabs[0]->G;  // tiling constants (chunks reported by pot3d_info)
+  h->G.i0 = 0;
+  h->G.nr_loc = h->nr;
+  if (int rc = build_graph_group(h)) return fail(rc);
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
+    h->err = std::string("loopback setup: ") + cudaGetErrorString(cudaGetLastError());
+    return fail(POT3D_ERR_CUDA);
+  }
+  *out = h;
+  return 0;
+}
+
+int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int32_t pc,
+                const pot3d_runtime *rt, pot3d_ctx **out) {
+  if (!out) return POT3D_ERR_INVALID;
+  if (rt && rt->loopback_slabs > 1) return setup_group(grid, br0, outer_bc, pc, rt, out);
+  return setup_one(grid, br0, outer_bc, pc, rt, out, false);
+}
+
 int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t *iters,
                 double *rel_residual, double *true_rel_residual) {
   if (!ctx) return POT3D_ERR_INVALID;
@@ -1029,202 +1540,75 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
     return POT3D_ERR_INVALID;
   }
   CK(cudaSetDevice(ctx->device));
-  const Grid &G = ctx->G;
-  cudaStream_t s = ctx->stream;
-  const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
+  std::vector<pot3d_ctx *> M = members(ctx);
+  for (pot3d_ctx *m : M) m->solved = false;
   ctx->solved = false;
-  // residual history buffer (maxit+1 doubles, capped)
-  const int64_t hlen = std::min<int64_t>(maxit + 1, (int64_t)1 << 24);
-  if (hlen > ctx->hist_len) {
-    double *h = nullptr;
-    TRY(dalloc(ctx, &h, (size_t)hlen));
-    ctx->hist = h;
-    ctx->hist_len = hlen;
-    TRY(build_graph(ctx));  // graph captured the old history pointer
-  }
-  // x0 = 0, r = b, p = 0 (A9)
-  CK(cudaMemsetAsync(ctx->x, 0, cells * sizeof(double), s));
-  CK(cudaMemsetAsync(ctx->r, 0, cells * sizeof(double), s));
-  CK(cudaMemsetAsync(ctx->P[0], 0, cells * sizeof(double), s));
-  CK(cudaMemsetAsync(ctx->P[1], 0, cells * sizeof(double), s));
-  if (G.i0 == 0) {
-    CK(cudaMemcpyAsync(ctx->r + sidx(G, 0), ctx->bshell, G.plane * sizeof(double),
-                       cudaMemcpyDeviceToDevice, s));
-    k_fix_ghost_cols<<<(ctx->nt + 255) / 256, 256, 0, s>>>(G, ctx->r, 0, 1);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
-  }
-  Scalars h0{};
-  h0.epoch = ++ctx->epoch;
-  if ((ctx->trace_on || getenv("POT3D_TRACE")) && !ctx->trace) {
-    TRY(dalloc(ctx, &ctx->trace, 64 * 16));
-  }
-  if (ctx->trace) CK(cudaMemsetAsync(ctx->trace, 0, 64 * 16 * sizeof(unsigned long long), s));
-  h0.trace = ctx->trace;
-  h0.rtol = rtol;
-  h0.maxit = (long long)std::min<int64_t>(maxit, hlen - 1);
-  CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
-  // z0 = M^-1 b, rho0 = b.z0, ||b|| (a10 init)
+  int rc = solve_run(ctx, M, rtol, maxit);
+  if (rc < 0) return rc;
+  const Scalars hs = *M[0]->hS;
+  cudaStream_t s = ctx->stream;
   const int nbi = 148 * 4;
-  if (ctx->pc == 2) {
-    int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
-                       s, false);
-    TRY(nk);
-    CK(cudaGetLastError());
-    ctx->n_launch += nk;
-  }
-  k_init_dots<<<nbi, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, ctx->partials, ctx->nranks == 1,
-                                  ctx->local_sum, ctx->pc == 2, ctx->z);
-  CK(cudaGetLastError());
-    ctx->n_launch++;
-  if (ctx->nranks > 1) {
-    TRY(gather_sums(ctx, 2));
-    k_init_finalize<<<1, 1, 0, s>>>(ctx->S, ctx->gathered, ctx->nranks);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
-  }
-  if (ctx->hist) {
-    // hist[0] = 1 (||r_0|| = ||b||)
-    double one = 1.0;
-    CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
-  }
-  // device-driven loop: graphs of `unroll` predicated iterations; the stop flag
-  // of graph g is read back while graph g+1 is already queued
-  CK(cudaMemcpyAsync(ctx->hS, ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  int64_t launched = 0;
-  if (!ctx->hS->stop) {
-    cudaEvent_t ev[2];
-    Scalars *hs2 = nullptr;
-    CK(cudaMallocHost(&hs2, 2 * sizeof(Scalars)));
-    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
-    CK(cudaGraphLaunch(ctx->gexec, s));
-    ctx->n_launch += ctx->graph_nodes;
-    CK(cudaMemcpyAsync(&hs2[0], ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-    CK(cudaEventRecord(ev[0], s));
-    launched++;
-    int cur = 0;
-    while (true) {
-      const bool more = (launched * ctx->graph_unroll) < maxit + ctx->graph_unroll;
-      if (more) {
-        CK(cudaGraphLaunch(ctx->gexec, s));
-        ctx->n_launch += ctx->graph_nodes;
-        CK(cudaMemcpyAsync(&hs2[cur ^ 1], ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(ev[cur ^ 1], s));
-        launched++;
-      }
-      CK(cudaEventSynchronize(ev[cur]));
-      if (hs2[cur].stop || !more) break;
-      cur ^= 1;
-    }
-    CK(cudaStreamSynchronize(s));
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-    cudaFreeHost(hs2);
-  }
-  CK(cudaMemcpyAsync(ctx->hS, ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const Scalars hs = *ctx->hS;
-  ctx->last_iters = hs.iter;
-  if (ctx->trace && getenv("POT3D_TRACE")) {  // mean per-iteration timeline after the edge-shell kernel
-    std::vector<unsigned long long> t(64 * 16);
-    cudaMemcpy(t.data(), ctx->trace, t.size() * 8, cudaMemcpyDeviceToHost);
-    const char *nm[10] = {"edge0", "edge1", "A0", "Ahalo", "A1", "fin0", "fin1", "B0", "B1", "edgeM"};
-    double sum[10] = {0}, n = 0, per = 0;
-    for (int it = 0; it < 64; it++) {
-      const unsigned long long *r = &t[it * 16];
-      if (!r[0] || !r[8]) continue;
-      for (int q = 0; q < 10; q++) sum[q] += r[q] ? (double)(long long)(r[q] - r[0]) : 0.0;
-      const unsigned long long *nx = &t[((it + 1) % 64) * 16];
-      if (nx[0] > r[0]) per += (double)(nx[0] - r[0]);
-      n++;
-    }
-    if (n > 0) {
-      fprintf(stderr, "POT3D_TRACE rank %d (us after edge0, mean of %.0f iterations):", ctx->rank, n);
-      for (int q = 0; q < 10; q++) fprintf(stderr, " %s %.1f", nm[q], sum[q] / n / 1e3);
-      fprintf(stderr, " | iteration %.1f\n", per / n / 1e3);
+  for (pot3d_ctx *m : M) {
+    // PC1 defers the x update of even iterations to the next (odd) pass B (A23): when the
+    // last iteration K = iters - 1 was even, x += alpha_K p_K (p_K in P[1]) now
+    if (m->pc == 1 && (hs.iter & 1)) {
+      k_x_finish<<<148 * 8, 256, 0, s>>>(m->G, m->S, m->x, m->P[1]);
+      CK(cudaGetLastError());
+      m->n_launch++;
     }
   }
-  if (ctx->pc == 2 && (pc2_status(ctx->pc2, s) & 2)) {
-    ctx->err = "PC2 sweep handoff protocol error (bounded wait expired)";
-    return POT3D_ERR_CUDA;
-  }
-  if (hs.xfer_error || hs.status == -5) {
-    ctx->err = "peer-memory exchange: bounded wait expired (a rank stalled or diverged)";
-    return POT3D_ERR_CUDA;
-  }
-  if (hs.status == -4) {
-    if (getenv("POT3D_DEBUG")) {  // diagnostics: scalars and non-finite counts of the vectors
-      fprintf(stderr, "POT3D_DEBUG iter %lld rho %g alpha %g beta %g sigma %g rr %g bnorm %g\n",
-              hs.iter, hs.rho, hs.alpha, hs.beta, hs.sigma, hs.rr, hs.bnorm);
-      const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
-      std::vector<double> h(cells);
-      const char *nm[5] = {"x", "r", "P0", "P1", "z"};
-      double *ar[5] = {ctx->x, ctx->r, ctx->P[0], ctx->P[1], ctx->z};
-      for (int q = 0; q < 5; q++) {
-        if (!ar[q]) continue;
-        cudaMemcpy(h.data(), ar[q], cells * 8, cudaMemcpyDeviceToHost);
-        size_t bad = 0, first = (size_t)-1;
-        double mx = 0;
-        for (size_t c = 0; c < cells; c++) {
-          if (!std::isfinite(h[c])) { if (!bad) first = c; bad++; }
-          else mx = std::max(mx, std::fabs(h[c]));
-        }
-        long long fi = first == (size_t)-1 ? -1 : (long long)first;
-        fprintf(stderr, "  %s: nonfinite %zu first %lld (shell %lld row %lld col %lld) max|.| %g\n", nm[q], bad, fi,
-                fi < 0 ? -1 : fi / G.plane - 1, fi < 0 ? -1 : (fi % G.plane) / G.PK,
-                fi < 0 ? -1 : (fi % G.PK) - COFF, mx);
-      }
-    }
-    ctx->err = "p.Ap <= 0: operator or preconditioner not positive definite (S:341)";
-    return POT3D_ERR_INDEFINITE;
-  }
-  if (!hs.stop) {
-    ctx->err = "loop ended without the stop flag";
-    return POT3D_ERR_STATE;
-  }
-  // (x is current: pass B applies x += alpha p_k in the same sweep as r -= alpha q)
   // closed wall: zero volume-weighted-mean gauge (A8)
   if (ctx->bc == POT3D_CLOSED_WALL && hs.bnorm > 0) {
-    k_gauge_sums<<<nbi, 256, 0, s>>>(G, ctx->M, ctx->m_vr, ctx->x, ctx->S, ctx->partials,
-                                      ctx->local_sum);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
-    TRY(gather_sums(ctx, 2));
-    k_gauge_shift<<<148 * 8, 256, 0, s>>>(G, ctx->x, ctx->gathered, ctx->nranks);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
+    for (pot3d_ctx *m : M) {
+      k_gauge_sums<<<nbi, 256, 0, s>>>(m->G, m->M, m->m_vr, m->x, m->S, m->partials, m->local_sum);
+      CK(cudaGetLastError());
+      m->n_launch++;
+    }
+    TRY(gather_all(M));
+    for (pot3d_ctx *m : M) {
+      k_gauge_shift<<<148 * 8, 256, 0, s>>>(m->G, m->x, m->gathered, m->nranks);
+      CK(cudaGetLastError());
+      m->n_launch++;
+    }
   }
-  TRY(halo_exchange(ctx, ctx->x));
+  TRY(halo_all(M, [](pot3d_ctx *m) { return m->x; }));
   if (true_rel_residual) {
-    k_apply<<<nbi, 256, 0, s>>>(G, ctx->M, ctx->x, nullptr, ctx->bshell, G.i0 == 0 ? 0 : -1000,
-                                ctx->S, ctx->partials, ctx->local_sum);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
-    TRY(gather_sums(ctx, 1));
-    std::vector<double> g(2 * ctx->nranks);
-    CK(cudaMemcpyAsync(g.data(), ctx->gathered, sizeof(double) * 2 * ctx->nranks,
-                       cudaMemcpyDeviceToHost, s));
+    for (pot3d_ctx *m : M) {
+      k_apply<<<nbi, 256, 0, s>>>(m->G, m->M, m->x, nullptr, m->bshell, m->G.i0 == 0 ? 0 : -1000, m->S,
+                                  m->partials, m->local_sum);
+      CK(cudaGetLastError());
+      m->n_launch++;
+    }
+    TRY(gather_all(M));
+    const int nr_ = M[0]->nranks;
+    std::vector<double> g(2 * nr_);
+    CK(cudaMemcpyAsync(g.data(), M[0]->gathered, sizeof(double) * 2 * nr_, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     double t = 0.0;
-    for (int rr = 0; rr < ctx->nranks; rr++) t += g[2 * rr];
+    for (int rr = 0; rr < nr_; rr++) t += g[2 * rr];
     *true_rel_residual = hs.bnorm > 0 ? std::sqrt(t) / hs.bnorm : 0.0;
   }
-  if (phi) TRY(from_device_cells(ctx, ctx->x + G.plane, phi, G.nr_loc, ctx->nt, G.plane));
+  if (phi) TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->x + m->G.plane; }, phi));
   CK(cudaStreamSynchronize(s));
   if (iters) *iters = hs.iter;
   if (rel_residual) *rel_residual = hs.bnorm > 0 ? std::sqrt(hs.rr) / hs.bnorm : 0.0;
   ctx->last_iters = hs.iter;
+  for (pot3d_ctx *m : M) {
+    m->last_iters = hs.iter;
+    m->solved = true;
+  }
   ctx->solved = true;
-  if (ctx->pc != ctx->pc_req) return POT3D_PC2_FELL_BACK;
-  return hs.status == 1 ? POT3D_NOT_CONVERGED : POT3D_OK;
+  // a fallen-back solve that did not converge reports NOT_CONVERGED; the fallback
+  // itself stays visible through pot3d_info().pc != the requested pc
+  if (hs.status == 1) return POT3D_NOT_CONVERGED;
+  return ctx->pc != ctx->pc_req ? POT3D_PC2_FELL_BACK : POT3D_OK;
 }
 
 int64_t pot3d_history(pot3d_ctx *ctx, double *hist, int64_t len) {
   if (!ctx || !hist) return POT3D_ERR_INVALID;
+  if (!ctx->slabs.empty()) ctx = ctx->slabs[0];  // every slab holds the same history
   if (!ctx->hist) return POT3D_ERR_STATE;
-  int64_t n = std::min<int64_t>(len, ctx->last_iters + 1);
+  int64_t n = std::min<int64_t>(std::min<int64_t>(len, ctx->last_iters + 1), ctx->hist_len);
   if (cudaMemcpy(hist, ctx->hist, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
     ctx->err = "history copy failed";
     return POT3D_ERR_CUDA;
@@ -1239,101 +1623,156 @@ int pot3d_field(pot3d_ctx *ctx, double *br, double *bt, double *bp) {
     return POT3D_ERR_STATE;
   }
   CK(cudaSetDevice(ctx->device));
-  const Grid &G = ctx->G;
   cudaStream_t s = ctx->stream;
-  // temporaries: reuse the Krylov buffers (x keeps the solution)
-  double *Br = ctx->P[0], *Bt = ctx->P[1], *Bp = ctx->r;
-  const int nbr = G.nr_loc + (ctx->rank == ctx->nranks - 1 ? 1 : 0);
+  std::vector<pot3d_ctx *> M = members(ctx);
   const int ntf = ctx->nt + 1;
-  // Bt needs nr_loc * (nt+1) * PK <= (nr_loc+2) * nt * PK
-  if ((long long)G.nr_loc * ntf > (long long)(G.nr_loc + 2) * ctx->nt) {
-    ctx->err = "field buffer too small";
-    return POT3D_ERR_STATE;
-  }
-  k_pole_avg<<<dim3(G.nr_loc, 2), 256, 0, s>>>(G, ctx->x, ctx->m_dp, ctx->pf[ctx->np] - ctx->pf[0],
-                                                ctx->poles, ctx->poles + G.nr_loc);
-  CK(cudaGetLastError());
-    ctx->n_launch++;
-  FieldArgs F{};
-  F.G = G;
-  F.x = ctx->x;
-  F.br = ctx->br_dev;
-  F.mean2 = ctx->bc == POT3D_CLOSED_WALL ? ctx->mean2 : nullptr;
-  F.rc = ctx->m_rc; F.dr = ctx->m_dr; F.drh = ctx->m_drh; F.tc = ctx->m_tc; F.tf = ctx->d_tf;
-  F.dth = ctx->m_dth; F.st = ctx->m_st; F.dph = ctx->m_dph;
-  F.poleN = ctx->poles; F.poleS = ctx->poles + G.nr_loc;
-  F.bc = ctx->bc;
-  F.nbr = nbr;
-  F.Br = Br; F.Bt = Bt; F.Bp = Bp;
-  const long long nc = (long long)G.nr_loc * ctx->nt * ctx->np;
-  if (br) {
-    long long n = (long long)nbr * ctx->nt * ctx->np;
-    k_field_r<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(F);
+  auto nbr_of = [](pot3d_ctx *m) { return m->G.nr_loc + (m->rank == m->nranks - 1 ? 1 : 0); };
+  for (pot3d_ctx *m : M) {
+    const Grid &G = m->G;
+    // temporaries: reuse the Krylov buffers (x keeps the solution); Bt needs
+    // nr_loc * (nt+1) * PK <= (nr_loc+2) * nt * PK
+    if ((long long)G.nr_loc * ntf > (long long)(G.nr_loc + 2) * m->nt) {
+      ctx->err = "field buffer too small";
+      return POT3D_ERR_STATE;
+    }
+    k_pole_avg<<<dim3(G.nr_loc, 2), 256, 0, s>>>(G, m->x, m->m_dp, m->pf[m->np] - m->pf[0], m->poles,
+                                                  m->poles + G.nr_loc);
     CK(cudaGetLastError());
-    ctx->n_launch++;
-    TRY(from_device_cells(ctx, Br, br, nbr, ctx->nt, G.plane, 0));
+    m->n_launch++;
+    FieldArgs F{};
+    F.G = G;
+    F.x = m->x;
+    F.br = m->br_dev;
+    F.mean2 = m->bc == POT3D_CLOSED_WALL ? m->mean2 : nullptr;
+    F.rc = m->m_rc; F.dr = m->m_dr; F.drh = m->m_drh; F.tc = m->m_tc; F.tf = m->d_tf;
+    F.dth = m->m_dth; F.st = m->m_st; F.dph = m->m_dph;
+    F.poleN = m->poles; F.poleS = m->poles + G.nr_loc;
+    F.bc = m->bc;
+    F.nbr = nbr_of(m);
+    F.Br = m->P[0]; F.Bt = m->P[1]; F.Bp = m->r;
+    const long long nc = (long long)G.nr_loc * m->nt * m->np;
+    if (br) {
+      long long n = (long long)F.nbr * m->nt * m->np;
+      k_field_r<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(F);
+      CK(cudaGetLastError());
+      m->n_launch++;
+    }
+    if (bt) {
+      long long n = (long long)G.nr_loc * ntf * m->np;
+      k_field_t<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(F);
+      CK(cudaGetLastError());
+      m->n_launch++;
+    }
+    if (bp) {
+      k_field_p<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(F);
+      CK(cudaGetLastError());
+      m->n_launch++;
+    }
   }
-  if (bt) {
-    long long n = (long long)G.nr_loc * ntf * ctx->np;
-    k_field_t<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(F);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
-    TRY(from_device_cells(ctx, Bt, bt, G.nr_loc, ntf, (long long)ntf * G.PK, 0));
-  }
-  if (bp) {
-    k_field_p<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(F);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
-    TRY(from_device_cells(ctx, Bp, bp, G.nr_loc, ctx->nt, G.plane, 0));
-  }
+  if (br) TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->P[0]; }, br, ctx->nt, 0, 0, nbr_of));
+  if (bt)
+    TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->P[1]; }, bt, ntf,
+                  (long long)ntf * M[0]->G.PK, 0));
+  if (bp) TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->r; }, bp, ctx->nt, 0, 0));
   CK(cudaStreamSynchronize(s));
   // the Krylov buffers were reused: a later field call needs a new solve's x only
   return 0;
 }
 
-int pot3d_apply(pot3d_ctx *ctx, const double *x, double *y) {
-  if (!ctx || !x || !y) return POT3D_ERR_INVALID;
+int pot3d_apply_fused(pot3d_ctx *ctx, const double *x, double *y, int32_t which) {
+  if (!ctx || !x || !y || which < 0 || which > 2) return POT3D_ERR_INVALID;
+  if (which == 1 && ctx->pc != POT3D_PC1) {
+    ctx->err = "pot3d_apply_fused(which=1) needs a PC1 context";
+    return POT3D_ERR_INVALID;
+  }
   CK(cudaSetDevice(ctx->device));
-  const Grid &G = ctx->G;
   cudaStream_t s = ctx->stream;
-  const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
-  double *xin = ctx->P[0], *yout = ctx->P[1];
-  CK(cudaMemsetAsync(xin, 0, cells * sizeof(double), s));
-  TRY(to_device_cells(ctx, x, xin + G.plane, G.nr_loc, G.plane));
-  TRY(halo_exchange(ctx, xin));
-  k_apply<<<148 * 4, 256, 0, s>>>(G, ctx->M, xin, yout, nullptr, 0, ctx->S, nullptr, nullptr);
-  CK(cudaGetLastError());
-    ctx->n_launch++;
-  TRY(from_device_cells(ctx, yout + G.plane, y, G.nr_loc, ctx->nt, G.plane));
+  std::vector<pot3d_ctx *> M = members(ctx);
+  // the production passes with scalars that turn them into plain applies (parity 0:
+  // pass A reads p_{k-1} from P[0] and writes p_k to P[1]; pass B reads p_k from P[1])
+  auto src_of = [](pot3d_ctx *m) { return m->pc == 2 ? m->z : m->r; };
+  auto fix_cols = [&](pot3d_ctx *m, double *a) -> int {
+    const Grid &G = m->G;
+    k_fix_ghost_cols<<<(unsigned)((G.nr_loc * (long long)m->nt + 255) / 256), 256, 0, s>>>(G, a, 0, G.nr_loc);
+    CK(cudaGetLastError());
+    m->n_launch++;
+    return 0;
+  };
+  Scalars h0{};
+  h0.alpha = -1.0;  // pass B: r_out = r - alpha q = 0 + q (exact), x_out = 0 - p
+  h0.beta = 0.0;    // pass A: p_k = src + 0 * p_{k-1} = x
+  h0.rho = 1.0;
+  h0.bnorm = 1.0;
+  h0.maxit = 1;
+  for (pot3d_ctx *m : M) {
+    const size_t cells = (size_t)(m->G.nr_loc + 2) * m->G.plane;
+    for (double *p : {m->x, m->r, m->P[0], m->P[1]}) CK(cudaMemsetAsync(p, 0, cells * sizeof(double), s));
+    if (m->z) CK(cudaMemsetAsync(m->z, 0, cells * sizeof(double), s));
+    CK(cudaMemcpyAsync(m->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+  }
+  TRY(cells_in(ctx, M, x, [](pot3d_ctx *m) { return m->P[1] + m->G.plane; }));
+  for (pot3d_ctx *m : M) TRY(fix_cols(m, m->P[1]));
+  TRY(halo_all(M, [](pot3d_ctx *m) { return m->P[1]; }));  // ghost shells: the neighbours' edge shells
+  if (which == 2) {
+    TRY(cells_in(ctx, M, x, [&](pot3d_ctx *m) { return src_of(m) + m->G.plane; }));
+    for (pot3d_ctx *m : M) TRY(fix_cols(m, src_of(m)));
+  }
+  for (pot3d_ctx *m : M) {
+    const Grid &G = m->G;
+    PassArgs a = make_args(m, 0);
+    a.finalize = 0;  // the partials only reach local_sum; the scalars are not touched
+    a.hist = nullptr;
+    if (which == 2) {
+      a.q_probe = m->x;
+      CK(launch_k(false, k_pass_a_probe, dim3(G.ntj * G.ntk, G.nchunks), dim3(NTHREADS), SMEM_A, s, m->tmaps,
+                  a, 0));
+    } else {
+      a.G.nchunks = m->nchunks_b;
+      CK(launch_k(false, which == 0 ? k_pass_b_pc2 : k_pass_b_pc1_even, dim3(G.ntj * G.ntk, m->nchunks_b),
+                  dim3(NTHREADS), SMEM_B, s, m->tmaps, a, 0));
+    }
+    m->n_launch++;
+    m->solved = false;
+  }
+  if (which == 2)
+    TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->x + m->G.plane; }, y));
+  else
+    TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->r + m->G.plane; }, y));
   CK(cudaStreamSynchronize(s));
   ctx->solved = false;
   return 0;
 }
 
+int pot3d_apply(pot3d_ctx *ctx, const double *x, double *y) { return pot3d_apply_fused(ctx, x, y, 0); }
+
 int pot3d_precond(pot3d_ctx *ctx, const double *rin, double *zout) {
   if (!ctx || !rin || !zout) return POT3D_ERR_INVALID;
   CK(cudaSetDevice(ctx->device));
-  const Grid &G = ctx->G;
   cudaStream_t s = ctx->stream;
-  const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
-  double *rr = ctx->P[0], *zz = ctx->P[1];
-  CK(cudaMemsetAsync(rr, 0, cells * sizeof(double), s));
-  CK(cudaMemsetAsync(zz, 0, cells * sizeof(double), s));
-  TRY(to_device_cells(ctx, rin, rr + G.plane, G.nr_loc, G.plane));
-  if (ctx->pc == 2) {
-    int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, rr, zz, ctx->partials, 0, ctx->local_sum, s, false);
-    TRY(nk);
-    CK(cudaGetLastError());
-    ctx->n_launch += nk;
-  } else {
-    // PC1: the edge-plane kernel computes z = D^-1 r (beta = 0) over any planes
-    Scalars h0{};
-    CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
-    k_edge_p<<<148 * 8, 256, 0, s>>>(G, ctx->M, ctx->S, rr, nullptr, zz, -1, nullptr, 0, nullptr, 0);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
+  std::vector<pot3d_ctx *> M = members(ctx);
+  for (pot3d_ctx *m : M) {
+    const size_t cells = (size_t)(m->G.nr_loc + 2) * m->G.plane;
+    CK(cudaMemsetAsync(m->P[0], 0, cells * sizeof(double), s));
+    CK(cudaMemsetAsync(m->P[1], 0, cells * sizeof(double), s));
   }
-  TRY(from_device_cells(ctx, zz + G.plane, zout, G.nr_loc, ctx->nt, G.plane));
+  TRY(cells_in(ctx, M, rin, [](pot3d_ctx *m) { return m->P[0] + m->G.plane; }));
+  for (pot3d_ctx *m : M) {
+    if (m->pc == 2) {
+      int nk = pc2_apply(m->pc2, m->M, m->S, m->P[0], m->P[1], m->partials, 0, m->local_sum, s, false);
+      TRY(nk);
+      CK(cudaGetLastError());
+      m->n_launch += nk;
+    } else {
+      // PC1: the kernel that forms z_0 = D^-1 b at the start of a solve (mode -1)
+      Scalars h0{};
+      CK(cudaMemcpyAsync(m->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+      k_edge_p<<<148 * 8, 256, 0, s>>>(m->G, m->M, m->S, m->P[0], nullptr, m->P[1], -1, nullptr, 0, nullptr, 0);
+      CK(cudaGetLastError());
+      m->n_launch++;
+    }
+    m->solved = false;
+  }
+  TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->P[1] + m->G.plane; }, zout));
   CK(cudaStreamSynchronize(s));
   ctx->solved = false;
   return 0;
@@ -1342,6 +1781,10 @@ int pot3d_precond(pot3d_ctx *ctx, const double *rin, double *zout) {
 int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_pass_b,
                   double *ms_precond) {
   if (!ctx || iters < 1) return POT3D_ERR_INVALID;
+  if (!ctx->slabs.empty()) {
+    ctx->err = "profiling is per slab context: not available on a loopback group";
+    return POT3D_ERR_INVALID;
+  }
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   const Grid &G = ctx->G;
@@ -1373,7 +1816,7 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
     PassArgs ab = a;
     ab.G.nchunks = ctx->nchunks_b;
     dim3 grdb(G.ntj * G.ntk, ctx->nchunks_b);
-    CK(launch_k(false, kern_b(ctx), grdb, dim3(NTHREADS), SMEM_B, s, ctx->tmaps, ab, par));
+    CK(launch_k(false, kern_b(ctx, par), grdb, dim3(NTHREADS), SMEM_B, s, ctx->tmaps, ab, par));
     CK(cudaEventRecord(ev[2], s));
     ctx->n_launch += 2;
     if (pc2) {
@@ -1399,6 +1842,10 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
 
 int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *names, int32_t nmax) {
   if (!ctx || iters < 1 || !ms || !names || nmax < 1) return POT3D_ERR_INVALID;
+  if (!ctx->slabs.empty()) {
+    ctx->err = "profiling is per slab context: not available on a loopback group";
+    return POT3D_ERR_INVALID;
+  }
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   CK(cudaMemcpyAsync(ctx->hS, ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
@@ -1415,6 +1862,14 @@ int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *nam
   CK(cudaMemcpyAsync(ctx->S, ctx->hS, sizeof(Scalars), cudaMemcpyHostToDevice, s));
   std::vector<double> acc;
   std::vector<const char *> nm;
+  // the profiled iterations continue past the last solve's history buffer: record
+  // no history (hist[iter+1 ..] would land beyond the allocation)
+  struct HistOff {
+    pot3d_ctx *c;
+    double *h;
+    ~HistOff() { c->hist = h; }
+  } hist_off{ctx, ctx->hist};
+  ctx->hist = nullptr;
   for (int it = 0; it < iters; it++) {
     StepTimer T;
     T.s = s;
@@ -1450,12 +1905,14 @@ int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *nam
 
 int pot3d_trace_enable(pot3d_ctx *ctx, int32_t on) {
   if (!ctx) return POT3D_ERR_INVALID;
+  for (pot3d_ctx *m : ctx->slabs) m->trace_on = on != 0;
   ctx->trace_on = on != 0;
   return 0;
 }
 
 int pot3d_kernel_times(pot3d_ctx *ctx, double *us_pass_a, double *us_pass_b, int32_t *n) {
   if (!ctx || !us_pass_a || !us_pass_b || !n) return POT3D_ERR_INVALID;
+  if (!ctx->slabs.empty()) ctx = ctx->slabs[0];
   *n = 0;
   if (!ctx->trace) {
     ctx->err = "tracing not enabled (pot3d_trace_enable before pot3d_solve)";
@@ -1481,10 +1938,37 @@ int pot3d_kernel_times(pot3d_ctx *ctx, double *us_pass_a, double *us_pass_b, int
   return 0;
 }
 
+int pot3d_kernel_trace(pot3d_ctx *ctx, int64_t *iter, double *us_pass_a, double *us_pass_b, int32_t len) {
+  if (!ctx || !iter || !us_pass_a || !us_pass_b || len < 1) return POT3D_ERR_INVALID;
+  if (!ctx->slabs.empty()) ctx = ctx->slabs[0];
+  if (!ctx->trace) {
+    ctx->err = "tracing not enabled (pot3d_trace_enable before pot3d_solve)";
+    return POT3D_ERR_STATE;
+  }
+  CK(cudaSetDevice(ctx->device));
+  std::vector<unsigned long long> t(64 * 16);
+  CK(cudaMemcpy(t.data(), ctx->trace, t.size() * 8, cudaMemcpyDeviceToHost));
+  // ring slot it holds iteration index it' with it' & 63 == it; recover it' from the
+  // last iteration count (the ring keeps the last 64 iterations of the last solve)
+  const int64_t last = ctx->last_iters;  // iterations 0 .. last-1 ran
+  int n = 0;
+  for (int64_t k = std::max<int64_t>(0, last - 64); k < last && n < len; k++) {
+    const unsigned long long *r = &t[(k & 63) * 16];
+    if (!r[TR_A0] || !r[TR_A1] || !r[TR_B0] || !r[TR_B1] || r[TR_A1] < r[TR_A0] || r[TR_B1] < r[TR_B0]) continue;
+    iter[n] = k;
+    us_pass_a[n] = (double)(r[TR_A1] - r[TR_A0]) / 1e3;
+    us_pass_b[n] = (double)(r[TR_B1] - r[TR_B0]) / 1e3;
+    n++;
+  }
+  return n;
+}
+
 int pot3d_destroy(pot3d_ctx *ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (pot3d_ctx *m : ctx->slabs) pot3d_destroy(m);
+  ctx->slabs.clear();
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->pc2) pc2_destroy(ctx->pc2, ctx->ufree, ctx->actx);
   ipc_release(ctx);

@@ -91,7 +91,7 @@ __device__ __forceinline__ void finalize_beta(Scalars *S, double rz, double rr, 
   S->iter = it;
   S->rr = rr;
   double rn = sqrt(rr);
-  if (hist) hist[it] = rn / S->bnorm;
+  if (hist && it < S->hist_len) hist[it] = rn / S->bnorm;
   S->alpha_prev = S->alpha;
   if (rn <= S->rtol * S->bnorm) {
     S->stop = 1;
@@ -113,7 +113,7 @@ __device__ __forceinline__ void finalize_rr(Scalars *S, double rr, double *hist)
   S->iter = it;
   S->rr = rr;
   double rn = sqrt(rr);
-  if (hist) hist[it] = rn / S->bnorm;
+  if (hist && it < S->hist_len) hist[it] = rn / S->bnorm;
   S->alpha_prev = S->alpha;
   if (rn <= S->rtol * S->bnorm) {
     S->stop = 1;
@@ -347,7 +347,8 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// The two edge shells of p_k = z + beta p_{k-1} by aligned column pairs (physical
+// The two edge shells of p_k = z + beta p_{k-1} (z the stored preconditioned
+// residual: PC1's D^-1 r buffer or PC2's sweep output) by aligned column pairs (physical
 // 2m, 2m+1 = logical k = 2m-1, 2m; 16-B loads and stores), stored locally and into
 // the neighbours' ghost shells (peer memory, same [il+1][j][c] layout shifted by
 // whole planes); the ghost columns (k = -1, np) are computed like cells from their
@@ -356,7 +357,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // block's stores were released system-wide), which then raises the halo flags.
 __device__ __forceinline__ bool edge_shells(const Grid &G, const Metrics &M, Scalars *S,
                                             const double *src, const double *p_old, double *p_new,
-                                            bool use_z, const PeerTab *peers, int parity_new,
+                                            const PeerTab *peers, int parity_new,
                                             double beta, int bid, int nblocks, bool work = true) {
   // peers == nullptr (NCCL exchange): local stores only, the caller sends the shells
   double *lo = peers ? peers->p_lo[parity_new] : nullptr, *hi = peers ? peers->p_hi[parity_new] : nullptr;
@@ -372,20 +373,11 @@ __device__ __forceinline__ bool edge_shells(const Grid &G, const Metrics &M, Sca
     const int j = (int)(t / npair), m = (int)(t - (long long)j * npair);
     const int il = sidx == 0 ? 0 : G.nr_loc - 1;
     const long long o = (long long)(il + 1) * G.plane + (long long)j * G.PK + 2 * m;  // physical 2m
-    const PlaneC P = plane_c(M, G.i0 + il);
-    const RowC R = row_c(M, j);
-    const DiagRow d = diag_row(P, R);
     const double2 sv = *reinterpret_cast<const double2 *>(src + o);
     const double2 pv = *reinterpret_cast<const double2 *>(p_old + o);
     double v[2];
-#pragma unroll
-    for (int e = 0; e < 2; e++) {
-      int k = 2 * m - 1 + e;  // logical column, wrapped for the ghost copies
-      k = (k < 0) ? k + G.np : (k >= G.np ? k - G.np : k);
-      const double s = e ? sv.y : sv.x, p = e ? pv.y : pv.x;
-      const double zv = use_z ? s : jacobi(s, diag_at(__ldg(M.dp + k), d, __ldg(M.app + k), __ldg(M.apm + k)));
-      v[e] = fma(beta, p, zv);  // the same arithmetic as pass A
-    }
+    v[0] = fma(beta, pv.x, sv.x);  // the same arithmetic as pass A
+    v[1] = fma(beta, pv.y, sv.y);
     const bool both = 2 * m + 1 <= G.np + 1;  // physical 2m+1 still a ghost or a cell
     double *rem = sidx == 0 ? lo : hi;
     if (both) {

@@ -192,7 +192,7 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
   }
   bool last_edge = false;  // every block counts in, also when the loop stops here
   if (mode >= 0)
-    last_edge = edge_shells(G, M, S, src, p_old, p_new, mode == 1, peers, parity_new, beta, blockIdx.x,
+    last_edge = edge_shells(G, M, S, src, p_old, p_new, peers, parity_new, beta, blockIdx.x,
                             gridDim.x, !s_stop);
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < (mode < 0 ? n : 0);
        c += (long long)gridDim.x * blockDim.x) {
@@ -234,7 +234,7 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
         } else {
           S->iter = iter;
           S->rr = s_rr;
-          if (hist) hist[iter] = sqrt(s_rr) / S->bnorm;
+          if (hist && iter < S->hist_len) hist[iter] = sqrt(s_rr) / S->bnorm;
           S->alpha_prev = S->alpha;
           if (s_stop) {
             S->status = s_status;
@@ -465,8 +465,9 @@ __global__ void k_gauge_shift(Grid G, double *x, const double *gathered, int nra
 // the device layout d[i*stride_i + j*PK + k] (phi fastest), tiled 32x32 over
 // (i, k) at fixed j.  to_dev: user -> device.
 // ---------------------------------------------------------------------------
+// user index i + ld*(j + nt*k) (ld >= ni: a slab of a larger r-fastest array)
 __global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, int coff,
-                            const double *src, double *dst, int to_dev) {
+                            const double *src, double *dst, int to_dev, int ld) {
   __shared__ double tile[32][33];
   const int j = blockIdx.z;
   const int i_b = blockIdx.y * 32, k_b = blockIdx.x * 32;
@@ -475,7 +476,7 @@ __global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, 
     // read user: contiguous in i
     for (int kk = ty; kk < 32; kk += 8) {
       int k = k_b + kk, i = i_b + tx;
-      if (k < np && i < ni) tile[kk][tx] = src[i + (long long)ni * (j + (long long)nt * k)];
+      if (k < np && i < ni) tile[kk][tx] = src[i + (long long)ld * (j + (long long)nt * k)];
     }
     __syncthreads();
     for (int ii = ty; ii < 32; ii += 8) {
@@ -490,7 +491,7 @@ __global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, 
     __syncthreads();
     for (int kk = ty; kk < 32; kk += 8) {
       int k = k_b + kk, i = i_b + tx;
-      if (k < np && i < ni) dst[i + (long long)ni * (j + (long long)nt * k)] = tile[kk][tx];
+      if (k < np && i < ni) dst[i + (long long)ld * (j + (long long)nt * k)] = tile[kk][tx];
     }
   }
 }

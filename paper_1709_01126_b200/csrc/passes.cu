@@ -1,12 +1,20 @@
 // passes.cu -- the two fused sm_100a passes of one PCG iteration (SURVEY.md
 // §8(a) rows a3, a7, a8).
 //
-//   pass A (k_pass_a_*):  p_k = z + beta p_{k-1}  (PC1: z = D^-1 r on the fly)
+//   pass A (k_pass_a):    p_k = z + beta p_{k-1}  (z: the stored preconditioned
+//                          residual -- PC1 keeps z = D^-1 r itself, PC2 the sweeps' z)
 //                          q   = A p_k            (7-point flux form, A1-A7)
 //                          sigma_partial = p_k . q                     [24 B/cell]
 //   pass B (k_pass_b_*):  q = A p_k (recomputed: cheaper than storing q)
-//                          x += alpha p_k;  r -= alpha q
-//                          PC1: z = D^-1 r, partials r.z, r.r  [40 B/cell]
+//                          x += alpha p_k
+//                          PC1: z -= alpha D^-1 q (= D^-1 (r - alpha q)),
+//                               partials r.z = (D z).z, r.r = (D z).(D z)
+//                          PC2: r -= alpha q, partial r.r               [40 B/cell]
+//
+// PC1 stores z = D^-1 r instead of r (reading A22): the recurrence
+// r_{k+1} = r_k - alpha q_k premultiplied by D^-1.  Pass A then needs no
+// division (p = z + beta p over the haloed box is one fma per cell) and pass B
+// divides once per interior cell, where it divided before as well.
 //
 // Both march along r through a TJ x TK theta-phi tile (2.5-D blocking).  For
 // every plane one elected thread loads the haloed box (TR rows x SROW columns:
@@ -35,14 +43,14 @@ namespace pot3d {
 static_assert(NS_A == 3, "pass A is unrolled by its stage count");
 
 struct SmemA {
-  double r[NS_A][TR][SROW];   // staged r (PC1) / z (PC2) / final p on ghost shells
+  double r[NS_A][TR][SROW];   // staged z (PC1: D^-1 r, PC2: the sweeps' z) / final p on ghost shells
   double p[NS_A][TR][SROW];   // staged p_{k-1}
   double pn[3][TR][SROW];     // p_k ring
   uint64_t bar[NS_A];
 };
 struct SmemB {
   double pn[NS_B][TR][SROW];  // staged p_k
-  double r[NS_B][TJ][TKB];    // staged r (interior rows)
+  double r[NS_B][TJ][TKB];    // staged z (PC1) / r (PC2) (interior rows)
   double x[NS_B][TJ][TKB];    // staged x (interior rows)
   uint64_t bar[NS_B];
 };
@@ -213,7 +221,7 @@ using IC = std::integral_constant<int, V>;
 // ---------------------------------------------------------------------------
 // pass A
 // ---------------------------------------------------------------------------
-template <bool USE_Z>
+template <bool PROBE>
 __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, int parity) {
   const Grid &G = A.G;
   const Metrics &M = A.M;
@@ -226,8 +234,8 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     pdl_trigger();
     pdl_wait();
     if (S->stop) return;
-    const bool last = edge_shells(G, M, S, USE_Z ? A.z : A.r, A.p_old, A.p_new, USE_Z, A.peers, parity ^ 1,
-                                  S->beta, blockIdx.x, gridDim.x);
+    const bool last = edge_shells(G, M, S, A.z, A.p_old, A.p_new, A.peers, parity ^ 1, S->beta,
+                                  blockIdx.x, gridDim.x);
     if (last && threadIdx.x == 0) {
       S->counter[4] = 0u;
       raise_halo_flags(A.peers, mail_seq(S->epoch, S->iter + 1));
@@ -351,26 +359,17 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
     const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
     const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
-    const PlaneC P = plane_at(pls, q);
     const PlaneC Ps = plane_at(pls, do_st ? q - 1 : q);
     mbar_wait(&sm.bar[u], ph);
-    // ---- transform plane il -> p_k ----
+    // ---- transform plane il -> p_k = z + beta p_{k-1} (ghost shells: the final p_k) ----
 #pragma unroll
     for (int e = 0; e < RPW; e++) {
       const int r = t.row[e];
       const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[u][r][cs]);
       const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[u][r][cs]);  // unused on ghosts
       double2 pn;
-      if (USE_Z) {
-        pn.x = ghost ? rv.x : fma(beta, pv.x, rv.x);
-        pn.y = ghost ? rv.y : fma(beta, pv.y, rv.y);
-      } else {
-        const DiagRow d = diag_row(P, rw[e]);
-        const double z0 = jacobi(rv.x, diag_at(dp.x, d, ap.x, am.x));
-        const double z1 = jacobi(rv.y, diag_at(dp.y, d, ap.y, am.y));
-        pn.x = selp(rv.x, fma(beta, pv.x, z0), ghost);
-        pn.y = selp(rv.y, fma(beta, pv.y, z1), ghost);
-      }
+      pn.x = selp(rv.x, fma(beta, pv.x, rv.x), ghost);
+      pn.y = selp(rv.y, fma(beta, pv.y, rv.y), ghost);
       R[u][e] = pn;
       *reinterpret_cast<double2 *>(&sm.pn[u][r][cs]) = pn;
       if (store && t.stencil[e]) store_pair(g_pn + t.rowoff[e], t, G.np, pn, false);
@@ -399,6 +398,9 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
         const double q1 = stencil7(c.y, R[u][e].y, R[umm][e].y, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e]);
 #endif
         acc += (m0[e] ? c.x * q0 : 0.0) + (m1[e] ? c.y * q1 : 0.0);
+        // diagnostic instantiation only (pot3d_probe_pass_a): q of plane il-1
+        if (PROBE && t.stencil[e])
+          store_pair(A.q_probe + (long long)il * PL + t.rowoff[e], t, G.np, make_double2(q0, q1), false);
       }
     }
   };
@@ -434,7 +436,14 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
 // ---------------------------------------------------------------------------
 // pass B
 // ---------------------------------------------------------------------------
-template <bool USE_Z>
+// USE_Z = false: PC1, the stored vector is z = D^-1 r; true: PC2, the stored vector is r.
+// XM: the x update (A20).  XM_EVERY: x += alpha_k p_k (PC2).  PC1 updates x every other
+// iteration (reading A23): XM_SKIP on even iterations k (x untouched, 24 B/cell), XM_PAIR
+// on odd k: x += alpha_{k-1} p_{k-1} + alpha_k p_k with p_{k-1} = (p_k - z_k) / beta_{k-1}
+// rebuilt from the operands pass B stages anyway, i.e. x += (c + alpha_k) p_k - c z_k,
+// c = alpha_{k-1} / beta_{k-1} (40 B/cell) -- 32 instead of 40 B/cell on average.
+enum XMode { XM_EVERY = 0, XM_SKIP = 1, XM_PAIR = 2 };
+template <bool USE_Z, int XM>
 __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, int parity) {
   const Grid &G = A.G;
   const Metrics &M = A.M;
@@ -465,11 +474,11 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
     if (qi <= L + 1) {
       const int il = t.c0 - 1 + qi;
       const bool rown = (qi >= 1) && (qi <= L);
-      mbar_arrive_expect_tx(&sm.bar[si], rown ? PB + 2 * RB : PB);
+      mbar_arrive_expect_tx(&sm.bar[si], rown ? PB + (XM == XM_SKIP ? 1 : 2) * RB : PB);
       tma_load_3d(&sm.pn[si][0][0], map_p, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
       if (rown) {
         tma_load_3d(&sm.r[si][0][0], map_r, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
-        tma_load_3d(&sm.x[si][0][0], map_x, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
+        if (XM != XM_SKIP) tma_load_3d(&sm.x[si][0][0], map_x, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
       }
     }
     ++qi;
@@ -485,6 +494,9 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   if (S->stop) return;
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_mark(S, TR_B0);
   const double alpha = S->alpha;
+  // XM_PAIR: c = alpha_{k-1} / beta_{k-1}; cp = c + alpha_k multiplies p_k, -c multiplies z_k
+  const double cpair = (XM == XM_PAIR) ? S->alpha_prev / S->beta : 0.0;
+  const double cp = (XM == XM_PAIR) ? cpair + alpha : alpha;
   if (threadIdx.x == 0)
     for (int s = 0; s < NS_B - 2; s++) issue();
 
@@ -522,27 +534,39 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
         const double q0 = stencil7(pc[e].x, pn[e].x, pm[e].x, dn.x, up.x, pc[e].y, lf, dp.x, ap.x, am.x, P, rw[e]);
         const double q1 = stencil7(pc[e].y, pn[e].y, pm[e].y, dn.y, up.y, rt, pc[e].x, dp.y, ap.y, am.y, P, rw[e]);
         const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[so][r - 1][2 * t.lane]);
-        const double2 xv = *reinterpret_cast<const double2 *>(&sm.x[so][r - 1][2 * t.lane]);
-        double2 rn, xn;
-        rn.x = fma(-alpha, q0, rv.x);
-        rn.y = fma(-alpha, q1, rv.y);
-        xn.x = fma(alpha, pc[e].x, xv.x);
-        xn.y = fma(alpha, pc[e].y, xv.y);
+        double2 rn, xn;  // rn: the stored vector after the update (PC1: z, PC2: r)
+        if (XM != XM_SKIP) {
+          const double2 xv = *reinterpret_cast<const double2 *>(&sm.x[so][r - 1][2 * t.lane]);
+          if (XM == XM_PAIR) {
+            xn.x = fma(cp, pc[e].x, fma(-cpair, rv.x, xv.x));
+            xn.y = fma(cp, pc[e].y, fma(-cpair, rv.y, xv.y));
+          } else {
+            xn.x = fma(alpha, pc[e].x, xv.x);
+            xn.y = fma(alpha, pc[e].y, xv.y);
+          }
+        }
         if (USE_Z) {
+          rn.x = fma(-alpha, q0, rv.x);
+          rn.y = fma(-alpha, q1, rv.y);
           acc_rr += (t.st0 ? rn.x * rn.x : 0.0) + (t.st1 ? rn.y * rn.y : 0.0);
         } else {
+          // z_{k+1} = z_k - alpha D^-1 q;  r_{k+1} = D z_{k+1}
           const DiagRow d = diag_row(P, rw[e]);
-          const double z0 = jacobi(rn.x, diag_at(dp.x, d, ap.x, am.x));
-          const double z1 = jacobi(rn.y, diag_at(dp.y, d, ap.y, am.y));
-          acc_rz += (t.st0 ? rn.x * z0 : 0.0) + (t.st1 ? rn.y * z1 : 0.0);
-          acc_rr += (t.st0 ? rn.x * rn.x : 0.0) + (t.st1 ? rn.y * rn.y : 0.0);
+          const double d0 = diag_at(dp.x, d, ap.x, am.x), d1 = diag_at(dp.y, d, ap.y, am.y);
+          rn.x = fma(-alpha, jacobi(q0, d0), rv.x);
+          rn.y = fma(-alpha, jacobi(q1, d1), rv.y);
+          const double s0 = d0 * rn.x, s1 = d1 * rn.y;
+          acc_rz += (t.st0 ? s0 * rn.x : 0.0) + (t.st1 ? s1 * rn.y : 0.0);
+          acc_rr += (t.st0 ? s0 * s0 : 0.0) + (t.st1 ? s1 * s1 : 0.0);
         }
         store_pair(g_w + t.rowoff[e], t, G.np, rn, true);
-        if (t.st0 && t.st1) {
-          __stcs(reinterpret_cast<double2 *>(g_x + t.rowoff[e]), xn);
-        } else {
-          if (t.st0) g_x[t.rowoff[e]] = xn.x;
-          if (t.st1) g_x[t.rowoff[e] + 1] = xn.y;
+        if (XM != XM_SKIP) {
+          if (t.st0 && t.st1) {
+            __stcs(reinterpret_cast<double2 *>(g_x + t.rowoff[e]), xn);
+          } else {
+            if (t.st0) g_x[t.rowoff[e]] = xn.x;
+            if (t.st1) g_x[t.rowoff[e] + 1] = xn.y;
+          }
         }
       }
       g_w += PL;
@@ -580,13 +604,33 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
 }
 
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
-    k_pass_a_pc1(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_a_body<false>(T, A, parity); }
+    k_pass_a(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_a_body<false>(T, A, parity); }
+// diagnostic instantiation: also stores q = A p_k into A.q_probe (pot3d_probe_pass_a)
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
-    k_pass_a_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_a_body<true>(T, A, parity); }
+    k_pass_a_probe(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_a_body<true>(T, A, parity); }
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
-    k_pass_b_pc1(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_b_body<false>(T, A, parity); }
+    k_pass_b_pc1_even(const __grid_constant__ TMaps T, PassArgs A, int parity) {
+  pass_b_body<false, XM_SKIP>(T, A, parity);
+}
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
-    k_pass_b_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_b_body<true>(T, A, parity); }
+    k_pass_b_pc1_odd(const __grid_constant__ TMaps T, PassArgs A, int parity) {
+  pass_b_body<false, XM_PAIR>(T, A, parity);
+}
+__global__ void __launch_bounds__(NTHREADS, PASS_MINB)
+    k_pass_b_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_b_body<true, XM_EVERY>(T, A, parity); }
+
+// PC1 after the loop: x += alpha_K p_K when the last iteration K was even (its x
+// update was deferred to the pair that never came, A23)
+__global__ void k_x_finish(Grid G, const Scalars *S, double *x, const double *p) {
+  const double alpha = S->alpha;
+  const long long n = (long long)G.nr_loc * G.plane;
+  double *xs = x + G.plane;
+  const double *ps = p + G.plane;
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+    const int col = (int)(c % G.PK);
+    if (col >= COFF && col < G.np + COFF) xs[c] = fma(alpha, ps[c], xs[c]);
+  }
+}
 
 // ghost columns of shells [il0, il0 + n): physical 0 <- k = np-1, physical np+1 <- k = 0
 __global__ void k_fix_ghost_cols(Grid G, double *a, int il0, int n) {

@@ -28,6 +28,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <string>
+
 #include "device_common.cuh"
 
 namespace pot3d {
@@ -586,10 +588,14 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
     *out = P;
     return -1;
   }
+  // the attribute is per function, shared by every context of the process: only raise it
+  // (a smaller context created later must not shrink a larger one's allowance)
+  static int nbmax_set = 0;
+  nbmax_set = std::max(nbmax_set, P->nbmax);
   if (cudaFuncSetAttribute(k_sweep4<SW_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(Sw4<SW_FWD>::SMEM + 16 * P->nbmax)) != cudaSuccess ||
+                           (int)(Sw4<SW_FWD>::SMEM + 16 * nbmax_set)) != cudaSuccess ||
       cudaFuncSetAttribute(k_sweep4<SW_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(Sw4<SW_BWD>::SMEM + 16 * P->nbmax)) != cudaSuccess) {
+                           (int)(Sw4<SW_BWD>::SMEM + 16 * nbmax_set)) != cudaSuccess) {
     *out = P;
     return -1;
   }
@@ -662,6 +668,8 @@ int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host)
 }
 
 // z = M^-1 r; returns the number of kernels launched (memsets excluded) or -1.
+static thread_local std::string g_pc2_err;
+
 int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, double *partials,
               int finalize, double *local_sum, cudaStream_t s, bool iteration, const PeerTab *peers) {
   const int pred = iteration ? 1 : 0;
@@ -679,9 +687,15 @@ int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, 
   const Grid &G = P->G;
   k_pc2_ghost<<<(unsigned)std::min<long long>(((long long)G.nr_loc * G.nt + 255) / 256, 4096), 256, 0,
                 s>>>(G, z, S, pred);
-  if (cudaGetLastError() != cudaSuccess) return -1;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_pc2_err = std::string("PC2 sweep launch: ") + cudaGetErrorString(e);
+    return -1;
+  }
   return 3;
 }
+
+const char *pc2_last_error() { return g_pc2_err.c_str(); }
 
 // flags of the last sweeps (1: pivot breakdown, 2: handoff protocol error); a
 // protocol error re-arms every edge slot so the next solve starts clean

@@ -94,6 +94,7 @@ struct Scalars {
   int pend_b;        // peer-memory PC1: pass B posted its sums; the next edge-shell kernel
                      // finalises them (convergence test, beta) before it builds p_k
   unsigned long long *trace;  // POT3D_TRACE: [64 iterations][16] %globaltimer marks, or null
+  long long hist_len;         // entries of the residual-history buffer (writes beyond are dropped)
 };
 
 // ---- peer-memory exchange between the rank processes (CUDA IPC over NVLink) ----
@@ -155,21 +156,21 @@ __host__ __device__ inline long long pidx(const Grid &g, int j, int k) {
 
 // TMA descriptors of the cell arrays (host-encoded, passed __grid_constant__).
 struct TMaps {
-  CUtensorMap src_h;    // pass A source: r (PC1) or z (PC2), haloed box {SROW, TR, 1}
+  CUtensorMap src_h;    // pass A source: z (PC1: the D^-1 r buffer, PC2: the sweeps' z), haloed box
   CUtensorMap p_h[2];   // P[0], P[1], haloed box
-  CUtensorMap r_i;      // r, interior box {TKB, TJ, 1}
+  CUtensorMap r_i;      // pass B: z (PC1) / r (PC2), interior box {TKB, TJ, 1}
   CUtensorMap x_i;      // x, interior box {TKB, TJ, 1}
 };
 
 
-// Arguments of the fused passes (kernels.cu, k_pass<PASS_A, USE_Z>).
+// Arguments of the fused passes (passes.cu).
 struct PassArgs {
   Grid G;
   Metrics M;
   Scalars *S;
-  const double *r;      // A: r (read, PC1)      B: r (read)
-  double *r_out;        // B: r (write, same buffer)
-  const double *z;      // A (PC2): stored z = M^-1 r
+  const double *r;      // B: the stored residual vector (PC1: z = D^-1 r, PC2: r)
+  double *r_out;        // B: its update (same buffer)
+  const double *z;      // A: stored z = M^-1 r (PC1: the same buffer as r)
   const double *p_old;  // A
   double *p_new;        // A: write, B: read
   double *x;            // A
@@ -180,6 +181,7 @@ struct PassArgs {
   const PeerTab *peers; // nranks > 1 with peer memory: mailbox / ghost-shell exchange
   int fold;             // peer memory, PC1: pass B posts its sums and leaves their
                         // finalisation (convergence, beta) to the next edge-shell kernel
+  double *q_probe;      // k_pass_a_probe only: q = A p_k (cell layout)
 };
 
 // Arguments of the field kernels (a11).
@@ -202,9 +204,12 @@ __global__ void k_metrics(int nr, int nt, int np, int bc, const double *rf, cons
                           double *apm, double *rc, double *drh, double *tc, double *dth,
                           double *st, double *dph, double *vr);
 // parity: P[parity] is p_{k-1}, P[parity^1] receives p_k
-__global__ void k_pass_a_pc1(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a3 (+a8)
-__global__ void k_pass_a_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a3
-__global__ void k_pass_b_pc1(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a7 + a8
+__global__ void k_pass_a(const __grid_constant__ TMaps T, PassArgs A, int parity);        // a3
+__global__ void k_pass_a_probe(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a3 + q out
+// PC1 pass B (a7 + a8): even iterations leave x alone, odd ones apply the pair update (A23)
+__global__ void k_pass_b_pc1_even(const __grid_constant__ TMaps T, PassArgs A, int parity);
+__global__ void k_pass_b_pc1_odd(const __grid_constant__ TMaps T, PassArgs A, int parity);
+__global__ void k_x_finish(Grid G, const Scalars *S, double *x, const double *p);
 __global__ void k_pass_b_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity);  // a7
 // ghost columns (physical 0 and np+1) of shells [il0, il0 + n) from the interior
 __global__ void k_fix_ghost_cols(Grid G, double *a, int il0, int n);
@@ -224,7 +229,7 @@ __global__ void k_gauge_sums(Grid G, Metrics M, const double *vr, const double *
                              double *partials, double *local_sum);
 __global__ void k_gauge_shift(Grid G, double *x, const double *gathered, int nranks);
 __global__ void k_transpose(int ni, int nt, int np, long long stride_i, int PK, int coff,
-                            const double *src, double *dst, int to_dev);
+                            const double *src, double *dst, int to_dev, int ld);
 __global__ void k_field_r(FieldArgs F);
 __global__ void k_field_t(FieldArgs F);
 __global__ void k_field_p(FieldArgs F);
@@ -253,5 +258,6 @@ void pc2_destroy(Pc2 *P, void (*fr)(void *, void *), void *actx);
 int pc2_status(Pc2 *P, cudaStream_t s);
 size_t pc2_bytes(const Pc2 *P);
 int pc2_kernels_per_apply(const Pc2 *P);
+const char *pc2_last_error();
 
 }  // namespace pot3d

@@ -31,7 +31,7 @@ PC2_FELL_BACK = 2
 STATUS_NAMES = {0: "ok", 1: "not_converged", 2: "pc2_fell_back", -1: "invalid", -2: "cuda",
                 -3: "nccl", -4: "indefinite", -5: "oom", -6: "state"}
 
-EXPORTS = ["pot3d_setup", "pot3d_set_br0", "pot3d_solve", "pot3d_field", "pot3d_apply",
+EXPORTS = ["pot3d_setup", "pot3d_set_br0", "pot3d_solve", "pot3d_field", "pot3d_apply", "pot3d_apply_fused", "pot3d_kernel_trace",
            "pot3d_precond", "pot3d_history", "pot3d_info", "pot3d_profile",
            "pot3d_profile_iteration", "pot3d_trace_enable", "pot3d_kernel_times",
            "pot3d_nccl_unique_id",
@@ -59,7 +59,8 @@ class _Runtime(ctypes.Structure):
                 ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p),
                 ("alloc", _ALLOC), ("free", _FREE), ("alloc_ctx", ctypes.c_void_p),
                 ("pc2_blocks", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("unroll", ctypes.c_int32)]
+                ("unroll", ctypes.c_int32), ("loopback_slabs", ctypes.c_int32),
+                ("variant", ctypes.c_int32)]
 
 
 class _Info(ctypes.Structure):
@@ -98,6 +99,7 @@ def library(build_if_missing: bool = True):
     L.pot3d_field.argtypes = [vp, vp, vp, vp]
     L.pot3d_apply.argtypes = [vp, vp, vp]
     L.pot3d_precond.argtypes = [vp, vp, vp]
+    L.pot3d_apply_fused.argtypes = [vp, vp, vp, ctypes.c_int32]
     L.pot3d_history.argtypes = [vp, vp, ctypes.c_int64]
     L.pot3d_history.restype = ctypes.c_int64
     L.pot3d_info.argtypes = [vp, ctypes.POINTER(_Info)]
@@ -105,6 +107,7 @@ def library(build_if_missing: bool = True):
     L.pot3d_profile_iteration.argtypes = [vp, ctypes.c_int32, d, ctypes.c_char_p, ctypes.c_int32]
     L.pot3d_trace_enable.argtypes = [vp, ctypes.c_int32]
     L.pot3d_kernel_times.argtypes = [vp, d, d, ctypes.POINTER(ctypes.c_int32)]
+    L.pot3d_kernel_trace.argtypes = [vp, vp, vp, vp, ctypes.c_int32]
     L.pot3d_nccl_unique_id.argtypes = [vp]
     L.pot3d_destroy.argtypes = [vp]
     L.pot3d_last_error.argtypes = [vp]
@@ -189,7 +192,11 @@ class Pot3d:
 
     def __init__(self, r_faces, t_faces, p_faces, br0, bc=SOURCE_SURFACE, pc=PC1, *, rank=0,
                  nranks=1, nccl_id: bytes | None = None, stream=None, pc2_blocks=1, device=None,
-                 unroll=32, torch_allocator=True):
+                 unroll=32, torch_allocator=True, loopback_slabs=0, variant=0):
+        """loopback_slabs = k > 1 (single process): the grid is split into k r-slabs on
+        this one device, exchanging halos and reductions through the multi-GPU
+        peer-memory kernels (include/pot3d.h); arrays are then the whole grid.
+        variant: 0 standard PCG, 1 single-reduction CG1."""
         import torch
 
         if not torch.cuda.is_available():
@@ -235,6 +242,8 @@ class Pot3d:
             self._cb = (_ALLOC(_alloc), _FREE(_free))
             rt.alloc, rt.free = self._cb
         rt.pc2_blocks = pc2_blocks
+        rt.loopback_slabs = int(loopback_slabs)
+        rt.variant = int(variant)
         rt.device = dev
         rt.unroll = unroll
         p_br, keep = _ptr(br0)
@@ -292,10 +301,12 @@ class Pot3d:
         self._check(self._L.pot3d_field(self._ctx, _ptr(br)[0], _ptr(bt)[0], _ptr(bp)[0]))
         return br, bt, bp
 
-    def apply(self, x, out="numpy"):
+    def apply(self, x, out="numpy", which=0):
+        """y = A x through the loop's pass B (which=0), D^-1 A x through PC1's
+        pass B (which=1) or A x from pass A's stencil (which=2)."""
         px, keep = _ptr(x)
         y = self._out((self.np, self.nt, self.nr_loc), out)
-        self._check(self._L.pot3d_apply(self._ctx, px, _ptr(y)[0]))
+        self._check(self._L.pot3d_apply_fused(self._ctx, px, _ptr(y)[0], int(which)))
         return y
 
     def precond(self, r, out="numpy"):
@@ -314,6 +325,14 @@ class Pot3d:
         a, b, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
         self._check(self._L.pot3d_kernel_times(self._ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
         return a.value, b.value, n.value
+
+    def kernel_trace(self):
+        """(iteration index, pass A us, pass B us) arrays over the last <= 64 loop
+        iterations of the last solve (pot3d_kernel_trace)."""
+        it = np.zeros(64, dtype=np.int64)
+        ua, ub = np.zeros(64), np.zeros(64)
+        n = self._check(self._L.pot3d_kernel_trace(self._ctx, it.ctypes.data, ua.ctypes.data, ub.ctypes.data, 64))
+        return it[:n], ua[:n], ub[:n]
 
     def history(self, n):
         h = np.empty(int(n), dtype=np.float64)
