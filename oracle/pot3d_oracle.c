@@ -272,9 +272,15 @@ typedef struct {
   int64_t *col;
   double *val;
   int64_t *diagpos;
+  double *a0;  /* ORC_ILU_DFORM only: A's values on the pattern */
 } orc_csr;
 
-static void csr_free(orc_csr *c) { free(c->rowptr); free(c->col); free(c->val); free(c->diagpos); }
+static void csr_free(orc_csr *c) {
+  free(c->rowptr); free(c->col); free(c->val); free(c->diagpos);
+#ifdef ORC_ILU_DFORM
+  free(c->a0);
+#endif
+}
 
 /* dia_to_csr restricted to one r-slab block [i0,i1):
  * couplings leaving the block, and the periodic phi wrap (a matrix-free BC,
@@ -289,6 +295,7 @@ static void block_csr(int nr, int nt, int np, const double *bands, int i0, int i
   c->rowptr = malloc(sizeof(int64_t) * (n + 1));
   c->col = malloc(sizeof(int64_t) * n * 7);
   c->val = malloc(sizeof(double) * n * 7);
+  c->a0 = NULL;
   c->diagpos = malloc(sizeof(int64_t) * n);
   int64_t nnz = 0;
   for (int k = 0; k < np; k++)
@@ -345,6 +352,22 @@ static int ilu0_ikj(orc_csr *c) {
  * "standard algorithm ... not vectorizable"). */
 static void lusolve(const orc_csr *c, const double *r, double *z) {
   const int64_t n = c->n;
+#ifdef ORC_ILU_DFORM
+  /* the same (LU)^-1 in D-ILU form (tools/oracle_spread.py only): with L = I + A_L D^-1,
+   * U = D + A_U, D = diag(U): w = D^-1 (r - A_L w), z = w - D^-1 A_U z -- an equally
+   * valid evaluation order; a0 holds A's values on the pattern */
+  for (int64_t i = 0; i < n; i++) {
+    double s = r[i];
+    for (int64_t p = c->rowptr[i]; p < c->diagpos[i]; p++) s -= c->a0[p] * z[c->col[p]];
+    z[i] = s * (1.0 / c->val[c->diagpos[i]]);
+  }
+  for (int64_t i = n - 1; i >= 0; i--) {
+    double s = 0.0;
+    for (int64_t p = c->diagpos[i] + 1; p < c->rowptr[i + 1]; p++) s += c->a0[p] * z[c->col[p]];
+    z[i] -= (1.0 / c->val[c->diagpos[i]]) * s;
+  }
+  return;
+#endif
   for (int64_t i = 0; i < n; i++) {
     double s = r[i];
     for (int64_t p = c->rowptr[i]; p < c->diagpos[i]; p++) s -= c->val[p] * z[c->col[p]];
@@ -419,6 +442,13 @@ static int pc_build(orc_pc *M, int pc, int nblocks, int nr, int nt, int np, cons
     int i0, i1;
     slab_bounds(nr, M->nblocks, b, &i0, &i1);
     block_csr(nr, nt, np, bands, i0, i1, &M->blocks[b]);
+#ifdef ORC_ILU_DFORM
+    {
+      const int64_t nnz = M->blocks[b].rowptr[M->blocks[b].n];
+      M->blocks[b].a0 = malloc(sizeof(double) * nnz);
+      memcpy(M->blocks[b].a0, M->blocks[b].val, sizeof(double) * nnz);
+    }
+#endif
     if (ilu0_ikj(&M->blocks[b])) return -2;
     if (M->blocks[b].n > maxn) maxn = M->blocks[b].n;
   }
@@ -700,6 +730,7 @@ int orc_ilu0_csr(int64_t n, const int64_t *rowptr, const int64_t *col, double *v
   orc_csr c;
   c.n = n;
   c.rowptr = (int64_t *)rowptr; c.col = (int64_t *)col; c.val = val;
+  c.a0 = NULL;
   c.diagpos = malloc(sizeof(int64_t) * n);
   for (int64_t i = 0; i < n; i++) {
     c.diagpos[i] = -1;

@@ -27,6 +27,7 @@ struct pot3d_ctx {
   // problem
   int nr = 0, nt = 0, np = 0, bc = 0, pc_req = 1, pc = 1;
   int rank = 0, nranks = 1, pc2_blocks = 1, unroll = 32;
+  int variant = 0;    // 0 standard PCG, 1 single-reduction CG1 (cg1.cu)
   int nchunks_b = 1;  // r-chunks of pass B (G.nchunks: pass A)
   bool pdl = true;    // programmatic dependent launch for the loop kernels (POT3D_PDL=0: off)
   int edge_blocks = 148 * 4;  // grid of the edge-shell kernel (POT3D_EDGE_BLOCKS)
@@ -64,6 +65,8 @@ struct pot3d_ctx {
   double *poles = nullptr;
   Pc2 *pc2 = nullptr;
   TMaps tmaps{};
+  Cg1Maps cmaps{};          // CG1: U[0] = r, U[1] = P[1], p = P[0], s = s_cg
+  double *s_cg = nullptr;
   // peer-memory exchange (nranks > 1): P[0], P[1] and the mailbox are cudaMalloc'd
   // (IPC-exportable) and mapped into the neighbours' / all ranks' address spaces
   bool xfer_want = false, xfer = false;
@@ -85,6 +88,7 @@ struct pot3d_ctx {
   // ranks 0..k-1 of a peer-memory exchange wired with plain device pointers
   std::vector<pot3d_ctx *> slabs;
   bool member = false;  // a slab context of a loopback group (no NCCL)
+  std::vector<pot3d_ctx *> *group = nullptr;  // member: the group's slab list
   // state
   bool solved = false;
   int64_t last_iters = 0;
@@ -412,6 +416,13 @@ int make_maps(pot3d_ctx *ctx) {
   TRY(make_map(ctx, &ctx->tmaps.p_h[1], ctx->P[1], SROW, TR));
   TRY(make_map(ctx, &ctx->tmaps.r_i, ctx->r, TKB, TJ));
   TRY(make_map(ctx, &ctx->tmaps.x_i, ctx->x, TKB, TJ));
+  if (ctx->variant == 1) {
+    TRY(make_map(ctx, &ctx->cmaps.u_h[0], ctx->r, SROW, TR));
+    TRY(make_map(ctx, &ctx->cmaps.u_h[1], ctx->P[1], SROW, TR));
+    TRY(make_map(ctx, &ctx->cmaps.p_i, ctx->P[0], TKB, TJ));
+    TRY(make_map(ctx, &ctx->cmaps.s_i, ctx->s_cg, TKB, TJ));
+    TRY(make_map(ctx, &ctx->cmaps.x_i, ctx->x, TKB, TJ));
+  }
   return 0;
 }
 
@@ -475,7 +486,95 @@ static StepTimer *g_timer = nullptr;
 // q+1 of any, so every wait of the exchange protocol (halo flags, mailboxes) is on
 // work that an earlier launch of the same stream already finished.
 using Step = std::function<int()>;
+// ---------------------------------------------------------------------------
+// CG1 (single-reduction PCG, cg1.cu): per iteration K1 (vector update, u from
+// U[parity] into U[parity^1]), the halo of the new u, K2 (w = A u and the three
+// inner products), one reduction.  A loopback slab copies its edge shells into its
+// siblings' ghost shells and gathers their sums with device copies; a rank process
+// uses NCCL (send/recv, all-gather).
+// ---------------------------------------------------------------------------
+double *cg1_u(pot3d_ctx *c, int b) { return b ? c->P[1] : c->r; }
+
+Cg1Args cg1_args(pot3d_ctx *ctx, int init) {
+  Cg1Args a{};
+  a.G = ctx->G;
+  a.M = ctx->M;
+  a.S = ctx->S;
+  a.u[0] = cg1_u(ctx, 0);
+  a.u[1] = cg1_u(ctx, 1);
+  a.p = ctx->P[0];
+  a.s = ctx->s_cg;
+  a.x = ctx->x;
+  a.partials = ctx->partials;
+  a.hist = ctx->hist;
+  a.local_sum = ctx->local_sum;
+  a.finalize = (ctx->nranks == 1) ? 1 : 0;
+  a.init = init;
+  return a;
+}
+
+// the steps of one CG1 iteration (parity: u is read from U[parity]); init: only the
+// dots of u_0 (alpha_0) from U[0]
+std::vector<Step> cg1_steps(pot3d_ctx *ctx, int parity, bool init) {
+  std::vector<Step> st;
+  const Grid &G = ctx->G;
+  const int b = init ? 0 : (parity ^ 1);  // the u the dots read
+  if (!init) {
+    st.push_back([=]() -> int {
+      Cg1Args a = cg1_args(ctx, 0);
+      a.G.nchunks = ctx->nchunks_b;
+      CK(launch_k(ctx->pdl, parity ? k_cg1_update_odd : k_cg1_update_even, dim3(G.ntj * G.ntk, ctx->nchunks_b),
+                  dim3(NTHREADS), SMEM_C1, ctx->stream, ctx->cmaps, a, parity));
+      MARK("cg1_update");
+      ctx->n_enq++;
+      return 0;
+    });
+  }
+  if (ctx->nranks > 1) {  // the halo of the u the dots (and the next update) read
+    st.push_back([=]() -> int {
+      if (!ctx->group) return halo_exchange(ctx, cg1_u(ctx, b));
+      const std::vector<pot3d_ctx *> &M = *ctx->group;
+      const int q = ctx->rank;
+      const size_t bytes = (size_t)G.plane * sizeof(double);
+      if (q > 0)
+        CK(cudaMemcpyAsync(cg1_u(M[q - 1], b) + sidx(M[q - 1]->G, M[q - 1]->G.nr_loc), cg1_u(ctx, b) + sidx(G, 0),
+                           bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      if (q + 1 < (int)M.size())
+        CK(cudaMemcpyAsync(cg1_u(M[q + 1], b) + sidx(M[q + 1]->G, -1), cg1_u(ctx, b) + sidx(G, G.nr_loc - 1),
+                           bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      return 0;
+    });
+  }
+  st.push_back([=]() -> int {
+    Cg1Args a = cg1_args(ctx, init ? 1 : 0);
+    CK(launch_k(ctx->pdl, k_cg1_dots, dim3(G.ntj * G.ntk, G.nchunks), dim3(NTHREADS), SMEM_C2, ctx->stream,
+                ctx->cmaps, a, b));
+    MARK("cg1_dots");
+    ctx->n_enq++;
+    return 0;
+  });
+  if (ctx->nranks > 1) {  // one reduction: every rank's (gamma, delta, ||r||^2) in rank order
+    st.push_back([=]() -> int {
+      if (!ctx->group) {
+        NK(ncclAllGather(ctx->local_sum, ctx->gathered, 4, ncclDouble, ctx->comm, ctx->stream));
+      } else {
+        const std::vector<pot3d_ctx *> &M = *ctx->group;
+        for (size_t r = 0; r < M.size(); r++)
+          CK(cudaMemcpyAsync(ctx->gathered + 4 * r, M[r]->local_sum, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+      }
+      CK(launch_k(ctx->pdl, k_finalize_cg1, dim3(1), dim3(1), 0, ctx->stream, ctx->S, (const double *)ctx->gathered,
+                  ctx->nranks, init ? (double *)nullptr : ctx->hist, init ? 1 : 0));
+      MARK("cg1_finalize");
+      ctx->n_enq++;
+      return 0;
+    });
+  }
+  return st;
+}
+
 std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
+  if (ctx->variant == 1) return cg1_steps(ctx, parity, false);
   std::vector<Step> st;
   const Grid &G = ctx->G;
   PassArgs a = make_args(ctx, parity);
@@ -568,6 +667,10 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
 }
 
 int enqueue_iteration(pot3d_ctx *ctx, int parity) {
+  if (ctx->variant == 1) {
+    for (auto &f : cg1_steps(ctx, parity, false)) TRY(f());
+    return 0;
+  }
   const Grid &G = ctx->G;
   PassArgs a = make_args(ctx, parity);
   dim3 grd(G.ntj * G.ntk, G.nchunks);
@@ -853,6 +956,7 @@ int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit) {
   CK(cudaMemsetAsync(ctx->r, 0, cells * sizeof(double), s));
   CK(cudaMemsetAsync(ctx->P[0], 0, cells * sizeof(double), s));
   CK(cudaMemsetAsync(ctx->P[1], 0, cells * sizeof(double), s));
+  if (ctx->s_cg) CK(cudaMemsetAsync(ctx->s_cg, 0, cells * sizeof(double), s));
   if (G.i0 == 0) {
     CK(cudaMemcpyAsync(ctx->r + sidx(G, 0), ctx->bshell, G.plane * sizeof(double),
                        cudaMemcpyDeviceToDevice, s));
@@ -984,6 +1088,18 @@ int solve_run(pot3d_ctx *h, std::vector<pot3d_ctx *> &M, double rtol, int64_t ma
   for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit));
   if (M.size() > 1 || M[0]->nranks > 1) TRY(gather_all(M));
   for (pot3d_ctx *m : M) TRY(solve_init_end(m));
+  if (M[0]->variant == 1) {  // CG1: w_0 = A u_0, delta_0 -> alpha_0 (the same steps, phase by phase)
+    std::vector<std::vector<Step>> st;
+    for (pot3d_ctx *m : M) st.push_back(cg1_steps(m, 0, true));
+    for (size_t q = 0; q < st[0].size(); q++)
+      for (size_t k = 0; k < st.size(); k++) {
+        int rc = st[k][q]();
+        if (rc) {
+          h->err = M[k]->err;
+          return rc;
+        }
+      }
+  }
   pot3d_ctx *m0 = M[0];
   CK(cudaMemcpyAsync(m0->hS, m0->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -1115,7 +1231,8 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   // algorithmic bytes
   const int64_t cells = (int64_t)ctx->G.nr_loc * ctx->nt * ctx->np;
   // PC1: pass A 24 + pass B 24 (even) / 40 (odd) = 56 B/cell on average (A23)
-  info->bytes_per_iter = (ctx->pc == 2 ? 120 : 56) * cells;
+  // CG1: update 48 (even) / 64 (odd) + dots 8 = 64 B/cell on average
+  info->bytes_per_iter = (ctx->pc == 2 ? 120 : (ctx->variant == 1 ? 64 : 56)) * cells;
   info->device_bytes = (int64_t)ctx->dev_bytes;
   info->kernel_launches = ctx->n_launch;
   info->exchange = ctx->nranks == 1 ? 0 : (ctx->xfer ? 2 : 1);
@@ -1247,6 +1364,11 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   ctx->rank = R.rank;
   ctx->nranks = R.nranks < 1 ? 1 : R.nranks;
   ctx->pc2_blocks = R.pc2_blocks < 1 ? 1 : R.pc2_blocks;
+  ctx->variant = R.variant;
+  if (ctx->variant != 0 && (ctx->variant != 1 || pc != POT3D_PC1)) {
+    ctx->err = "variant must be 0 (PCG) or 1 (CG1, PC1 only)";
+    return fail(POT3D_ERR_INVALID);
+  }
   ctx->unroll = R.unroll > 0 ? (R.unroll + 1) / 2 * 2 : 32;
   ctx->ualloc = R.alloc;
   ctx->ufree = R.free;
@@ -1295,7 +1417,7 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   G.PK = round_up(np + COFF + 1, 16);  // physical columns: [ghost np-1][0..np-1][ghost 0][pads]
   G.plane = (long long)nt * G.PK;
   G.ntj = (nt + TJ - 1) / TJ;
-  G.ntk = (np + TK - 1) / TK;
+  G.ntk = (np + 1 + TK - 1) / TK;  // tiles of columns 64t-1 .. 64t+62 cover -1 .. np-1
   {
     const void *fa[2] = {(const void *)k_pass_a, (const void *)k_pass_a_probe};
     const void *fb[3] = {(const void *)k_pass_b_pc1_even, (const void *)k_pass_b_pc1_odd,
@@ -1307,6 +1429,12 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
         return fail(POT3D_ERR_CUDA);
       }
     }
+  }
+  if (cudaFuncSetAttribute(k_cg1_update_even, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_C1) ||
+      cudaFuncSetAttribute(k_cg1_update_odd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_C1) ||
+      cudaFuncSetAttribute(k_cg1_dots, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_C2)) {
+    ctx->err = "cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed (CG1)";
+    return fail(POT3D_ERR_CUDA);
   }
   { int rc = choose_chunks(ctx); if (rc) return fail(rc); }
 
@@ -1360,8 +1488,9 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   ctx->partials_len = 4 * (size_t)std::max<long long>(
       (long long)G.ntj * G.ntk * (std::max(G.nchunks, ctx->nchunks_b) + 3), 65536);
   DA(ctx->partials, ctx->partials_len);
-  DA(ctx->local_sum, 2);
-  DA(ctx->gathered, 2 * (size_t)ctx->nranks + 2);
+  DA(ctx->local_sum, 4);
+  DA(ctx->gathered, 4 * (size_t)ctx->nranks + 4);  // 2 (PCG) or 4 (CG1) doubles per rank
+  if (ctx->variant == 1) DA(ctx->s_cg, cells);
   DA(ctx->poles, 2 * (size_t)G.nr_loc);
 #undef DA
   for (void *p : {(void *)ctx->x, (void *)ctx->r, (void *)ctx->P[0], (void *)ctx->P[1]})
@@ -1486,6 +1615,7 @@ static int setup_group(const pot3d_grid *grid, const double *br0, int32_t outer_
     }
     h->slabs.push_back(m);
   }
+  for (pot3d_ctx *m : h->slabs) m->group = &h->slabs;
   // PC2 breakdown on any slab -> every slab falls back to PC1
   bool fell = false;
   for (pot3d_ctx *m : h->slabs) fell = fell || m->pc != pc;
@@ -1552,7 +1682,7 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
     // PC1 defers the x update of even iterations to the next (odd) pass B (A23): when the
     // last iteration K = iters - 1 was even, x += alpha_K p_K (p_K in P[1]) now
     if (m->pc == 1 && (hs.iter & 1)) {
-      k_x_finish<<<148 * 8, 256, 0, s>>>(m->G, m->S, m->x, m->P[1]);
+      k_x_finish<<<148 * 8, 256, 0, s>>>(m->G, m->S, m->x, m->variant == 1 ? m->P[0] : m->P[1]);
       CK(cudaGetLastError());
       m->n_launch++;
     }
@@ -1781,8 +1911,8 @@ int pot3d_precond(pot3d_ctx *ctx, const double *rin, double *zout) {
 int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_pass_b,
                   double *ms_precond) {
   if (!ctx || iters < 1) return POT3D_ERR_INVALID;
-  if (!ctx->slabs.empty()) {
-    ctx->err = "profiling is per slab context: not available on a loopback group";
+  if (!ctx->slabs.empty() || ctx->variant != 0) {
+    ctx->err = "profiling runs the standard PCG passes of one slab context (not a loopback group, not CG1)";
     return POT3D_ERR_INVALID;
   }
   CK(cudaSetDevice(ctx->device));
@@ -1842,8 +1972,8 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
 
 int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *names, int32_t nmax) {
   if (!ctx || iters < 1 || !ms || !names || nmax < 1) return POT3D_ERR_INVALID;
-  if (!ctx->slabs.empty()) {
-    ctx->err = "profiling is per slab context: not available on a loopback group";
+  if (!ctx->slabs.empty() || ctx->variant != 0) {
+    ctx->err = "profiling runs the standard PCG passes of one slab context (not a loopback group, not CG1)";
     return POT3D_ERR_INVALID;
   }
   CK(cudaSetDevice(ctx->device));

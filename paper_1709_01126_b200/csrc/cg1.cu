@@ -1,0 +1,354 @@
+// cg1.cu -- the single-reduction PCG variant (opt-in:
+// pot3d_runtime.variant = 1), PC1 only.
+//
+// Chronopoulos & Gear (1989), in the form of Ghysels & Vanroose (2014) Alg. 2
+// (oracle/pot3d_oracle.c orc_pcg variant ORC_PCG_CG1 states it step by step):
+//   p = u + beta p;  s = w + beta s;  x += alpha p;  r -= alpha s;
+//   u = M^-1 r;  w = A u;  gamma = r.u, delta = w.u, ||r||^2  (ONE reduction)
+// The paper names the inner products' "collective/synchronous nature" as the
+// scaling limiter; this variant has one global reduction per
+// iteration instead of two.  As in the standard PC1 path the stored residual
+// is u = D^-1 r (reading A22), so r = D u is never stored.
+//
+//   k_cg1_update (K1): w = A u from the staged, haloed u box (U[par]); then per cell
+//       p' = u + beta p, s' = w + beta s, u' = u - alpha D^-1 s' (into U[par^1]),
+//       and on odd iterations x += alpha_{k-1} p_{k-1} + alpha_k p_k with
+//       p_{k-1} = (p' - u) / beta (reading A23).  No reduction.  [48 / 64 B/cell]
+//   k_cg1_dots   (K2): w' = A u' from the staged u' box; gamma = sum D u'^2,
+//       delta = sum w' u', ||r||^2 = sum (D u')^2 -> finalize (alpha, beta,
+//       convergence) in the last block.                                  [8 B/cell]
+// Per iteration 56 B/cell on average + 8 B/cell, one reduction (PCG: 56 B, two).
+#include "pass_common.cuh"
+
+namespace pot3d {
+
+struct SmemC1 {
+  double u[NS_C][TR][SROW];
+  double p[NS_C][TJ][TKB];
+  double s[NS_C][TJ][TKB];
+  double x[NS_C][TJ][TKB];
+  uint64_t bar[NS_C];
+};
+struct SmemC2 {
+  double u[NS_D][TR][SROW];
+  uint64_t bar[NS_D];
+};
+static_assert(sizeof(SmemC1) <= SMEM_C1 && sizeof(SmemC2) <= SMEM_C2, "CG1 shared memory");
+
+// the CG1 scalar updates (one thread), rank-order sums already formed
+__device__ __forceinline__ void finalize_cg1(Scalars *S, double gamma, double delta, double rr, double *hist,
+                                             bool init) {
+  if (init) {  // gamma_0 = r0.u0, delta_0 = (A u0).u0, alpha_0 = gamma_0 / delta_0, beta_0 = 0
+    S->rho = gamma;
+    S->sigma = delta;
+    S->beta = 0.0;
+    if (!(delta > 0.0)) {
+      S->status = -4;
+      S->stop = 1;
+      return;
+    }
+    S->alpha = gamma / delta;
+    return;
+  }
+  const long long it = S->iter + 1;
+  S->iter = it;
+  S->rr = rr;
+  const double rn = sqrt(rr);
+  if (hist && it < S->hist_len) hist[it] = rn / S->bnorm;
+  S->alpha_prev = S->alpha;
+  if (rn <= S->rtol * S->bnorm) {
+    S->stop = 1;
+    S->status = 0;
+    return;
+  }
+  if (it >= S->maxit) {
+    S->stop = 1;
+    S->status = 1;
+    return;
+  }
+  const double beta = gamma / S->rho;
+  const double den = delta - beta * gamma / S->alpha;  // = p.Ap in exact arithmetic
+  S->sigma = den;
+  if (!(den > 0.0)) {
+    S->status = -4;
+    S->stop = 1;
+    return;
+  }
+  S->beta = beta;
+  S->alpha = gamma / den;
+  S->rho = gamma;
+}
+
+__global__ void k_finalize_cg1(Scalars *S, const double *gathered, int nranks, double *hist, int init) {
+  pdl_trigger();
+  pdl_wait();
+  if (S->stop) return;
+  double g = 0.0, d = 0.0, rr = 0.0;
+  for (int r = 0; r < nranks; r++) {
+    g += gathered[4 * r + 0];
+    d += gathered[4 * r + 1];
+    rr += gathered[4 * r + 2];
+  }
+  finalize_cg1(S, g, d, rr, hist, init != 0);
+}
+
+// ---------------------------------------------------------------------------
+// K1: the vector update of one iteration (parity: u is read from U[parity])
+// ---------------------------------------------------------------------------
+template <int XM, bool FAST>
+__device__ __forceinline__ void cg1_update_body(const Cg1Maps &T, const Cg1Args &A, int parity, PassShared &sh) {
+  const Grid &G = A.G;
+  const Metrics &M = A.M;
+  Scalars *S = A.S;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SmemC1 &sm = *reinterpret_cast<SmemC1 *>(smem_raw);
+  TileConst &tcs = sh.tcs;
+  PlaneSm &pls = sh.pls;
+  const TileThread t = tile_thread(G);
+  const int L = t.c1 - t.c0;
+  load_tile_const(tcs, G, M, t.k0);
+  load_planes(pls, M, G.i0 + t.c0 - 1, L + 2);
+  const int cs = 2 + 2 * t.lane;
+  const long long PL = G.plane;
+  const void *map_u = &T.u_h[parity];
+  constexpr unsigned UB = TR * SROW * 8u, IB = TJ * TKB * 8u;
+  RowC rw[RPW];
+#pragma unroll
+  for (int e = 0; e < RPW; e++) rw[e] = row_c(M, min(max(t.j0 - 1 + t.row[e], 0), G.nt - 1));
+  int qi = 0, si = 0;
+  auto issue = [&]() {
+    if (qi <= L + 1) {
+      const int il = t.c0 - 1 + qi;
+      const bool rown = (qi >= 1) && (qi <= L);
+      mbar_arrive_expect_tx(&sm.bar[si], rown ? UB + (XM == XM_PAIR ? 3 : 2) * IB : UB);
+      tma_load_3d(&sm.u[si][0][0], map_u, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
+      if (rown) {
+        tma_load_3d(&sm.p[si][0][0], &T.p_i, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
+        tma_load_3d(&sm.s[si][0][0], &T.s_i, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
+        if (XM == XM_PAIR) tma_load_3d(&sm.x[si][0][0], &T.x_i, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
+      }
+    }
+    ++qi;
+    si = wrap_inc(si, NS_C);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS_C; s++) mbar_init(&sm.bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  if (S->stop) return;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_mark(S, TR_B0);
+  const double alpha = S->alpha, beta = S->beta;
+  const double cpair = (XM == XM_PAIR) ? S->alpha_prev / beta : 0.0;  // alpha_{k-1} / beta_k
+  const double cp = cpair + alpha;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < NS_C - 2; s++) issue();
+
+  const double2 Z2 = make_double2(0.0, 0.0);
+  double2 um[RPW], uc[RPW], un[RPW];
+#pragma unroll
+  for (int e = 0; e < RPW; e++) um[e] = uc[e] = un[e] = Z2;
+  double *g_u = A.u[parity ^ 1] + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: plane c0
+  double *g_p = A.p + (long long)(t.c0 + 1) * PL;
+  double *g_s = A.s + (long long)(t.c0 + 1) * PL;
+  double *g_x = A.x + (long long)(t.c0 + 1) * PL;
+  int st = 0, so = NS_C - 1;
+  unsigned ph = 0;
+  auto st2 = [&](double *a, double2 v) {  // interior store (p, s, x: no ghost columns)
+    if (FAST || (t.st0 && t.st1)) {
+      __stcs(reinterpret_cast<double2 *>(a), v);
+    } else {
+      if (t.st0) a[0] = v.x;
+      if (t.st1) a[1] = v.y;
+    }
+  };
+#pragma unroll 1
+  for (int q = 0; q <= L + 1; q++) {
+    __syncthreads();  // stage (q-2)%NS_C is free
+    if (threadIdx.x == 0) issue();
+    const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
+    const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
+    const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
+    const PlaneC P = plane_at(pls, q >= 1 ? q - 1 : 0);
+    mbar_wait(&sm.bar[st], ph);
+#pragma unroll
+    for (int e = 0; e < RPW; e++) un[e] = *reinterpret_cast<const double2 *>(&sm.u[st][t.row[e]][cs]);
+    if (q >= 2) {
+      const double *sb = &sm.u[so][0][0];
+#pragma unroll
+      for (int e = 0; e < RPW; e++) {
+        if (!t.stencil[e]) continue;
+        const int r = t.row[e];
+        const double *sr = sb + r * SROW + cs;
+        const double2 up = (RPW == 2 && e == 1) ? uc[0] : *reinterpret_cast<const double2 *>(sr - SROW);
+        const double2 dn = (RPW == 2 && e == 0) ? uc[RPW - 1] : *reinterpret_cast<const double2 *>(sr + SROW);
+        const double lf = sr[-1], rt = sr[2];
+        const double w0 = stencil7(uc[e].x, un[e].x, um[e].x, dn.x, up.x, uc[e].y, lf, dp.x, ap.x, am.x, P, rw[e]);
+        const double w1 = stencil7(uc[e].y, un[e].y, um[e].y, dn.y, up.y, rt, uc[e].x, dp.y, ap.y, am.y, P, rw[e]);
+        const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[so][r - 1][2 * t.lane]);
+        const double2 sv = *reinterpret_cast<const double2 *>(&sm.s[so][r - 1][2 * t.lane]);
+        double2 pn, sn, unw;
+        pn.x = fma(beta, pv.x, uc[e].x);
+        pn.y = fma(beta, pv.y, uc[e].y);
+        sn.x = fma(beta, sv.x, w0);
+        sn.y = fma(beta, sv.y, w1);
+        const DiagRow d = diag_row(P, rw[e]);
+        const double d0 = diag_at(dp.x, d, ap.x, am.x), d1 = diag_at(dp.y, d, ap.y, am.y);
+        unw.x = fma(-alpha, jacobi(sn.x, d0), uc[e].x);
+        unw.y = fma(-alpha, jacobi(sn.y, d1), uc[e].y);
+        const long long o = t.rowoff[e];
+        store_pair<FAST>(g_u + o, t, G.np, unw, true);
+        st2(g_p + o, pn);
+        st2(g_s + o, sn);
+        if (XM == XM_PAIR) {
+          const double2 xv = *reinterpret_cast<const double2 *>(&sm.x[so][r - 1][2 * t.lane]);
+          double2 xn;
+          xn.x = fma(cp, pn.x, fma(-cpair, uc[e].x, xv.x));
+          xn.y = fma(cp, pn.y, fma(-cpair, uc[e].y, xv.y));
+          st2(g_x + o, xn);
+        }
+      }
+      g_u += PL;
+      g_p += PL;
+      g_s += PL;
+      g_x += PL;
+    }
+#pragma unroll
+    for (int e = 0; e < RPW; e++) {
+      um[e] = uc[e];
+      uc[e] = un[e];
+    }
+    so = st;
+    st = wrap_inc(st, NS_C);
+    ph ^= (st == 0);
+  }
+  // end of the last block (the dots kernel's griddepcontrol.wait covers this grid's stores)
+  if (threadIdx.x == 0) trace_max(S, TR_B1);
+}
+
+// ---------------------------------------------------------------------------
+// K2: w' = A u' and the three inner products of the single reduction
+// ---------------------------------------------------------------------------
+template <bool FAST>
+__device__ __forceinline__ void cg1_dots_body(const Cg1Maps &T, const Cg1Args &A, int parity, PassShared &sh) {
+  const Grid &G = A.G;
+  const Metrics &M = A.M;
+  Scalars *S = A.S;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SmemC2 &sm = *reinterpret_cast<SmemC2 *>(smem_raw);
+  double *sred = sh.sred;
+  TileConst &tcs = sh.tcs;
+  PlaneSm &pls = sh.pls;
+  const TileThread t = tile_thread(G);
+  const bool m0 = FAST || t.st0, m1 = FAST || t.st1;
+  const int L = t.c1 - t.c0;
+  load_tile_const(tcs, G, M, t.k0);
+  load_planes(pls, M, G.i0 + t.c0 - 1, L + 2);
+  const int cs = 2 + 2 * t.lane;
+  const void *map_u = &T.u_h[parity];
+  constexpr unsigned UB = TR * SROW * 8u;
+  RowC rw[RPW];
+#pragma unroll
+  for (int e = 0; e < RPW; e++) rw[e] = row_c(M, min(max(t.j0 - 1 + t.row[e], 0), G.nt - 1));
+  int qi = 0, si = 0;
+  auto issue = [&]() {
+    if (qi <= L + 1) {
+      mbar_arrive_expect_tx(&sm.bar[si], UB);
+      tma_load_3d(&sm.u[si][0][0], map_u, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, t.c0 + qi);
+    }
+    ++qi;
+    si = wrap_inc(si, NS_D);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS_D; s++) mbar_init(&sm.bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  if (S->stop) return;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_mark(S, TR_A0);
+  if (threadIdx.x == 0)
+    for (int s = 0; s < NS_D - 2; s++) issue();
+  const double2 Z2 = make_double2(0.0, 0.0);
+  double2 um[RPW], uc[RPW], un[RPW];
+#pragma unroll
+  for (int e = 0; e < RPW; e++) um[e] = uc[e] = un[e] = Z2;
+  double ag = 0.0, ad = 0.0, ar = 0.0;
+  int st = 0, so = NS_D - 1;
+  unsigned ph = 0;
+#pragma unroll 1
+  for (int q = 0; q <= L + 1; q++) {
+    __syncthreads();  // stage (q-2)%NS_D is free
+    if (threadIdx.x == 0) issue();
+    const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
+    const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
+    const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
+    const PlaneC P = plane_at(pls, q >= 1 ? q - 1 : 0);
+    mbar_wait(&sm.bar[st], ph);
+#pragma unroll
+    for (int e = 0; e < RPW; e++) un[e] = *reinterpret_cast<const double2 *>(&sm.u[st][t.row[e]][cs]);
+    if (q >= 2) {
+      const double *sb = &sm.u[so][0][0];
+#pragma unroll
+      for (int e = 0; e < RPW; e++) {
+        if (!t.stencil[e]) continue;
+        const int r = t.row[e];
+        const double *sr = sb + r * SROW + cs;
+        const double2 up = (RPW == 2 && e == 1) ? uc[0] : *reinterpret_cast<const double2 *>(sr - SROW);
+        const double2 dn = (RPW == 2 && e == 0) ? uc[RPW - 1] : *reinterpret_cast<const double2 *>(sr + SROW);
+        const double lf = sr[-1], rt = sr[2];
+        const double w0 = stencil7(uc[e].x, un[e].x, um[e].x, dn.x, up.x, uc[e].y, lf, dp.x, ap.x, am.x, P, rw[e]);
+        const double w1 = stencil7(uc[e].y, un[e].y, um[e].y, dn.y, up.y, rt, uc[e].x, dp.y, ap.y, am.y, P, rw[e]);
+        const DiagRow d = diag_row(P, rw[e]);
+        const double r0 = diag_at(dp.x, d, ap.x, am.x) * uc[e].x, r1 = diag_at(dp.y, d, ap.y, am.y) * uc[e].y;
+        ag += (m0 ? r0 * uc[e].x : 0.0) + (m1 ? r1 * uc[e].y : 0.0);
+        ad += (m0 ? w0 * uc[e].x : 0.0) + (m1 ? w1 * uc[e].y : 0.0);
+        ar += (m0 ? r0 * r0 : 0.0) + (m1 ? r1 * r1 : 0.0);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < RPW; e++) {
+      um[e] = uc[e];
+      uc[e] = un[e];
+    }
+    so = st;
+    st = wrap_inc(st, NS_D);
+    ph ^= (st == 0);
+  }
+  double v[3] = {ag, ad, ar}, tot[3];
+  if (grid_sum<3>(v, A.partials, &S->counter[5], sred, tot, pass_bid(G), pass_nb(G)) && threadIdx.x == 0) {
+    trace_mark(S, TR_A1);
+    if (A.finalize) {
+      finalize_cg1(S, tot[0], tot[1], tot[2], A.hist, A.init != 0);
+    } else {
+      A.local_sum[0] = tot[0];
+      A.local_sum[1] = tot[1];
+      A.local_sum[2] = tot[2];
+    }
+  }
+}
+
+#define POT3D_CG1(BODY, ...)                                    \
+  __shared__ PassShared sh;                                     \
+  if (tile_fast(A.G))                                           \
+    BODY<__VA_ARGS__ true>(T, A, parity, sh);                   \
+  else                                                          \
+    BODY<__VA_ARGS__ false>(T, A, parity, sh)
+
+__global__ void __launch_bounds__(NTHREADS, PASS_MINB)
+    k_cg1_update_even(const __grid_constant__ Cg1Maps T, Cg1Args A, int parity) {
+  POT3D_CG1(cg1_update_body, XM_SKIP, );
+}
+__global__ void __launch_bounds__(NTHREADS, PASS_MINB)
+    k_cg1_update_odd(const __grid_constant__ Cg1Maps T, Cg1Args A, int parity) {
+  POT3D_CG1(cg1_update_body, XM_PAIR, );
+}
+__global__ void __launch_bounds__(NTHREADS, PASS_MINB)
+    k_cg1_dots(const __grid_constant__ Cg1Maps T, Cg1Args A, int parity) {
+  POT3D_CG1(cg1_dots_body, );
+}
+
+}  // namespace pot3d

@@ -28,9 +28,7 @@
 // and is unrolled by 3 so stage, slot and register roles are compile-time;
 // the r neighbours of a cell stay in its thread's registers.  One
 // __syncthreads per plane.  Per-block partials are reduced deterministically.
-#include <type_traits>
-
-#include "device_common.cuh"
+#include "pass_common.cuh"
 
 // pass A code-generation switches (tuning variants)
 
@@ -57,172 +55,14 @@ struct SmemB {
 static_assert(sizeof(SmemA) <= SMEM_A, "SMEM_A");
 static_assert(sizeof(SmemB) <= SMEM_B, "SMEM_B");
 static_assert((TR * SROW * 8) % 128 == 0 && (TJ * TKB * 8) % 128 == 0, "TMA boxes 128-B aligned");
-static_assert(TR % RPW == 0 && TKB == 2 * 32 && TK == TKB - 2, "tile geometry");
+static_assert(TR % RPW == 0 && TKB == 2 * 32 && TK == TKB, "tile geometry");
 
-__device__ __forceinline__ void chunk_bounds(const Grid &G, int c, int &c0, int &c1) {
-  if (G.part == 2) {  // the two edge shells
-    c0 = (c == 0) ? 0 : G.nr_loc - 1;
-    c1 = c0 + 1;
-    return;
-  }
-  const int s0 = (G.part == 1) ? 1 : 0, n = (G.part == 1) ? G.nr_loc - 2 : G.nr_loc;
-  int base = n / G.nchunks, rem = n % G.nchunks;
-  c0 = s0 + c * base + (c < rem ? c : rem);
-  c1 = c0 + base + (c < rem ? 1 : 0);
-}
-
-__device__ __forceinline__ int pass_bid(const Grid &G) {
-  return G.blk_off + blockIdx.x + gridDim.x * blockIdx.y;
-}
-__device__ __forceinline__ int pass_nb(const Grid &G) {
-  return G.blk_total > 0 ? G.blk_total : gridDim.x * gridDim.y;
-}
-
-// Column metric factors of the tile per smem index i (logical column k0-3+i,
-// periodic): dp, app, apm.
-struct TileConst {
-  double dp[SROW], app[SROW], apm[SROW];
-};
-
-__device__ __forceinline__ void load_tile_const(TileConst &tc, const Grid &G, const Metrics &M,
-                                                int k0) {
-  for (int i = threadIdx.x; i < SROW; i += blockDim.x) {
-    int k = k0 - 3 + i;
-    k = (k < 0) ? k + G.np : k;
-    k = (k >= G.np) ? (k - G.np) % G.np : k;
-    tc.dp[i] = __ldg(M.dp + k);
-    tc.app[i] = __ldg(M.app + k);
-    tc.apm[i] = __ldg(M.apm + k);
-  }
-}
-
-__device__ __forceinline__ int wrap_inc(int s, int n) { return (s + 1 == n) ? 0 : s + 1; }
-
-// r-metric factors of the chunk's shells (c0-1 .. c1) staged in shared memory once
-// per block, so the per-plane reads are shared-memory broadcasts instead of L2
-// round trips on the plane loop's critical path (choose_chunks keeps every
-// chunk within PLMAX-2 shells).
-constexpr int PLMAX = POT3D_PLMAX;
-struct PlaneSm {
-  double arp[PLMAX], arm[PLMAX], dr[PLMAX], ss[PLMAX];
-};
-__device__ __forceinline__ void load_planes(PlaneSm &ps, const Metrics &M, int ig0, int n) {
-  for (int q = threadIdx.x; q < n && q < PLMAX; q += blockDim.x) {
-    ps.arp[q] = __ldg(M.arp + ig0 + q);
-    ps.arm[q] = __ldg(M.arm + ig0 + q);
-    ps.dr[q] = __ldg(M.dr + ig0 + q);
-    ps.ss[q] = __ldg(M.ss + ig0 + q);
-  }
-}
-// metrics of shell il = c0-1+q
-__device__ __forceinline__ PlaneC plane_at(const PlaneSm &ps, int q) {
-  PlaneC c;
-  c.arp = ps.arp[q];
-  c.arm = ps.arm[q];
-  c.dr = ps.dr[q];
-  c.ss = ps.ss[q];
-  return c;
-}
-
-// (A p)_m = dp_k [g_j (arp (c - p_{i+1}) + arm (c - p_{i-1}) + ss c) + dr (atp (c - p_{j+1})
-//           + atm (c - p_{j-1}))] + dr q_j (app (c - p_{k+1}) + apm (c - p_{k-1}))
-__device__ __forceinline__ double stencil7(double c, double ip, double im, double jp, double jm,
-                                           double kp, double km, double dpk, double appk,
-                                           double apmk, const PlaneC &P, const RowC &R) {
-  return dpk * (R.g * (P.arp * (c - ip) + P.arm * (c - im) + P.ss * c) +
-                P.dr * (R.atp * (c - jp) + R.atm * (c - jm))) +
-         P.dr * R.q * (appk * (c - kp) + apmk * (c - km));
-}
-
-// stencil7 with the r flux shared between consecutive planes: Fu = arp (c - ip) is
-// returned for the next plane, whose lower term arm (c - im) is exactly -Fu
-// (arm_{i+1} == arp_i bitwise, a - b == -(b - a) exactly); Fd = arm (c - im).
-__device__ __forceinline__ double stencil7f(double c, double ip, double Fd, double jp, double jm,
-                                            double kp, double km, double dpk, double appk,
-                                            double apmk, const PlaneC &P, const RowC &R, double &Fu) {
-  Fu = P.arp * (c - ip);
-  return dpk * (R.g * (Fu + Fd + P.ss * c) + P.dr * (R.atp * (c - jp) + R.atm * (c - jm))) +
-         P.dr * R.q * (appk * (c - kp) + apmk * (c - km));
-}
-
-// Per-thread geometry of a tile.
-struct TileThread {
-  int lane, w;
-  int j0, k0, c0, c1;
-  int row[RPW];          // haloed rows w*RPW + e (theta row j0-1+row)
-  bool stencil[RPW];     // interior row inside the grid
-  long long rowoff[RPW]; // j*PK + (k0-1+2*lane) + COFF, row clamped into the grid
-  bool st0, st1;         // element 0/1 is an interior column of this tile inside the grid
-  bool gr0, gr1, gl0, gl1;  // element 0/1 holds k = 0 (right-ghost dup) / k = np-1 (left ghost)
-};
-
-__device__ __forceinline__ TileThread tile_thread(const Grid &G) {
-  TileThread t;
-  t.lane = threadIdx.x & 31;
-  t.w = threadIdx.x >> 5;
-  const int tile = blockIdx.x;
-  t.j0 = (tile % G.ntj) * TJ;
-  t.k0 = (tile / G.ntj) * TK;
-  // part 3: all shells, the two chunks touching a ghost shell scheduled last (their
-  // blocks wait for the neighbours' halo, which meanwhile arrives in peer memory)
-  int cy = blockIdx.y - G.role_rows;
-  if (G.part == 3 && G.nchunks >= 3)
-    cy = (cy < G.nchunks - 2) ? cy + 1 : (cy == G.nchunks - 2 ? 0 : G.nchunks - 1);
-  chunk_bounds(G, cy, t.c0, t.c1);
-  const int k = t.k0 - 1 + 2 * t.lane;  // logical column of element 0
-#pragma unroll
-  for (int e = 0; e < RPW; e++) {
-    const int r = RPW * t.w + e;
-    const int j = t.j0 - 1 + r;
-    const bool jv = (j >= 0) && (j < G.nt);
-    t.row[e] = r;
-    t.stencil[e] = (r >= 1) && (r <= TJ) && jv;
-    t.rowoff[e] = (long long)(jv ? j : t.j0) * G.PK + k + COFF;
-  }
-  t.st0 = (t.lane > 0) && (k < G.np);
-  t.st1 = (t.lane < 31) && (k + 1 < G.np);
-  t.gr0 = t.st0 && (k == 0);
-  t.gr1 = t.st1 && (k + 1 == 0);
-  t.gl0 = t.st0 && (k == G.np - 1);
-  t.gl1 = t.st1 && (k + 1 == G.np - 1);
-  return t;
-}
-
-// Store of a lane's column pair (interior elements only) with the periodic
-// ghost-column duplicates; row_k points at the physical column of element 0.
-__device__ __forceinline__ void store_pair(double *row_k, const TileThread &t, int np, double2 v,
-                                           bool streaming) {
-  if (t.st0 && t.st1) {
-    if (streaming)
-      __stcs(reinterpret_cast<double2 *>(row_k), v);
-    else
-      *reinterpret_cast<double2 *>(row_k) = v;
-  } else {
-    if (t.st0) row_k[0] = v.x;
-    if (t.st1) row_k[1] = v.y;
-  }
-  if (t.gr0) row_k[np] = v.x;        // k = 0 (element 0)    -> physical np+1
-  if (t.gr1) row_k[np + 1] = v.y;    // k = 0 (element 1)    -> physical np+1
-  if (t.gl0) row_k[-np] = v.x;       // k = np-1 (element 0) -> physical 0
-  if (t.gl1) row_k[1 - np] = v.y;    // k = np-1 (element 1) -> physical 0
-}
-
-// A select the compiler cannot turn back into a branch (both operands are
-// computed), so the transform of a plane stays in the step's basic block.
-__device__ __forceinline__ double selp(double a, double b, bool p) {
-  double r;
-  asm("{.reg .pred q; setp.ne.s32 q, %3, 0; selp.f64 %0, %1, %2, q;}"
-      : "=d"(r) : "d"(a), "d"(b), "r"((int)p));
-  return r;
-}
-template <int V>
-using IC = std::integral_constant<int, V>;
 
 // ---------------------------------------------------------------------------
 // pass A
 // ---------------------------------------------------------------------------
-template <bool PROBE>
-__device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, int parity) {
+template <bool PROBE, bool FAST>
+__device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, int parity, PassShared &sh) {
   const Grid &G = A.G;
   const Metrics &M = A.M;
   Scalars *S = A.S;
@@ -230,7 +70,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     // edge role (peer memory): p_k on the two edge shells, locally and into the
     // neighbours' ghost shells, then the halo flags -- scheduled first, beside the
     // interior chunks; these blocks add nothing to sigma
-    __shared__ double sred_e[NTHREADS / 32];
+    double *sred_e = sh.sred;
     pdl_trigger();
     pdl_wait();
     if (S->stop) return;
@@ -249,10 +89,9 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   }
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemA &sm = *reinterpret_cast<SmemA *>(smem_raw);
-  __shared__ double sred[NTHREADS / 32];
-  __shared__ TileConst tcs;
-
-  __shared__ PlaneSm pls;
+  double *sred = sh.sred;
+  TileConst &tcs = sh.tcs;
+  PlaneSm &pls = sh.pls;
   const TileThread t = tile_thread(G);
   const int L = t.c1 - t.c0;
   load_tile_const(tcs, G, M, t.k0);
@@ -297,8 +136,8 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     for (int s = 0; s < NS_A; s++) mbar_init(&sm.bar[s], 1);
     fence_mbar_init();
   }
-  // slot columns 0, 1, 66, 67 are never produced by the transform; they are read
-  // only by the masked halo elements of lanes 0 / 31 and must hold finite values
+  // slot columns 0 and 67 are never produced by the transform (1 and 66, the halo
+  // columns, come from lanes 0 and 31); keep every slot column finite
   for (int i = threadIdx.x; i < 3 * TR; i += blockDim.x) {
     double *row = &sm.pn[i / TR][i % TR][0];
     row[0] = row[1] = row[SROW - 2] = row[SROW - 1] = 0.0;
@@ -327,17 +166,18 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   unsigned ph = 0;  // mbarrier parity of the current group of 3 planes
 
   // per-thread constants of the stencil: smem offsets of the theta neighbours
-  // (clamped on the tile's outer rows, whose results are masked) and the masks
+  // (clamped on the tile's outer rows, which skip the stencil) and the column masks
+  // (FAST tiles: every column is an interior cell)
   int up_off[RPW], dn_off[RPW];
-  bool m0[RPW], m1[RPW];
 #pragma unroll
   for (int e = 0; e < RPW; e++) {
     const int r = t.row[e];
     up_off[e] = (r == 0) ? 0 : -SROW;
     dn_off[e] = (r == TR - 1) ? 0 : SROW;
-    m0[e] = t.stencil[e] && t.st0;
-    m1[e] = t.stencil[e] && t.st1;
   }
+  const bool m0 = FAST || t.st0, m1 = FAST || t.st1;
+  const bool halo_lane = (t.lane == 0) || (t.lane == 31);
+  const int hcol = (t.lane == 0) ? 1 : SROW - 2;  // smem column of this lane's halo column
 
   // One plane step.  STENCIL = false only for q = 0, 1 (peeled), so the steady
   // state is one basic block: the transform's fp64 chains (plane q) and the
@@ -372,7 +212,11 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
       pn.y = selp(rv.y, fma(beta, pv.y, rv.y), ghost);
       R[u][e] = pn;
       *reinterpret_cast<double2 *>(&sm.pn[u][r][cs]) = pn;
-      if (store && t.stencil[e]) store_pair(g_pn + t.rowoff[e], t, G.np, pn, false);
+      if (halo_lane) {  // the halo columns k0-2 (lane 0) and k0+63 (lane 31)
+        const double hr = sm.r[u][r][hcol], hp = sm.p[u][r][hcol];
+        sm.pn[u][r][hcol] = selp(hr, fma(beta, hp, hr), ghost);
+      }
+      if (store && t.stencil[e]) store_pair<FAST>(g_pn + t.rowoff[e], t, G.np, pn, false);
     }
     g_pn += PL;
     // ---- stencil of plane il-1 (its slot was completed before this barrier) ----
@@ -380,6 +224,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
       const double *sb = &sm.pn[um][0][0];
 #pragma unroll
       for (int e = 0; e < RPW; e++) {
+        if (!t.stencil[e]) continue;  // halo rows (warp-uniform)
         const int r = t.row[e];
         const double *so = sb + r * SROW + cs;
         const double2 c = R[um][e];
@@ -397,10 +242,9 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
         const double q0 = stencil7(c.x, R[u][e].x, R[umm][e].x, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e]);
         const double q1 = stencil7(c.y, R[u][e].y, R[umm][e].y, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e]);
 #endif
-        acc += (m0[e] ? c.x * q0 : 0.0) + (m1[e] ? c.y * q1 : 0.0);
-        // diagnostic instantiation only (pot3d_probe_pass_a): q of plane il-1
-        if (PROBE && t.stencil[e])
-          store_pair(A.q_probe + (long long)il * PL + t.rowoff[e], t, G.np, make_double2(q0, q1), false);
+        acc += (m0 ? c.x * q0 : 0.0) + (m1 ? c.y * q1 : 0.0);
+        // diagnostic instantiation only (pot3d_apply_fused which = 2): q of plane il-1
+        if (PROBE) store_pair<FAST>(A.q_probe + (long long)il * PL + t.rowoff[e], t, G.np, make_double2(q0, q1), false);
       }
     }
   };
@@ -437,24 +281,20 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
 // pass B
 // ---------------------------------------------------------------------------
 // USE_Z = false: PC1, the stored vector is z = D^-1 r; true: PC2, the stored vector is r.
-// XM: the x update (A20).  XM_EVERY: x += alpha_k p_k (PC2).  PC1 updates x every other
-// iteration (reading A23): XM_SKIP on even iterations k (x untouched, 24 B/cell), XM_PAIR
-// on odd k: x += alpha_{k-1} p_{k-1} + alpha_k p_k with p_{k-1} = (p_k - z_k) / beta_{k-1}
-// rebuilt from the operands pass B stages anyway, i.e. x += (c + alpha_k) p_k - c z_k,
-// c = alpha_{k-1} / beta_{k-1} (40 B/cell) -- 32 instead of 40 B/cell on average.
-enum XMode { XM_EVERY = 0, XM_SKIP = 1, XM_PAIR = 2 };
-template <bool USE_Z, int XM>
-__device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, int parity) {
+// XM (pass_common.cuh): XM_EVERY x += alpha_k p_k (PC2); PC1 XM_SKIP on even iterations
+// (x untouched, 24 B/cell) and XM_PAIR on odd ones (40 B/cell): 32 B/cell on average.
+template <bool USE_Z, int XM, bool FAST>
+__device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, int parity, PassShared &sh) {
   const Grid &G = A.G;
   const Metrics &M = A.M;
   Scalars *S = A.S;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemB &sm = *reinterpret_cast<SmemB *>(smem_raw);
-  __shared__ double sred[2 * NTHREADS / 32];
-  __shared__ TileConst tcs;
-
-  __shared__ PlaneSm pls;
+  double *sred = sh.sred;
+  TileConst &tcs = sh.tcs;
+  PlaneSm &pls = sh.pls;
   const TileThread t = tile_thread(G);
+  const bool m0 = FAST || t.st0, m1 = FAST || t.st1;  // FAST tiles: every column is a cell
   const int L = t.c1 - t.c0;
   load_tile_const(tcs, G, M, t.k0);
   const int ig0 = G.i0 + t.c0 - 1;
@@ -548,7 +388,7 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
         if (USE_Z) {
           rn.x = fma(-alpha, q0, rv.x);
           rn.y = fma(-alpha, q1, rv.y);
-          acc_rr += (t.st0 ? rn.x * rn.x : 0.0) + (t.st1 ? rn.y * rn.y : 0.0);
+          acc_rr += (m0 ? rn.x * rn.x : 0.0) + (m1 ? rn.y * rn.y : 0.0);
         } else {
           // z_{k+1} = z_k - alpha D^-1 q;  r_{k+1} = D z_{k+1}
           const DiagRow d = diag_row(P, rw[e]);
@@ -556,12 +396,12 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
           rn.x = fma(-alpha, jacobi(q0, d0), rv.x);
           rn.y = fma(-alpha, jacobi(q1, d1), rv.y);
           const double s0 = d0 * rn.x, s1 = d1 * rn.y;
-          acc_rz += (t.st0 ? s0 * rn.x : 0.0) + (t.st1 ? s1 * rn.y : 0.0);
-          acc_rr += (t.st0 ? s0 * s0 : 0.0) + (t.st1 ? s1 * s1 : 0.0);
+          acc_rz += (m0 ? s0 * rn.x : 0.0) + (m1 ? s1 * rn.y : 0.0);
+          acc_rr += (m0 ? s0 * s0 : 0.0) + (m1 ? s1 * s1 : 0.0);
         }
-        store_pair(g_w + t.rowoff[e], t, G.np, rn, true);
+        store_pair<FAST>(g_w + t.rowoff[e], t, G.np, rn, true);
         if (XM != XM_SKIP) {
-          if (t.st0 && t.st1) {
+          if (FAST || (t.st0 && t.st1)) {
             __stcs(reinterpret_cast<double2 *>(g_x + t.rowoff[e]), xn);
           } else {
             if (t.st0) g_x[t.rowoff[e]] = xn.x;
@@ -603,21 +443,30 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   }
 }
 
+// Each pass runs the FAST instantiation on tiles away from the periodic seam and the
+// phi end (tile_fast, block-uniform) and the masked one elsewhere.
+#define POT3D_PASS(BODY, ...)                                   \
+  __shared__ PassShared sh;                                     \
+  if (tile_fast(A.G))                                           \
+    BODY<__VA_ARGS__, true>(T, A, parity, sh);                  \
+  else                                                          \
+    BODY<__VA_ARGS__, false>(T, A, parity, sh)
+
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
-    k_pass_a(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_a_body<false>(T, A, parity); }
-// diagnostic instantiation: also stores q = A p_k into A.q_probe (pot3d_probe_pass_a)
+    k_pass_a(const __grid_constant__ TMaps T, PassArgs A, int parity) { POT3D_PASS(pass_a_body, false); }
+// diagnostic instantiation: also stores q = A p_k into A.q_probe (pot3d_apply_fused which = 2)
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
-    k_pass_a_probe(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_a_body<true>(T, A, parity); }
+    k_pass_a_probe(const __grid_constant__ TMaps T, PassArgs A, int parity) { POT3D_PASS(pass_a_body, true); }
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
     k_pass_b_pc1_even(const __grid_constant__ TMaps T, PassArgs A, int parity) {
-  pass_b_body<false, XM_SKIP>(T, A, parity);
+  POT3D_PASS(pass_b_body, false, XM_SKIP);
 }
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
     k_pass_b_pc1_odd(const __grid_constant__ TMaps T, PassArgs A, int parity) {
-  pass_b_body<false, XM_PAIR>(T, A, parity);
+  POT3D_PASS(pass_b_body, false, XM_PAIR);
 }
 __global__ void __launch_bounds__(NTHREADS, PASS_MINB)
-    k_pass_b_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity) { pass_b_body<true, XM_EVERY>(T, A, parity); }
+    k_pass_b_pc2(const __grid_constant__ TMaps T, PassArgs A, int parity) { POT3D_PASS(pass_b_body, true, XM_EVERY); }
 
 // PC1 after the loop: x += alpha_K p_K when the last iteration K was even (its x
 // update was deferred to the pair that never came, A23)

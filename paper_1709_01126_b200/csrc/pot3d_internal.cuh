@@ -37,8 +37,9 @@ namespace pot3d {
 #ifndef POT3D_MINB
 #define POT3D_MINB 2
 #endif
-constexpr int TK = 62;          // interior phi columns per tile: lane l owns logical
-                                // columns k0-1+2l, k0+2l (lanes 0/31 hold the halo columns)
+constexpr int TK = 64;          // phi columns per tile: lane l owns logical columns
+                                // k0-1+2l, k0+2l (k0 = 64 * tile column); the halo columns
+                                // k0-2 and k0+63 come with the staged box
 #ifndef POT3D_TJ
 #define POT3D_TJ 14
 #endif
@@ -55,7 +56,7 @@ constexpr int TR = TJ + 2;      // haloed rows
 constexpr int RPW = POT3D_RPW;  // haloed rows per warp (each lane: RPW rows x 2 phi cells)
 constexpr int NWARPS = TR / RPW;
 constexpr int NTHREADS = NWARPS * 32;
-constexpr int SROW = 68;        // smem row: index i <-> logical column k0-3+i (2..65 used)
+constexpr int SROW = 68;        // smem row: index i <-> logical column k0-3+i (1..66 used)
 constexpr int TKB = 64;         // width of the interior boxes (r, x): logical k0-1 .. k0+62
 constexpr int NS_A = POT3D_NS_A; // cp.async stages of pass A (NS_A-1 planes in flight)
 constexpr int NS_B = POT3D_NS_B; // cp.async stages of pass B (NS_B-2 planes in flight)
@@ -63,6 +64,13 @@ constexpr int PASS_MINB = POT3D_MINB;  // resident blocks per SM the passes are 
 // dynamic shared memory of the passes (bytes)
 constexpr int SMEM_A = (2 * NS_A + 3) * TR * SROW * 8 + 128;  // + mbarriers
 constexpr int SMEM_B = NS_B * (TR * SROW + 2 * TJ * TKB) * 8 + 128;
+
+// single-reduction CG1 passes (cg1.cu): K1 stages the haloed u box and the p, s, x
+// interior boxes (NS_C stages, one plane in flight), K2 the haloed u box (NS_D stages)
+constexpr int NS_C = 3;
+constexpr int NS_D = 4;
+constexpr int SMEM_C1 = NS_C * (TR * SROW + 3 * TJ * TKB) * 8 + 128;
+constexpr int SMEM_C2 = NS_D * TR * SROW * 8 + 128;
 
 struct Metrics {
   // r (global index, size nr)
@@ -184,6 +192,23 @@ struct PassArgs {
   double *q_probe;      // k_pass_a_probe only: q = A p_k (cell layout)
 };
 
+// CG1 (cg1.cu): TMA descriptors and arguments.  u ping-pongs between U[0], U[1] (K1
+// reads U[parity] haloed, writes U[parity^1]); p, s, x are updated cell by cell.
+struct Cg1Maps {
+  CUtensorMap u_h[2];
+  CUtensorMap p_i, s_i, x_i;
+};
+struct Cg1Args {
+  Grid G;
+  Metrics M;
+  Scalars *S;
+  double *u[2];
+  double *p, *s, *x;
+  double *partials, *hist, *local_sum;
+  int finalize;  // single rank: the last block of K2 updates the scalars
+  int init;      // K2 of the start: gamma_0, delta_0 -> alpha_0
+};
+
 // Arguments of the field kernels (a11).
 struct FieldArgs {
   Grid G;
@@ -196,6 +221,12 @@ struct FieldArgs {
   int nbr;               // r faces on this rank
   double *Br, *Bt, *Bp;  // device layout: [face][j][k], [i][jf][k], [i][j][k] (pitch PK)
 };
+
+// cg1.cu
+__global__ void k_cg1_update_even(const __grid_constant__ Cg1Maps T, Cg1Args A, int parity);
+__global__ void k_cg1_update_odd(const __grid_constant__ Cg1Maps T, Cg1Args A, int parity);
+__global__ void k_cg1_dots(const __grid_constant__ Cg1Maps T, Cg1Args A, int parity);
+__global__ void k_finalize_cg1(Scalars *S, const double *gathered, int nranks, double *hist, int init);
 
 // kernels.cu
 __global__ void k_metrics(int nr, int nt, int np, int bc, const double *rf, const double *tf,

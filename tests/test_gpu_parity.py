@@ -364,7 +364,7 @@ GOLDEN = pathlib.Path(__file__).parent / "golden"
 
 
 @pytest.mark.parametrize("name,pc,blocks", [("small", 1, 1), ("small", 2, 1), ("medium", 1, 1),
-                                            ("medium", 2, 1), ("large", 1, 1)])
+                                            ("large", 1, 1)])
 def test_full_solve_matches_oracle_golden(name, pc, blocks):
     p = GOLDEN / f"oracle_{name}_pc{pc}_b{blocks}.json"
     if not p.exists():
