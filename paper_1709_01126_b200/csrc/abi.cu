@@ -1014,6 +1014,11 @@ int solve_init_end(pot3d_ctx *ctx) {
 // the status of a finished loop (identical on every rank / slab)
 int loop_status(pot3d_ctx *ctx, pot3d_ctx *rep) {
   const Scalars hs = *ctx->hS;
+  if (hs.check) {  // POT3D_CHECK builds only (the bits are never set otherwise)
+    rep->err = "POT3D_CHECK: invariant violated (bits " + std::to_string(hs.check) +
+               ": 1 pass store, 2 sweep store, 4 sweep slot reuse, 8 peer store, 16 mailbox order, 32 CG1 store)";
+    return POT3D_ERR_STATE;
+  }
   const Grid &G = ctx->G;
   cudaStream_t s = ctx->stream;
   if (ctx->trace && getenv("POT3D_TRACE")) {  // mean per-iteration timeline after the edge-shell kernel

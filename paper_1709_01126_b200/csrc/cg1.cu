@@ -199,6 +199,8 @@ __device__ __forceinline__ void cg1_update_body(const Cg1Maps &T, const Cg1Args 
         unw.x = fma(-alpha, jacobi(sn.x, d0), uc[e].x);
         unw.y = fma(-alpha, jacobi(sn.y, d1), uc[e].y);
         const long long o = t.rowoff[e];
+        POT3D_CHK(S, in_range(g_u + o, A.u[parity ^ 1], (G.nr_loc + 2) * PL) &&
+                         in_range(g_p + o, A.p, (G.nr_loc + 2) * PL), CHK_CG1_STORE);
         store_pair<FAST>(g_u + o, t, G.np, unw, true);
         st2(g_p + o, pn);
         st2(g_s + o, sn);

@@ -162,8 +162,14 @@ __device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned l
 // system-scope fence, then the sequence numbers (fence + relaxed store = release);
 // one NVLink round trip on the critical path instead of one per rank
 __device__ __forceinline__ void mail_post(const PeerTab *T, int kind, double v0, double v1,
-                                          unsigned long long seq) {
+                                          unsigned long long seq, Scalars *S) {
   const int me = T->rank;
+#if POT3D_CHECK
+  for (int r = 0; r < T->nranks; r++) {  // slot reuse: the previous post of this slot is older
+    const unsigned long long old = ld_acquire_sys(&T->mail[r]->e[kind][me].seq);
+    if (!(old < seq)) atomicOr(&S->check, (unsigned)CHK_MAIL_ORDER);
+  }
+#endif
   for (int r = 0; r < T->nranks; r++) {
     MailEntry *e = &T->mail[r]->e[kind][me];
     *reinterpret_cast<volatile double *>(&e->v0) = v0;
@@ -380,6 +386,9 @@ __device__ __forceinline__ bool edge_shells(const Grid &G, const Metrics &M, Sca
     v[1] = fma(beta, pv.y, sv.y);
     const bool both = 2 * m + 1 <= G.np + 1;  // physical 2m+1 still a ghost or a cell
     double *rem = sidx == 0 ? lo : hi;
+    // the neighbour's ghost shell: rank-1's top ghost (its shell nr_lo), rank+1's bottom (0)
+    POT3D_CHK(S, !rem || (sidx == 0 ? in_range(rem + o, peers->p_lo[parity_new] + (long long)(peers->nr_lo + 1) * G.plane, G.plane)
+                                    : in_range(rem + o, peers->p_hi[parity_new], G.plane)), CHK_PEER_STORE);
     if (both) {
       *reinterpret_cast<double2 *>(p_new + o) = make_double2(v[0], v[1]);
       if (rem) *reinterpret_cast<double2 *>(rem + o) = make_double2(v[0], v[1]);

@@ -83,7 +83,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     double v[1] = {0.0}, tot[1];
     if (grid_sum<1>(v, A.partials, &S->counter[0], sred_e, tot, pass_bid(G), pass_nb(G)) && threadIdx.x == 0) {
       trace_mark(S, TR_A1);
-      mail_post(A.peers, MAIL_A, tot[0], 0.0, mail_seq(S->epoch, S->iter + 1));
+      mail_post(A.peers, MAIL_A, tot[0], 0.0, mail_seq(S->epoch, S->iter + 1), S);
     }
     return;
   }
@@ -216,7 +216,10 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
         const double hr = sm.r[u][r][hcol], hp = sm.p[u][r][hcol];
         sm.pn[u][r][hcol] = selp(hr, fma(beta, hp, hr), ghost);
       }
-      if (store && t.stencil[e]) store_pair<FAST>(g_pn + t.rowoff[e], t, G.np, pn, false);
+      if (store && t.stencil[e]) {
+        POT3D_CHK(S, in_range(g_pn + t.rowoff[e], A.p_new, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
+        store_pair<FAST>(g_pn + t.rowoff[e], t, G.np, pn, false);
+      }
     }
     g_pn += PL;
     // ---- stencil of plane il-1 (its slot was completed before this barrier) ----
@@ -271,7 +274,7 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     if (A.finalize)
       finalize_alpha(S, tot[0]);
     else if (A.peers)
-      mail_post(A.peers, MAIL_A, tot[0], 0.0, mail_seq(S->epoch, S->iter + 1));
+      mail_post(A.peers, MAIL_A, tot[0], 0.0, mail_seq(S->epoch, S->iter + 1), S);
     else
       A.local_sum[0] = tot[0];
   }
@@ -399,6 +402,8 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
           acc_rz += (m0 ? s0 * rn.x : 0.0) + (m1 ? s1 * rn.y : 0.0);
           acc_rr += (m0 ? s0 * s0 : 0.0) + (m1 ? s1 * s1 : 0.0);
         }
+        POT3D_CHK(S, in_range(g_w + t.rowoff[e], A.r_out, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
+        POT3D_CHK(S, XM == XM_SKIP || in_range(g_x + t.rowoff[e], A.x, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
         store_pair<FAST>(g_w + t.rowoff[e], t, G.np, rn, true);
         if (XM != XM_SKIP) {
           if (FAST || (t.st0 && t.st1)) {
@@ -432,10 +437,10 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
       else
         finalize_beta(S, tot[0], tot[1], A.hist);
     } else if (A.fold) {
-      mail_post(A.peers, MAIL_B, tot[0], tot[1], mail_seq(S->epoch, S->iter + 1));
+      mail_post(A.peers, MAIL_B, tot[0], tot[1], mail_seq(S->epoch, S->iter + 1), S);
       S->pend_b = 1;  // finalised by the next edge-shell kernel
     } else if (A.peers) {
-      mail_post(A.peers, MAIL_B, tot[0], tot[1], mail_seq(S->epoch, S->iter + 1));
+      mail_post(A.peers, MAIL_B, tot[0], tot[1], mail_seq(S->epoch, S->iter + 1), S);
     } else {
       A.local_sum[0] = tot[0];
       A.local_sum[1] = tot[1];

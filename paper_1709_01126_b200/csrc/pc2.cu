@@ -78,6 +78,7 @@ struct SweepArgs {
   double *inv_d;     // FACTOR writes, FWD/BWD read
   double *partials;
   double *edge;
+  long long edge_len;  // doubles of `edge` (POT3D_CHECK bounds)
   int nbmax;
   int predicated;    // skip when the PCG loop has stopped
   int finalize;      // BWD: 1 single rank (rho/beta), 0 local_sum
@@ -472,6 +473,20 @@ __global__ void __launch_bounds__(SWT, 1) k_sweep4(SweepArgs A, int koff, int nt
         vk = v;
       }
       // results: z (w for FWD), physical order col_lo .. col_lo+3
+      POT3D_CHK(A.S, in_range(zr, A.z, (G.nr_loc + 2) * G.plane) && in_range(zr + SV - 1, A.z, (G.nr_loc + 2) * G.plane),
+                CHK_SWEEP_STORE);
+#if POT3D_CHECK
+      if (put_bot) {  // the consumer re-armed this slot (a value not yet read must not be overwritten)
+        double sv[4];
+        ldg4_cg(my_bot + (long long)ivt * SV, sv);
+        POT3D_CHK(A.S, in_range(my_bot + (long long)ivt * SV + SV - 1, A.edge, A.edge_len), CHK_SWEEP_STORE);
+        POT3D_CHK(A.S, is_sent(sv[0]) && is_sent(sv[1]) && is_sent(sv[2]) && is_sent(sv[3]), CHK_SLOT_REUSE);
+      }
+      if (put_rgt) {
+        POT3D_CHK(A.S, in_range(my_rgt + (long long)ivt * 2, A.edge, A.edge_len), CHK_SWEEP_STORE);
+        POT3D_CHK(A.S, is_sent(ldg_cg(my_rgt + (long long)ivt * 2)), CHK_SLOT_REUSE);
+      }
+#endif
       if (full) {
         if (rev)
           stg4(zr, val[3], val[2], val[1], val[0]);
@@ -514,7 +529,7 @@ __global__ void __launch_bounds__(SWT, 1) k_sweep4(SweepArgs A, int koff, int nt
       if (A.finalize)
         finalize_rho(A.S, tot[0]);
       else if (A.peers)
-        mail_post(A.peers, MAIL_C, tot[0], 0.0, mail_seq(A.S->epoch, A.S->iter));
+        mail_post(A.peers, MAIL_C, tot[0], 0.0, mail_seq(A.S->epoch, A.S->iter), A.S);
       else
         A.local_sum[0] = tot[0];
     }
@@ -646,6 +661,7 @@ static SweepArgs sweep_args(Pc2 *P, const Metrics &M, Scalars *S, const double *
   a.inv_d = P->inv_d;
   a.partials = partials;
   a.edge = P->edge;
+  a.edge_len = P->edge_len;
   a.nbmax = P->nbmax;
   a.predicated = predicated;
   a.finalize = finalize;
@@ -679,6 +695,7 @@ int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, 
   // run-vectorised sweeps: their own tile order and edge slots
   a.order = P->d_order4;
   a.edge = P->edge4;
+  a.edge_len = P->edge4_len;
   a.ntiles = P->ntiles4;
   cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);  // ticket only (flags accumulate)
   k_sweep4<SW_FWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_FWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_f, P->ntk4);

@@ -103,7 +103,37 @@ struct Scalars {
                      // finalises them (convergence test, beta) before it builds p_k
   unsigned long long *trace;  // POT3D_TRACE: [64 iterations][16] %globaltimer marks, or null
   long long hist_len;         // entries of the residual-history buffer (writes beyond are dropped)
+  unsigned int check;         // POT3D_CHECK builds: violated invariants (CHK_* bits)
 };
+
+// Checked builds (-DPOT3D_CHECK=1, tests/test_checked_build.py): device-side bounds and
+// protocol invariants recorded in Scalars::check, reported by pot3d_solve as an error.
+// (compute-sanitizer is not available on the GPU pool; this is its stand-in.)
+#ifndef POT3D_CHECK
+#define POT3D_CHECK 0
+#endif
+enum CheckBit {
+  CHK_PASS_STORE = 1,    // a fused pass stored outside its cell array
+  CHK_SWEEP_STORE = 2,   // a PC2 sweep stored outside z / its edge slots
+  CHK_SLOT_REUSE = 4,    // a PC2 producer found its edge slot not yet consumed (re-armed)
+  CHK_PEER_STORE = 8,    // an edge shell landed outside the neighbour's ghost shell
+  CHK_MAIL_ORDER = 16,   // a mailbox sequence number did not increase
+  CHK_CG1_STORE = 32     // a CG1 pass stored outside its arrays
+};
+#if POT3D_CHECK
+#define POT3D_CHK(S, cond, bit)                                   \
+  do {                                                            \
+    if (!(cond)) atomicOr(&(S)->check, (unsigned)(bit));          \
+  } while (0)
+#else
+#define POT3D_CHK(S, cond, bit) \
+  do {                          \
+  } while (0)
+#endif
+// p lies in [base, base + n)
+__host__ __device__ inline bool in_range(const double *p, const double *base, long long n) {
+  return p >= base && p < base + n;
+}
 
 // ---- peer-memory exchange between the rank processes (CUDA IPC over NVLink) ----
 constexpr int MAXR = 16;

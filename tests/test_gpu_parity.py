@@ -363,26 +363,33 @@ def test_random_grids_apply_precond_parity(seed):
 GOLDEN = pathlib.Path(__file__).parent / "golden"
 
 
-@pytest.mark.parametrize("name,pc,blocks", [("small", 1, 1), ("small", 2, 1), ("medium", 1, 1),
-                                            ("large", 1, 1)])
-def test_full_solve_matches_oracle_golden(name, pc, blocks):
-    p = GOLDEN / f"oracle_{name}_pc{pc}_b{blocks}.json"
+@pytest.mark.parametrize("gold", ["oracle_small_pc1_b1", "oracle_small_pc2_b1", "oracle_medium_pc1_b1",
+                                  "oracle_large_pc1_b1_it300"])
+def test_full_solve_matches_oracle_golden(gold):
+    """Full solves (small, medium) and the first 300 iterations of the large grid
+    (A26) against the oracle's committed goldens."""
+    p = GOLDEN / f"{gold}.json"
     if not p.exists():
         pytest.skip(f"{p.name} not written yet (tools/oracle_golden.py)")
     g = json.loads(p.read_text())
-    c = synth.CONFIGS[name]
+    c = synth.CONFIGS[g["config"]]
     rf, tf, pf = c.faces()
-    assert g["grid"] == [c.nr, c.nt, c.np] and g["status"] == 0
-    with solver(rf, tf, pf, c.br0(), pc=pc, pc2_blocks=blocks) as s:
-        res = s.solve(rtol=g["rtol"], true_residual=False)
+    assert g["grid"] == [c.nr, c.nt, c.np]
+    fixed = g.get("fixed_iters", 0)
+    with solver(rf, tf, pf, c.br0(), pc=g["pc"], pc2_blocks=g["pc2_blocks"]) as s:
+        res = s.solve(rtol=g["rtol"], maxit=fixed if fixed else 100000, true_residual=False)
         h = s.history(res.iters + 1)
-    assert res.status == 0
-    assert abs(res.iters - g["iters"]) <= 1, (res.iters, g["iters"])
+    if fixed:
+        assert res.iters == fixed and res.status == 1
+    else:
+        assert res.status == 0 and g["status"] == 0
+        assert abs(res.iters - g["iters"]) <= 1, (res.iters, g["iters"])
     phi = np.asarray(res.phi).reshape(-1)
     ref = np.asarray(g["sample"])
     got = phi[:: g["stride"]]
     assert got.shape == ref.shape
     rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    print(f"{gold}: iters {res.iters} (oracle {g['iters']}), sample rel L2 {rel:.2e}")
     assert rel <= 1e-9, rel
     assert abs(np.linalg.norm(phi) - g["phi_norm2"]) <= 1e-9 * g["phi_norm2"]
     # residual histories: same recurrences, different rounding order; they agree
