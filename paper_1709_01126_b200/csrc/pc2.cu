@@ -59,6 +59,8 @@ struct Pc2 {
   // run-vectorised sweeps (k_sweep4)
   int ntj4, ntk4, ntiles4, koff_f, koff_b;
   int2 *d_order4;
+  int2 *d_orderS;           // k_sweepS: tiles by estimated start step tj*SWJ + tk
+  bool scan;                // k_sweepS (default) or k_sweep4 (POT3D_PC2_SWEEP=4)
   double *edge4;
   long long edge4_len;
   std::vector<void *> allocs;
@@ -536,6 +538,273 @@ __global__ void __launch_bounds__(SWT, 1) k_sweep4(SweepArgs A, int koff, int nt
   }
 }
 
+// ---------------------------------------------------------------------------
+// Row-scan sweeps (k_sweepS, the default): the D-ILU recurrences, tile grid and
+// edge-slot handoff of k_sweep4, but the 32 lanes of a warp work on ONE shell of
+// one theta row: lane m owns the run of SV = 4 phi-consecutive cells 4m .. 4m+3
+// of the tile, so each warp-wide load or store is one contiguous 1-KB segment
+// (k_sweep4's lanes sit on 32 different shells: one L1TEX wavefront per lane and
+// access bounds its 0.72 us step).  Along the row the recurrence
+// w_k = c_k + m_k w_{k-1} is an affine map per cell; the lane composes its run's
+// four maps, an inclusive scan of the lanes' maps (5 shuffle rounds) gives every
+// lane the value entering its run, and the carry into lane 0 is the last cell of
+// the tile to the left (edge slot).  Step t: warp jj handles shell t - jj; the
+// theta neighbour comes from warp jj-1's previous step (shared memory) or the
+// tile above (edge slot); the r neighbour stays in registers.  The scan
+// re-associates the phi recurrence (same operator, rounding of the composed maps).
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int ntk4) {
+  constexpr bool rev = (MODE == SW_BWD);
+  constexpr int PD = SPD;
+  const Grid &G = A.G;
+  const Metrics &M = A.M;
+  if (A.predicated && A.S->stop) return;
+  extern __shared__ __align__(16) double sm4[];
+  double *xw = sm4;                         // [2][SWJ][SNR][SV] rows of the previous step
+  double *crs = xw + Sw4<MODE>::XW;         // [nbmax] r coupling factor of virtual shell iv
+  double *drs = crs + A.nbmax;              // [nbmax] dr of virtual shell iv
+  __shared__ int s_ticket;
+  __shared__ double sred[SWT / 32];
+  const int tid = threadIdx.x;
+  const int jj = tid / SNR, m = tid % SNR;
+  if (tid == 0) s_ticket = atomicAdd(&A.sync[0], 1);
+  __syncthreads();
+  const int ticket = s_ticket;
+  const int b = ticket % A.nblk;
+  const int pos = ticket / A.nblk;
+  const int2 tl = A.order[pos];
+  const int l0 = A.l0[b], l1 = A.l0[b + 1];
+  const int nb = l1 - l0;
+  for (int iv = tid; iv < nb; iv += SWT) {
+    const int ig = G.i0 + (rev ? l1 - 1 - iv : l0 + iv);
+    crs[iv] = (iv > 0) ? (rev ? __ldg(M.arp + ig) : __ldg(M.arm + ig)) : 0.0;
+    drs[iv] = __ldg(M.dr + ig);
+  }
+  const int jv = tl.x * SWJ + jj;
+  const bool vrow = jv < G.nt;  // warp-uniform
+  const int jc = vrow ? (rev ? G.nt - 1 - jv : jv) : 0;
+  const int kv0 = koff + tl.y * SWK + SV * m;        // virtual k of element 0
+  const double g = __ldg(M.g + jc), q = __ldg(M.q + jc);
+  const double ct = rev ? __ldg(M.atp + jc) : __ldg(M.atm + jc);
+  bool ve[SV];
+  double gd[SV], td[SV], qc[SV];
+  bool any = false, full = true;
+#pragma unroll
+  for (int e = 0; e < SV; e++) {
+    const int kv = kv0 + e;
+    ve[e] = vrow && kv >= 0 && kv < G.np;
+    any |= ve[e];
+    full &= ve[e];
+    const int k = rev ? G.np - 1 - kv : kv;
+    const int kc = ve[e] ? k : 0;
+    const double dpk = ve[e] ? __ldg(M.dp + kc) : 0.0;
+    const double cpk = !ve[e] ? 0.0 : rev ? ((k < G.np - 1) ? __ldg(M.app + kc) : 0.0)
+                                          : ((k > 0) ? __ldg(M.apm + kc) : 0.0);
+    gd[e] = g * dpk;
+    td[e] = ct * dpk;
+    qc[e] = q * cpk;
+  }
+  const int col_lo = rev ? G.np - kv0 - 3 : kv0 + COFF;
+  const long long ostep = rev ? -G.plane : G.plane;
+  const long long o0 = (long long)((rev ? l1 - 1 : l0) + 1) * G.plane + (long long)jc * G.PK + col_lo -
+                       (long long)jj * ostep;
+
+  const int my = tl.x * ntk4 + tl.y;
+  const long long tstride = (long long)A.nbmax * (SNR * SV + SWJ * 2);
+  double *eb = A.edge + (long long)b * A.ntiles * tstride;
+  double *my_bot = eb + my * tstride + (long long)m * A.nbmax * SV;
+  double *my_rgt = eb + my * tstride + (long long)SNR * A.nbmax * SV + (long long)jj * A.nbmax * 2;
+  const bool put_bot = (jj == SWJ - 1) && (jv + 1 < G.nt) && any;
+  const bool put_rgt = (m == SNR - 1) && vrow && (kv0 + SV < G.np);
+  const bool need_j = (jj == 0) && vrow && (jv > 0) && any;
+  const bool need_k = (m == 0) && vrow && (kv0 > 0);
+  double *up_bot = eb + (long long)(my - ntk4) * tstride + (long long)m * A.nbmax * SV;
+  double *lf_rgt = eb + (long long)(my - 1) * tstride + (long long)SNR * A.nbmax * SV + (long long)jj * A.nbmax * 2;
+
+  const double *src0 = (MODE == SW_FWD) ? A.r : A.z;
+  const double *src1 = A.inv_d;
+  const double *src2 = A.r;
+  const int ts_lo = jj;  // first step with a cell of this warp
+  double *xo_me = xw + (jj * SNR + m) * SV;
+  const double *xj_me = xw + ((jj > 0 ? jj - 1 : 0) * SNR + m) * SV;
+  constexpr int XB = SWJ * SNR * SV;
+
+  double ra[PD][SV], rb[PD][SV], rc[PD][SV], rj[PD][SV], rk[PD];
+  int pf_t = 0;
+  long long pf_o = o0;
+  auto prefetch = [&](auto U) {
+    constexpr int u = decltype(U)::value;
+    const int iv = pf_t - ts_lo;
+    if (any && (unsigned)iv < (unsigned)nb) {
+      ldg4(src0 + pf_o, ra[u]);
+      ldg4(src1 + pf_o, rb[u]);
+      if (MODE == SW_BWD) ldg4(src2 + pf_o, rc[u]);
+      if (need_j) ldg4_cg(up_bot + iv * SV, rj[u]);
+      if (need_k) rk[u] = ldg_cg(lf_rgt + iv * 2);
+    }
+    ++pf_t;
+    pf_o += ostep;
+  };
+
+  double wprev[SV];
+#pragma unroll
+  for (int e = 0; e < SV; e++) wprev[e] = 0.0;
+  double acc = 0.0;
+  bool proto = false;
+  double *zr = A.z + o0;
+
+  auto step = [&](auto U, int t) {
+    constexpr int u = decltype(U)::value;
+    __syncthreads();  // row jj-1 of step t-1 is in xw; crs/drs staged
+    const int ivt = t - ts_lo;
+    if (vrow && (unsigned)ivt < (unsigned)nb) {  // warp-uniform: every lane takes part in the scan
+      double a0[SV], b0[SV], c0[SV];
+#pragma unroll
+      for (int e = 0; e < SV; e++) {
+        const int pe = rev ? SV - 1 - e : e;
+        a0[e] = ra[u][pe];
+        b0[e] = rb[u][pe];
+        c0[e] = (MODE == SW_BWD) ? rc[u][pe] : 0.0;
+      }
+      const double *xp = (t & 1) ? xw : xw + XB;  // buffer of step t-1
+      double vj[SV];
+      if (jj > 0) {
+        const double2 u0 = *reinterpret_cast<const double2 *>(xp + (xj_me - xw));
+        const double2 u1 = *reinterpret_cast<const double2 *>(xp + (xj_me - xw) + 2);
+        vj[0] = u0.x; vj[1] = u0.y; vj[2] = u1.x; vj[3] = u1.y;
+      } else if (need_j) {
+        double *slot = up_bot + (long long)ivt * SV;
+#pragma unroll
+        for (int e = 0; e < SV; e++) {
+          double v = rj[u][e];
+          if (ve[e] && is_sent(v)) v = poll_slot(slot + e, v, A.sync + 1, proto);
+          vj[e] = ve[e] ? v : 0.0;
+        }
+        stg4_cg(slot, __longlong_as_double((long long)SENT), __longlong_as_double((long long)SENT),
+                __longlong_as_double((long long)SENT), __longlong_as_double((long long)SENT));
+      } else {
+        vj[0] = vj[1] = vj[2] = vj[3] = 0.0;
+      }
+      double vk0 = 0.0;  // the carry into lane 0: the left tile's last cell of this row and shell
+      if (need_k) {
+        vk0 = rk[u];
+        if (is_sent(vk0)) vk0 = poll_slot(lf_rgt + (long long)ivt * 2, vk0, A.sync + 1, proto);
+        __stcg(reinterpret_cast<unsigned long long *>(lf_rgt + (long long)ivt * 2), SENT);
+      }
+      const double cr = crs[ivt], dr = drs[ivt];
+      // per cell: w_e = cc_e + mm_e w_{e-1}
+      double cc[SV], mm[SV];
+#pragma unroll
+      for (int e = 0; e < SV; e++) {
+        const double Ar = cr * gd[e], At = dr * td[e], Ap = dr * qc[e];
+        double c, mul;
+        if (MODE == SW_FWD) {
+          c = (a0[e] + Ar * wprev[e] + At * vj[e]) * b0[e];
+          mul = Ap * b0[e];
+        } else {
+          c = a0[e] + b0[e] * (Ar * wprev[e] + At * vj[e]);
+          mul = b0[e] * Ap;
+        }
+        cc[e] = ve[e] ? c : 0.0;
+        mm[e] = ve[e] ? mul : 0.0;
+      }
+      // the run's map w_out = C + Mr w_in, then the inclusive scan over the lanes
+      double C = cc[0], Mr = mm[0];
+#pragma unroll
+      for (int e = 1; e < SV; e++) {
+        C = fma(mm[e], C, cc[e]);
+        Mr = mm[e] * Mr;
+      }
+#pragma unroll
+      for (int o = 1; o < SNR; o <<= 1) {
+        const double Cp = __shfl_up_sync(0xffffffffu, C, o);
+        const double Mp = __shfl_up_sync(0xffffffffu, Mr, o);
+        if (m >= o) {
+          C = fma(Mr, Cp, C);
+          Mr = Mr * Mp;
+        }
+      }
+      double Ce = __shfl_up_sync(0xffffffffu, C, 1), Me = __shfl_up_sync(0xffffffffu, Mr, 1);
+      if (m == 0) {
+        Ce = 0.0;
+        Me = 1.0;
+      }
+      vk0 = __shfl_sync(0xffffffffu, vk0, 0);
+      double vk = fma(Me, vk0, Ce);  // the value entering this lane's run
+      double val[SV];
+#pragma unroll
+      for (int e = 0; e < SV; e++) {
+        double v = fma(mm[e], vk, cc[e]);
+        v = ve[e] ? v : 0.0;
+        // lanes past the grid take part in the scan with unloaded operands: select, never multiply
+        if (MODE == SW_BWD) acc += ve[e] ? c0[e] * v : 0.0;
+        val[e] = v;
+        vk = v;
+      }
+      POT3D_CHK(A.S, !any || (in_range(zr, A.z, (G.nr_loc + 2) * G.plane) &&
+                              in_range(zr + SV - 1, A.z, (G.nr_loc + 2) * G.plane)), CHK_SWEEP_STORE);
+#if POT3D_CHECK
+      if (put_bot) {
+        double sv[4];
+        ldg4_cg(my_bot + (long long)ivt * SV, sv);
+        POT3D_CHK(A.S, in_range(my_bot + (long long)ivt * SV + SV - 1, A.edge, A.edge_len), CHK_SWEEP_STORE);
+        POT3D_CHK(A.S, is_sent(sv[0]) && is_sent(sv[1]) && is_sent(sv[2]) && is_sent(sv[3]), CHK_SLOT_REUSE);
+      }
+      if (put_rgt) {
+        POT3D_CHK(A.S, in_range(my_rgt + (long long)ivt * 2, A.edge, A.edge_len), CHK_SWEEP_STORE);
+        POT3D_CHK(A.S, is_sent(ldg_cg(my_rgt + (long long)ivt * 2)), CHK_SLOT_REUSE);
+      }
+#endif
+      if (full) {
+        if (rev)
+          stg4(zr, val[3], val[2], val[1], val[0]);
+        else
+          stg4(zr, val[0], val[1], val[2], val[3]);
+      } else if (any) {
+        if (rev ? ve[3] : ve[0]) zr[0] = rev ? val[3] : val[0];
+        if (rev ? ve[2] : ve[1]) zr[1] = rev ? val[2] : val[1];
+        if (rev ? ve[1] : ve[2]) zr[2] = rev ? val[1] : val[2];
+        if (rev ? ve[0] : ve[3]) zr[3] = rev ? val[0] : val[3];
+      }
+      if (put_bot) stg4_cg(my_bot + (long long)ivt * SV, val[0], val[1], val[2], val[3]);
+      if (put_rgt) __stcg(my_rgt + (long long)ivt * 2, val[SV - 1]);
+      double *xo = ((t & 1) ? xw + XB : xw) + (xo_me - xw);
+      *reinterpret_cast<double2 *>(xo) = make_double2(val[0], val[1]);
+      *reinterpret_cast<double2 *>(xo + 2) = make_double2(val[2], val[3]);
+#pragma unroll
+      for (int e = 0; e < SV; e++) wprev[e] = val[e];
+    }
+    zr += ostep;
+    prefetch(U);  // step t + PD into this slot
+  };
+
+  const int nsteps = nb + SWJ - 1;
+  prefetch(IC2<0>{});
+  if (PD > 1) prefetch(IC2<(PD > 1 ? 1 : 0)>{});
+  if (PD > 2) prefetch(IC2<(PD > 2 ? 2 : 0)>{});
+  if (PD > 3) prefetch(IC2<(PD > 3 ? 3 : 0)>{});
+#pragma unroll 1
+  for (int t = 0; t < nsteps; t += PD) {
+    step(IC2<0>{}, t);
+    if (PD > 1) { if (t + 1 >= nsteps) break; step(IC2<(PD > 1 ? 1 : 0)>{}, t + 1); }
+    if (PD > 2) { if (t + 2 >= nsteps) break; step(IC2<(PD > 2 ? 2 : 0)>{}, t + 2); }
+    if (PD > 3) { if (t + 3 >= nsteps) break; step(IC2<(PD > 3 ? 3 : 0)>{}, t + 3); }
+  }
+  if (__syncthreads_or(proto) && tid == 0) atomicOr(&A.sync[1], 2);
+  if (MODE == SW_BWD) {
+    double v[1] = {acc}, tot[1];
+    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket) && tid == 0) {
+      if (A.finalize)
+        finalize_rho(A.S, tot[0]);
+      else if (A.peers)
+        mail_post(A.peers, MAIL_C, tot[0], 0.0, mail_seq(A.S->epoch, A.S->iter), A.S);
+      else
+        A.local_sum[0] = tot[0];
+    }
+  }
+}
+
 __global__ void k_fill_u64(unsigned long long *a, long long n, unsigned long long v) {
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
        c += (long long)gridDim.x * blockDim.x)
@@ -598,8 +867,14 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
   P->ntiles4 = P->ntj4 * P->ntk4;
   P->edge4_len = (long long)P->nblk * P->ntiles4 * P->nbmax * (SNR * SV + SWJ * 2);
   P->d_order4 = (int2 *)p_alloc(P, sizeof(int2) * P->ntiles4, alloc, actx);
+  P->d_orderS = (int2 *)p_alloc(P, sizeof(int2) * P->ntiles4, alloc, actx);
   P->edge4 = (double *)p_alloc(P, sizeof(double) * P->edge4_len, alloc, actx);
-  if (!P->d_l0 || !P->d_order || !P->d_sync || !P->inv_d || !P->edge || !P->d_order4 || !P->edge4) {
+  {
+    const char *e = getenv("POT3D_PC2_SWEEP");
+    P->scan = !(e && atoi(e) == 4);
+  }
+  if (!P->d_l0 || !P->d_order || !P->d_sync || !P->inv_d || !P->edge || !P->d_order4 || !P->d_orderS ||
+      !P->edge4) {
     *out = P;
     return -1;
   }
@@ -610,6 +885,10 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
   if (cudaFuncSetAttribute(k_sweep4<SW_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(Sw4<SW_FWD>::SMEM + 16 * nbmax_set)) != cudaSuccess ||
       cudaFuncSetAttribute(k_sweep4<SW_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(Sw4<SW_BWD>::SMEM + 16 * nbmax_set)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_sweepS<SW_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(Sw4<SW_FWD>::SMEM + 16 * nbmax_set)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_sweepS<SW_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(Sw4<SW_BWD>::SMEM + 16 * nbmax_set)) != cudaSuccess) {
     *out = P;
     return -1;
@@ -632,9 +911,17 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
     const int sx = x.x * SWJ + x.y * SNR, sy = y.x * SWJ + y.y * SNR;
     return sx != sy ? sx < sy : x.x < y.x;
   });
+  // k_sweepS: a tile's row waits for the same row and shell of the tile to its left
+  // (one step) and for the bottom row of the tile above (SWJ steps)
+  std::vector<int2> orderS(order4);
+  std::stable_sort(orderS.begin(), orderS.end(), [](const int2 &x, const int2 &y) {
+    const int sx = x.x * SWJ + x.y, sy = y.x * SWJ + y.y;
+    return sx != sy ? sx < sy : x.x < y.x;
+  });
   // everything on the context stream (the factor kernel runs there too)
   cudaMemcpyAsync(P->d_order, order.data(), sizeof(int2) * P->ntiles, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(P->d_order4, order4.data(), sizeof(int2) * P->ntiles4, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(P->d_orderS, orderS.data(), sizeof(int2) * P->ntiles4, cudaMemcpyHostToDevice, s);
   k_fill_u64<<<1024, 256, 0, s>>>(reinterpret_cast<unsigned long long *>(P->edge4), P->edge4_len, SENT);
   cudaMemcpyAsync(P->d_l0, block_l0, sizeof(int) * (nblocks_local + 1), cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(P->inv_d, 0, sizeof(double) * cells, s);
@@ -692,15 +979,21 @@ int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, 
   SweepArgs a = sweep_args(P, M, S, r, z, partials, pred, finalize, local_sum);
   a.peers = iteration ? peers : nullptr;
   if (!iteration) a.finalize = 0, a.local_sum = local_sum;
-  // run-vectorised sweeps: their own tile order and edge slots
-  a.order = P->d_order4;
+  // run-vectorised / row-scan sweeps: their own tile order and edge slots
+  a.order = P->scan ? P->d_orderS : P->d_order4;
   a.edge = P->edge4;
   a.edge_len = P->edge4_len;
   a.ntiles = P->ntiles4;
   cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);  // ticket only (flags accumulate)
-  k_sweep4<SW_FWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_FWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_f, P->ntk4);
+  if (P->scan)
+    k_sweepS<SW_FWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_FWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_f, P->ntk4);
+  else
+    k_sweep4<SW_FWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_FWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_f, P->ntk4);
   cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);
-  k_sweep4<SW_BWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_BWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_b, P->ntk4);
+  if (P->scan)
+    k_sweepS<SW_BWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_BWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_b, P->ntk4);
+  else
+    k_sweep4<SW_BWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_BWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_b, P->ntk4);
   const Grid &G = P->G;
   k_pc2_ghost<<<(unsigned)std::min<long long>(((long long)G.nr_loc * G.nt + 255) / 256, 4096), 256, 0,
                 s>>>(G, z, S, pred);

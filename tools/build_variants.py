@@ -6,6 +6,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
+    "spd3": ["POT3D_SPD=3"],
+    "spd4": ["POT3D_SPD=4"],
     "pd3": [],
     "pd2": ["POT3D_SPD=2"],
     "pd4": ["POT3D_SPD=4"],

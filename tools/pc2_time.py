@@ -9,4 +9,4 @@ rf, tf, pf = c.faces()
 with Pot3d(rf, tf, pf, c.br0(), pc=2, pc2_blocks=blocks) as s:
     s.solve(rtol=0.0, maxit=10, true_residual=False)
     a, b, p = s.profile(10)
-    print(f"{os.environ.get('POT3D_LIB','default')[-14:]} blocks {blocks}: pass A {a*1e3:.0f} us, pass B {b*1e3:.0f} us, sweeps {p*1e3:.0f} us")
+    print(f"sweep={os.environ.get("POT3D_PC2_SWEEP", "scan")} {cfg} blocks {blocks}: pass A {a*1e3:.0f} us, pass B {b*1e3:.0f} us, sweeps {p*1e3:.0f} us")

@@ -12,5 +12,7 @@ for (nr, nt, np_) in GEOMS:
         s.solve(rtol=0.0, maxit=4, true_residual=False, want_phi=False)
         a, b, p = s.profile(6)
         ntj, ntk = (nt + 7) // 8, (np_ + 3 + 127) // 128
-        steps = nr + 8 + 32 - 2
-        print(f"{nr}x{nt}x{np_}: tiles {ntj}x{ntk} sweeps {p*1e3:.0f} us  per sweep-step {p*1e3/2/steps:.2f} us", flush=True)
+        scan = os.environ.get("POT3D_PC2_SWEEP", "0") != "4"
+        steps = nr + 8 - 1 if scan else nr + 8 + 32 - 2
+        print(f"{'scan' if scan else 'sweep4'} {nr}x{nt}x{np_}: tiles {ntj}x{ntk} sweeps {p*1e3:.0f} us  "
+              f"per sweep-step {p*1e3/2/steps:.2f} us", flush=True)
