@@ -18,6 +18,8 @@ Parity status of each function:
   pcg (CG1)        pinned: the same SPEC 2x2 / random SPD / brute-force pins,
                    and exact-arithmetic equivalence with the standard
                    variant (iterates agree to rounding, iterations +-1).
+  cheb_apply (PC3) pinned: the closed form (I - R_m(D^-1 A)) A^-1 with the
+                   Chebyshev residual polynomial on random SPD matrices.
   solve (PC1/PC2)  pinned: dense brute force, closed form, the survey's
                    independent iteration counts (tiny PC1 229, PC2 91/96/104/
                    114 for 1/2/4/8 blocks, closed wall 428, small 913),
@@ -101,6 +103,11 @@ def lib():
         L.orc_pcg.argtypes = [ctypes.c_int64, LINOP, ctypes.c_void_p, LINOP, ctypes.c_void_p, d,
                               ctypes.c_double, ctypes.c_int64, ci, d, i64, d, d]
         L.orc_slab_bounds.argtypes = [ci, ci, ci, P(ci), P(ci)]
+        L.orc_set_poly.argtypes = [ci, ctypes.c_double]
+        L.orc_set_poly.restype = None
+        L.orc_cheb_apply.argtypes = [ctypes.c_int64, LINOP, ctypes.c_void_p, d, ci, ctypes.c_double,
+                                     ctypes.c_double, d, d]
+        L.orc_cheb_apply.restype = None
         L.orc_slab_bounds.restype = None
         L.orc_session_create.argtypes = [ci, ci, ci, d, d, d, ci, ci, ci, d]
         L.orc_session_create.restype = ctypes.c_void_p
@@ -182,10 +189,36 @@ class System:
         return A
 
 
+POLY_DEFAULT = (4, 100.0)  # PC3: Chebyshev steps m, interval ratio b/a (b = 2)
+
+
+def set_poly(m=POLY_DEFAULT[0], ratio=POLY_DEFAULT[1]):
+    """Parameters of PC3 (Chebyshev-accelerated Jacobi) for the following calls."""
+    lib().orc_set_poly(int(m), float(ratio))
+
+
+def cheb_apply(A, inv_d, r, m, a, b=2.0):
+    """z = (I - R_m(D^-1 A)) A^-1 r by the oracle's Chebyshev loop (orc_cheb_apply)
+    on a caller operator (dense matrix or callable)."""
+    r = _f(r).reshape(-1)
+    n = r.size
+    fa = (lambda v: A @ v) if isinstance(A, np.ndarray) else A
+
+    def cb(_ctx, x, y):
+        np.ctypeslib.as_array(y, shape=(n,))[:] = fa(np.ctypeslib.as_array(x, shape=(n,)).copy())
+
+    c = LINOP(cb)
+    z = np.empty(n)
+    lib().orc_cheb_apply(n, c, None, _d(_f(inv_d)), int(m), float(a), float(b), _d(r), _d(z))
+    return z
+
+
 def solve(rf, tf, pf, br0, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1, rtol=1e-9, maxit=100000,
-          history=False, variant=STANDARD):
+          history=False, variant=STANDARD, poly=POLY_DEFAULT):
     """Oracle PCG solve.  Returns dict(x, iters, rel_res, true_rel_res, status[, hist]).
-    variant: STANDARD or CG1 (Chronopoulos-Gear)."""
+    variant: STANDARD or CG1 (Chronopoulos-Gear).
+    pc: 1 Jacobi, 2 block ILU0, 3 Chebyshev-accelerated Jacobi (poly = (m, b/a))."""
+    set_poly(*poly)
     rf, tf, pf, br0 = _f(rf), _f(tf), _f(pf), _f(br0)
     nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
     x = np.zeros(nr * nt * np_)
@@ -242,7 +275,8 @@ def slab_bounds(nr, nblocks):
     return out
 
 
-def precond(rf, tf, pf, r, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1):
+def precond(rf, tf, pf, r, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1, poly=POLY_DEFAULT):
+    set_poly(*poly)
     rf, tf, pf, r = _f(rf), _f(tf), _f(pf), _f(r).reshape(-1)
     nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
     z = np.empty_like(r)

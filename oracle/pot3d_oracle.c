@@ -390,15 +390,79 @@ static void slab_bounds(int nr, int nblocks, int b, int *i0, int *i1) {
 
 typedef struct {
   int pc, nblocks, nr, nt, np;
-  double *inv_diag;      /* PC1 */
+  double *inv_diag;      /* PC1, PC3 */
+  int poly_m;            /* PC3: Chebyshev steps (the degree of the residual polynomial) */
+  double poly_a, poly_b; /* PC3: eigenvalue interval of D^-1 A the polynomial targets */
+  const double *wrap;    /* PC3: the operator's periodic couplings (set by the caller) */
   orc_csr *blocks;       /* PC2 */
   double *rb, *zb;       /* PC2 scratch */
 } orc_pc;
 
+/* ------------------------------------------------------------------------ */
+/* PC3 (the "vector-friendly" preconditioner the paper    */
+/* calls for; not in the paper): Chebyshev acceleration of Jacobi,    */
+/* Saad, Iterative Methods 2nd ed., Alg. 12.1, applied to A z = r from       */
+/* z_0 = 0 with the preconditioned residual D^-1 r, m steps:                 */
+/*   theta = (b+a)/2, delta = (b-a)/2, sigma1 = theta/delta, rho0 = 1/sigma1 */
+/*   res_0 = D^-1 r;  d_0 = res_0 / theta;  z_1 = d_0                        */
+/*   k = 1..m-1: res_k = res_{k-1} - D^-1 A d_{k-1}                          */
+/*               rho_k = 1 / (2 sigma1 - rho_{k-1})                          */
+/*               d_k = rho_k rho_{k-1} d_{k-1} + (2 rho_k / delta) res_k     */
+/*               z_{k+1} = z_k + d_k                                         */
+/* so z_m = (I - R_m(D^-1 A)) A^-1 r with R_m(t) = T_m((b+a-2t)/(b-a)) /     */
+/* T_m((b+a)/(b-a)): a fixed SPD operator when the spectrum of D^-1 A lies   */
+/* in (0, b].  b = 2 bounds it (Gershgorin: A is diagonally dominant).       */
+/* ------------------------------------------------------------------------ */
+typedef void (*orc_linop)(void *ctx, const double *x, double *y);
+
+void orc_cheb_apply(int64_t N, orc_linop A, void *actx, const double *inv_d, int m, double a,
+                    double b, const double *r, double *z) {
+  double *res = malloc(sizeof(double) * N), *d = malloc(sizeof(double) * N);
+  double *q = malloc(sizeof(double) * N);
+  const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma1 = theta / delta;
+  double rho = 1.0 / sigma1;
+  for (int64_t i = 0; i < N; i++) {
+    res[i] = inv_d[i] * r[i];
+    d[i] = res[i] / theta;
+    z[i] = d[i];
+  }
+  for (int k = 1; k < m; k++) {
+    A(actx, d, q);
+    const double rho_new = 1.0 / (2.0 * sigma1 - rho);
+    const double c1 = rho_new * rho, c2 = 2.0 * rho_new / delta;
+    for (int64_t i = 0; i < N; i++) {
+      res[i] -= inv_d[i] * q[i];
+      d[i] = c1 * d[i] + c2 * res[i];
+      z[i] += d[i];
+    }
+    rho = rho_new;
+  }
+  free(res); free(d); free(q);
+}
+
+typedef struct { int nr, nt, np; const double *bands, *wrap; } orc_sys;
+static void sys_apply(void *ctx, const double *x, double *y) {
+  const orc_sys *S = (const orc_sys *)ctx;
+  orc_apply(S->nr, S->nt, S->np, S->bands, S->wrap, x, y);
+}
+
+/* PC3 parameters (degree m, interval ratio b/a); orc_set_poly changes them for
+ * the following builds of the preconditioner. */
+static int g_poly_m = 4;
+static double g_poly_ratio = 100.0;
+void orc_set_poly(int m, double ratio) {
+  g_poly_m = m;
+  g_poly_ratio = ratio;
+}
+
 /* PC1: inverse of the diagonal of A. */
 static void pc_apply(const orc_pc *M, const double *bands, const double *r, double *z) {
   const int64_t N = (int64_t)M->nr * M->nt * M->np;
-  (void)bands;
+  if (M->pc == 3) {
+    orc_sys op = {M->nr, M->nt, M->np, bands, M->wrap};
+    orc_cheb_apply(N, sys_apply, &op, M->inv_diag, M->poly_m, M->poly_a, M->poly_b, r, z);
+    return;
+  }
   if (M->pc == 1) {
 #pragma omp parallel for schedule(static)
     for (int64_t m = 0; m < N; m++) z[m] = M->inv_diag[m] * r[m];
@@ -427,7 +491,13 @@ static int pc_build(orc_pc *M, int pc, int nblocks, int nr, int nt, int np, cons
   const int64_t N = (int64_t)nr * nt * np;
   memset(M, 0, sizeof(*M));
   M->pc = pc; M->nblocks = nblocks < 1 ? 1 : nblocks; M->nr = nr; M->nt = nt; M->np = np;
-  if (pc == 1) {
+  if (pc == 3) {
+    if (g_poly_m < 1 || !(g_poly_ratio > 1.0)) return -1;
+    M->poly_m = g_poly_m;
+    M->poly_b = 2.0;
+    M->poly_a = 2.0 / g_poly_ratio;
+  }
+  if (pc == 1 || pc == 3) {
     M->inv_diag = malloc(sizeof(double) * N);
     for (int64_t m = 0; m < N; m++) {
       if (bands[3 * N + m] == 0.0) return -1;
@@ -520,7 +590,6 @@ static double dot(int64_t n, const double *x, const double *y) {
 /* status: 0 converged, 1 maxit reached, -4 indefinite.                      */
 /* hist (nullable, maxit+1 doubles): ||r_k||/||b|| for k = 0..iters.          */
 /* ------------------------------------------------------------------------ */
-typedef void (*orc_linop)(void *ctx, const double *x, double *y);
 #define ORC_PCG_STANDARD 0
 #define ORC_PCG_CG1 1
 
@@ -606,12 +675,7 @@ done:
   return status;
 }
 
-/* The POT3D operator and preconditioners as orc_pcg callbacks. */
-typedef struct { int nr, nt, np; const double *bands, *wrap; } orc_sys;
-static void sys_apply(void *ctx, const double *x, double *y) {
-  const orc_sys *S = (const orc_sys *)ctx;
-  orc_apply(S->nr, S->nt, S->np, S->bands, S->wrap, x, y);
-}
+/* The POT3D preconditioners as orc_pcg callbacks. */
 typedef struct { const orc_pc *M; const double *bands; } orc_pcctx;
 static void pc_cb(void *ctx, const double *r, double *z) {
   const orc_pcctx *C = (const orc_pcctx *)ctx;
@@ -639,6 +703,7 @@ int orc_solve_v(int nr, int nt, int np, const double *rf, const double *tf,
   orc_rhs(nr, nt, np, rf, tf, pf, bc, br0, b, NULL);
   orc_pc M;
   int prc = pc_build(&M, pc, pc2_blocks, nr, nt, np, bands);
+  M.wrap = wrap;
   if (prc == -2) { /* ILU breakdown: fall back to PC1 */
     pc_free(&M);
     pc_build(&M, 1, 1, nr, nt, np, bands);
@@ -698,6 +763,7 @@ int orc_precond(int nr, int nt, int np, const double *rf, const double *tf,
   orc_assemble(nr, nt, np, rf, tf, pf, bc, bands, wrap);
   orc_pc M;
   int rc = pc_build(&M, pc, pc2_blocks, nr, nt, np, bands);
+  M.wrap = wrap;
   if (rc == 0) pc_apply(&M, bands, r, z);
   pc_free(&M);
   free(bands); free(wrap);
@@ -858,6 +924,7 @@ void *orc_session_create(int nr, int nt, int np, const double *rf, const double 
     pc_free(&S->M);
     pc_build(&S->M, 1, 1, nr, nt, np, S->bands);
   }
+  S->M.wrap = S->wrap;
   S->sys = (orc_sys){nr, nt, np, S->bands, S->wrap};
   S->pcc = (orc_pcctx){&S->M, S->bands};
   return S;
