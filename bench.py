@@ -49,6 +49,8 @@ def parse():
                     choices=["tiny", "small", "medium", "large", "pc2", "weak"])
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
     ap.add_argument("--pc2-blocks", type=int, default=1)
+    ap.add_argument("--variant", type=int, default=0, choices=[0, 1],
+                    help="0 standard PCG, 1 single-reduction CG1 (PC1; SURVEY 8(f)-1)")
     ap.add_argument("--weak-iters", type=int, default=300)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=20)
@@ -67,7 +69,8 @@ def workload_desc(c, args):
     law = "uniform" if c.uniform else "nonuniform (A13)"
     mp = "dipole" if c.lmax == 0 else f"dipole + l<={c.lmax} multipoles seed {c.seed} (A14)"
     return (f"{c.name} {c.nr}x{c.nt}x{c.np} {law}, {mp}, "
-            f"{'source surface' if c.bc == 0 else 'closed wall'}, PC{c.pc}")
+            f"{'source surface' if c.bc == 0 else 'closed wall'}, PC{c.pc}"
+            f"{', CG1 single-reduction PCG' if getattr(args, 'variant', 0) else ''}")
 
 
 # --------------------------------------------------------------------------- clocks
@@ -249,7 +252,7 @@ def main():
     rf, tf, pf = c.faces()
     br_np = c.br0((rf, tf, pf))
     s = Pot3d(rf, tf, pf, br_np, bc=c.bc, pc=c.pc, rank=rank, nranks=world,
-              pc2_blocks=args.pc2_blocks, unroll=32)  # fresh NCCL id broadcast inside
+              pc2_blocks=args.pc2_blocks, unroll=32, variant=args.variant)  # fresh NCCL id inside
     s.trace(True)  # in-situ pass durations of the timed solves (%globaltimer, no extra launches)
     info = s.info()
     fixed_iters = args.weak_iters if args.config == "weak" else 0
@@ -328,7 +331,11 @@ def main():
 
     # roofline of the dominant kernel: live durations from the timed solve; the
     # same passes launched separately between CUDA events are reported beside them
-    ms_a_iso, ms_b_iso, ms_pc = s.profile(args.profile_iters)
+    cg1 = args.variant == 1
+    if cg1:  # pot3d_profile runs the standard passes only
+        ms_a_iso = ms_b_iso = ms_pc = 0.0
+    else:
+        ms_a_iso, ms_b_iso, ms_pc = s.profile(args.profile_iters)
     cells_loc = s.nr_loc * c.nt * c.np
     pc1 = info["pc"] == 1
     try:
@@ -350,12 +357,16 @@ def main():
     else:
         timing = "isolated launches between CUDA events"
         ms_a, ms_be, ms_bo, ms_b = ms_a_iso, ms_b_iso, ms_b_iso, ms_b_iso
-    kern = [("k_pass_a", 24 * cells_loc, 1.0, ms_a)]
-    if pc1:
-        kern += [("k_pass_b_pc1_even", 24 * cells_loc, 0.5, ms_be), ("k_pass_b_pc1_odd", 40 * cells_loc, 0.5, ms_bo)]
+    if cg1:  # the trace's "pass A" slot is the dots kernel, "pass B" the update kernel
+        kern = [("k_cg1_dots", 8 * cells_loc, 1.0, ms_a), ("k_cg1_update_even", 48 * cells_loc, 0.5, ms_be),
+                ("k_cg1_update_odd", 64 * cells_loc, 0.5, ms_bo)]
     else:
+        kern = [("k_pass_a", 24 * cells_loc, 1.0, ms_a)]
+    if pc1 and not cg1:
+        kern += [("k_pass_b_pc1_even", 24 * cells_loc, 0.5, ms_be), ("k_pass_b_pc1_odd", 40 * cells_loc, 0.5, ms_bo)]
+    elif not pc1:
         kern += [("k_pass_b_pc2", 40 * cells_loc, 1.0, ms_b),
-                 ("k_sweep4 (forward + backward)", 56 * cells_loc, 1.0, ms_pc)]
+                 ("k_sweepS (forward + backward)", 56 * cells_loc, 1.0, ms_pc)]
     table = {k: {"bytes_per_launch": by, "launches_per_iter": lp, "ms": t, "gbs": by / (t * 1e-3) / 1e9,
                  "frac": by / (t * 1e-3) / 1e9 / peak} for k, by, lp, t in kern}
     dom, dom_bytes, _, dom_ms = max(kern, key=lambda k: k[2] * k[3])

@@ -79,7 +79,8 @@ typedef enum {
 } pot3d_status;
 
 typedef enum { POT3D_SOURCE_SURFACE = 0, POT3D_CLOSED_WALL = 1 } pot3d_outer_bc; /* P:54 */
-typedef enum { POT3D_PC1 = 1, POT3D_PC2 = 2 } pot3d_pc;                          /* P:88 */
+typedef enum { POT3D_PC1 = 1, POT3D_PC2 = 2,                                    /* P:88 */
+               POT3D_PC3 = 3 /* Chebyshev-accelerated Jacobi (SURVEY §8(f)-2; one rank) */ } pot3d_pc;
 
 typedef struct {
   int32_t nr, nt, np;            /* cell counts (ghosts excluded, A12); each >= 2 */
@@ -107,6 +108,9 @@ typedef struct {
   int32_t variant;               /* PCG recurrences: 0 standard (two reductions per
                                     iteration), 1 single-reduction CG1
                                     (Chronopoulos-Gear) */
+  int32_t poly_degree;           /* PC3: Chebyshev steps m per apply (2..8); 0 -> 4 */
+  double poly_ratio;             /* PC3: the polynomial targets [2/ratio, 2] of D^-1 A's
+                                    spectrum (Saad Alg. 12.1); 0 -> 100 */
 } pot3d_runtime;
 
 typedef struct {

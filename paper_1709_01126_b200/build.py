@@ -14,7 +14,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpot3d.so"
-SOURCES = ["kernels.cu", "passes.cu", "cg1.cu", "pc2.cu", "abi.cu"]
+SOURCES = ["kernels.cu", "passes.cu", "cg1.cu", "poly.cu", "pc2.cu", "abi.cu"]
 HEADERS = ["pot3d_internal.cuh", "device_common.cuh", "pass_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

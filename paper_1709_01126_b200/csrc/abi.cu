@@ -67,6 +67,12 @@ struct pot3d_ctx {
   TMaps tmaps{};
   Cg1Maps cmaps{};          // CG1: U[0] = r, U[1] = P[1], p = P[0], s = s_cg
   double *s_cg = nullptr;
+  // PC3 (poly.cu): Chebyshev steps, their coefficients and work vectors
+  int poly_m = 4;
+  double poly_ratio = 100.0;
+  PolyMaps pmaps{};
+  double *p_res = nullptr, *p_d[2] = {nullptr, nullptr}, *p_x = nullptr;
+  double p_theta = 0.0, p_c1[POLY_MMAX] = {0.0}, p_c2[POLY_MMAX] = {0.0};
   // peer-memory exchange (nranks > 1): P[0], P[1] and the mailbox are cudaMalloc'd
   // (IPC-exportable) and mapped into the neighbours' / all ranks' address spaces
   bool xfer_want = false, xfer = false;
@@ -411,11 +417,18 @@ int make_map(pot3d_ctx *ctx, CUtensorMap *m, double *base, unsigned b0, unsigned
 }
 
 int make_maps(pot3d_ctx *ctx) {
-  TRY(make_map(ctx, &ctx->tmaps.src_h, ctx->pc == 2 ? ctx->z : ctx->r, SROW, TR));
+  TRY(make_map(ctx, &ctx->tmaps.src_h, ctx->pc >= 2 ? ctx->z : ctx->r, SROW, TR));
   TRY(make_map(ctx, &ctx->tmaps.p_h[0], ctx->P[0], SROW, TR));
   TRY(make_map(ctx, &ctx->tmaps.p_h[1], ctx->P[1], SROW, TR));
   TRY(make_map(ctx, &ctx->tmaps.r_i, ctx->r, TKB, TJ));
   TRY(make_map(ctx, &ctx->tmaps.x_i, ctx->x, TKB, TJ));
+  if (ctx->pc == 3) {
+    TRY(make_map(ctx, &ctx->pmaps.d_h[0], ctx->p_d[0], SROW, TR));
+    TRY(make_map(ctx, &ctx->pmaps.d_h[1], ctx->p_d[1], SROW, TR));
+    TRY(make_map(ctx, &ctx->pmaps.res_i, ctx->p_res, TKB, TJ));
+    TRY(make_map(ctx, &ctx->pmaps.x_i, ctx->p_x, TKB, TJ));
+    TRY(make_map(ctx, &ctx->pmaps.r_i, ctx->r, TKB, TJ));
+  }
   if (ctx->variant == 1) {
     TRY(make_map(ctx, &ctx->cmaps.u_h[0], ctx->r, SROW, TR));
     TRY(make_map(ctx, &ctx->cmaps.u_h[1], ctx->P[1], SROW, TR));
@@ -434,7 +447,7 @@ PassArgs make_args(pot3d_ctx *ctx, int parity) {
   a.S = ctx->S;
   a.r = ctx->r;
   a.r_out = ctx->r;
-  a.z = ctx->pc == 2 ? ctx->z : ctx->r;  // PC1 stores z = D^-1 r in ctx->r (A22)
+  a.z = ctx->pc >= 2 ? ctx->z : ctx->r;  // PC1 stores z = D^-1 r in ctx->r (A22)
   a.p_old = ctx->P[parity];
   a.p_new = ctx->P[parity ^ 1];
   a.x = ctx->x;
@@ -450,7 +463,7 @@ PassKernel kern_a(const pot3d_ctx *) { return k_pass_a; }
 // parity = iteration index & 1 (every solve starts at iteration 0; graphs hold an even
 // number of iterations): PC1 updates x on odd iterations only (A23)
 PassKernel kern_b(const pot3d_ctx *ctx, int parity) {
-  if (ctx->pc == 2) return k_pass_b_pc2;
+  if (ctx->pc >= 2) return k_pass_b_pc2;
   return parity ? k_pass_b_pc1_odd : k_pass_b_pc1_even;
 }
 
@@ -666,6 +679,43 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
   return st;
 }
 
+// PC3: z = M^-1 r (ctx->r -> ctx->z), the partial r.z to rho/beta (finalize) or local_sum
+int poly_apply(pot3d_ctx *ctx, int finalize, bool iteration) {
+  const Grid &G = ctx->G;
+  PolyArgs a{};
+  a.G = G;
+  a.M = ctx->M;
+  a.S = ctx->S;
+  a.r = ctx->r;
+  a.res = ctx->p_res;
+  a.d[0] = ctx->p_d[0];
+  a.d[1] = ctx->p_d[1];
+  a.x = ctx->p_x;
+  a.z = ctx->z;
+  a.theta = ctx->p_theta;
+  for (int k = 0; k < POLY_MMAX; k++) {
+    a.c1[k] = ctx->p_c1[k];
+    a.c2[k] = ctx->p_c2[k];
+  }
+  a.partials = ctx->partials;
+  a.local_sum = ctx->local_sum;
+  a.finalize = finalize;
+  a.predicated = iteration ? 1 : 0;
+  const bool pdl = ctx->pdl && iteration;
+  CK(launch_k(pdl, k_poly_init, dim3(148 * 8), dim3(256), 0, ctx->stream, a));
+  a.G.nchunks = ctx->nchunks_b;
+  const dim3 grd(G.ntj * G.ntk, ctx->nchunks_b);
+  for (int k = 1; k < ctx->poly_m; k++)
+    CK(launch_k(pdl, k + 1 == ctx->poly_m ? k_poly_last : k_poly_step, grd, dim3(NTHREADS), SMEM_P, ctx->stream,
+                ctx->pmaps, a, k));
+  if (iteration)
+    ctx->n_enq += ctx->poly_m;
+  else
+    ctx->n_launch += ctx->poly_m;
+  MARK("pc3");
+  return 0;
+}
+
 int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   if (ctx->variant == 1) {
     for (auto &f : cg1_steps(ctx, parity, false)) TRY(f());
@@ -755,6 +805,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     CK(cudaGetLastError());
     ctx->n_enq++;
   }
+  if (ctx->pc == 3) TRY(poly_apply(ctx, 1, true));
   if (pc2) {
     int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, multi ? 0 : 1,
                        ctx->local_sum, ctx->stream, true);
@@ -983,8 +1034,9 @@ int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit) {
     CK(cudaGetLastError());
     ctx->n_launch += nk;
   }
+  if (ctx->pc == 3) TRY(poly_apply(ctx, 0, false));  // z0 = M^-1 b
   k_init_dots<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, ctx->partials, ctx->nranks == 1,
-                                      ctx->local_sum, ctx->pc == 2, ctx->z);
+                                      ctx->local_sum, ctx->pc >= 2, ctx->z);
   CK(cudaGetLastError());
   ctx->n_launch++;
   if (ctx->pc == 1) {
@@ -1232,12 +1284,15 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   int64_t k = 2;
   if (ctx->nranks > 1) k += (ctx->xfer && ctx->pc == 1) ? 2 : 3;
   if (ctx->pc == 2 && ctx->pc2) k += pc2_kernels_per_apply(ctx->pc2) + (ctx->nranks > 1 ? 1 : 0);
+  if (ctx->pc == 3) k += ctx->poly_m;
   info->graph_kernels_per_iter = k;
   // algorithmic bytes
   const int64_t cells = (int64_t)ctx->G.nr_loc * ctx->nt * ctx->np;
   // PC1: pass A 24 + pass B 24 (even) / 40 (odd) = 56 B/cell on average (A23)
   // CG1: update 48 (even) / 64 (odd) + dots 8 = 64 B/cell on average
-  info->bytes_per_iter = (ctx->pc == 2 ? 120 : (ctx->variant == 1 ? 64 : 56)) * cells;
+  // PC3: passes 64 + Chebyshev 32 (init) + 48 per middle step + 40 (last) = 48 m + 40
+  info->bytes_per_iter = (ctx->pc == 2 ? 120 : ctx->pc == 3 ? 48 * ctx->poly_m + 40
+                                                            : (ctx->variant == 1 ? 64 : 56)) * cells;
   info->device_bytes = (int64_t)ctx->dev_bytes;
   info->kernel_launches = ctx->n_launch;
   info->exchange = ctx->nranks == 1 ? 0 : (ctx->xfer ? 2 : 1);
@@ -1326,8 +1381,8 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
     ctx->err = "outer_bc must be SOURCE_SURFACE or CLOSED_WALL";
     return fail(POT3D_ERR_INVALID);
   }
-  if (pc != POT3D_PC1 && pc != POT3D_PC2) {
-    ctx->err = "pc must be 1 or 2";
+  if (pc != POT3D_PC1 && pc != POT3D_PC2 && pc != POT3D_PC3) {
+    ctx->err = "pc must be 1, 2 or 3";
     return fail(POT3D_ERR_INVALID);
   }
   ctx->rf.assign(grid->r_faces, grid->r_faces + nr + 1);
@@ -1370,6 +1425,13 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   ctx->nranks = R.nranks < 1 ? 1 : R.nranks;
   ctx->pc2_blocks = R.pc2_blocks < 1 ? 1 : R.pc2_blocks;
   ctx->variant = R.variant;
+  ctx->poly_m = R.poly_degree > 0 ? R.poly_degree : 4;
+  ctx->poly_ratio = R.poly_ratio > 0.0 ? R.poly_ratio : 100.0;
+  if (pc == POT3D_PC3 && (ctx->nranks > 1 || member || R.variant != 0 || ctx->poly_m < 2 ||
+                          ctx->poly_m > POLY_MMAX || !(ctx->poly_ratio > 1.0))) {
+    ctx->err = "PC3 runs on one rank (no loopback, standard PCG) with 2 <= poly_degree <= 8, poly_ratio > 1";
+    return fail(POT3D_ERR_INVALID);
+  }
   if (ctx->variant != 0 && (ctx->variant != 1 || pc != POT3D_PC1)) {
     ctx->err = "variant must be 0 (PCG) or 1 (CG1, PC1 only)";
     return fail(POT3D_ERR_INVALID);
@@ -1435,7 +1497,9 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
       }
     }
   }
-  if (cudaFuncSetAttribute(k_cg1_update_even, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_C1) ||
+  if (cudaFuncSetAttribute(k_poly_step, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_P) ||
+      cudaFuncSetAttribute(k_poly_last, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_P) ||
+      cudaFuncSetAttribute(k_cg1_update_even, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_C1) ||
       cudaFuncSetAttribute(k_cg1_update_odd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_C1) ||
       cudaFuncSetAttribute(k_cg1_dots, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_C2)) {
     ctx->err = "cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed (CG1)";
@@ -1487,7 +1551,23 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   } else {
     DA(ctx->P[0], cells); DA(ctx->P[1], cells);
   }
-  if (pc == POT3D_PC2) DA(ctx->z, cells);
+  if (pc == POT3D_PC2 || pc == POT3D_PC3) DA(ctx->z, cells);
+  if (pc == POT3D_PC3) {
+    DA(ctx->p_res, cells); DA(ctx->p_d[0], cells); DA(ctx->p_d[1], cells); DA(ctx->p_x, cells);
+    for (double *p : {ctx->p_res, ctx->p_d[0], ctx->p_d[1], ctx->p_x})
+      if (cudaMemsetAsync(p, 0, cells * sizeof(double), ctx->stream)) { ctx->err = "memset"; return fail(POT3D_ERR_CUDA); }
+    // Saad Alg. 12.1 coefficients on [a, b] = [2 / ratio, 2] (the oracle's arithmetic)
+    const double b = 2.0, a = 2.0 / ctx->poly_ratio;
+    const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma1 = theta / delta;
+    double rho = 1.0 / sigma1;
+    ctx->p_theta = theta;
+    for (int k = 1; k < ctx->poly_m; k++) {
+      const double rho_new = 1.0 / (2.0 * sigma1 - rho);
+      ctx->p_c1[k] = rho_new * rho;
+      ctx->p_c2[k] = 2.0 * rho_new / delta;
+      rho = rho_new;
+    }
+  }
   DA(ctx->bshell, G.plane + 16); DA(ctx->br_dev, G.plane + 16); DA(ctx->mean2, 2);
   DA(ctx->S, 1);
   ctx->partials_len = 4 * (size_t)std::max<long long>(
@@ -1825,7 +1905,7 @@ int pot3d_apply_fused(pot3d_ctx *ctx, const double *x, double *y, int32_t which)
   std::vector<pot3d_ctx *> M = members(ctx);
   // the production passes with scalars that turn them into plain applies (parity 0:
   // pass A reads p_{k-1} from P[0] and writes p_k to P[1]; pass B reads p_k from P[1])
-  auto src_of = [](pot3d_ctx *m) { return m->pc == 2 ? m->z : m->r; };
+  auto src_of = [](pot3d_ctx *m) { return m->pc >= 2 ? m->z : m->r; };
   auto fix_cols = [&](pot3d_ctx *m, double *a) -> int {
     const Grid &G = m->G;
     k_fix_ghost_cols<<<(unsigned)((G.nr_loc * (long long)m->nt + 255) / 256), 256, 0, s>>>(G, a, 0, G.nr_loc);
@@ -1897,6 +1977,13 @@ int pot3d_precond(pot3d_ctx *ctx, const double *rin, double *zout) {
       TRY(nk);
       CK(cudaGetLastError());
       m->n_launch += nk;
+    } else if (m->pc == 3) {  // the Chebyshev steps read r and write z (their TMA maps)
+      const size_t bytes = (size_t)(m->G.nr_loc + 2) * m->G.plane * sizeof(double);
+      Scalars h0{};
+      CK(cudaMemcpyAsync(m->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(m->r, m->P[0], bytes, cudaMemcpyDeviceToDevice, s));
+      TRY(poly_apply(m, 0, false));
+      CK(cudaMemcpyAsync(m->P[1], m->z, bytes, cudaMemcpyDeviceToDevice, s));
     } else {
       // PC1: the kernel that forms z_0 = D^-1 b at the start of a solve (mode -1)
       Scalars h0{};

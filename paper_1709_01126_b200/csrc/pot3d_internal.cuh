@@ -71,6 +71,9 @@ constexpr int NS_C = 3;
 constexpr int NS_D = 4;
 constexpr int SMEM_C1 = NS_C * (TR * SROW + 3 * TJ * TKB) * 8 + 128;
 constexpr int SMEM_C2 = NS_D * TR * SROW * 8 + 128;
+// PC3 Chebyshev steps (poly.cu): the haloed d box and the res, z (and r) interior boxes
+constexpr int SMEM_P = NS_C * (TR * SROW + 3 * TJ * TKB) * 8 + 128;
+constexpr int POLY_MMAX = 8;  // most Chebyshev steps per PC3 apply
 
 struct Metrics {
   // r (global index, size nr)
@@ -239,6 +242,24 @@ struct Cg1Args {
   int init;      // K2 of the start: gamma_0, delta_0 -> alpha_0
 };
 
+// PC3 (poly.cu): TMA descriptors and arguments.  d ping-pongs between d[0], d[1].
+struct PolyMaps {
+  CUtensorMap d_h[2];
+  CUtensorMap res_i, x_i, r_i;
+};
+struct PolyArgs {
+  Grid G;
+  Metrics M;
+  Scalars *S;
+  const double *r;       // the residual the apply starts from
+  double *res, *d[2], *x, *z;
+  double theta;          // (b + a) / 2
+  double c1[POLY_MMAX], c2[POLY_MMAX];  // step k: d_k = c1[k] d_{k-1} + c2[k] res_k
+  double *partials, *local_sum;
+  int finalize;          // LAST: 1 updates rho/beta, 0 writes local_sum
+  int predicated;        // skip when the PCG loop has stopped
+};
+
 // Arguments of the field kernels (a11).
 struct FieldArgs {
   Grid G;
@@ -257,6 +278,11 @@ __global__ void k_cg1_update_even(const __grid_constant__ Cg1Maps T, Cg1Args A, 
 __global__ void k_cg1_update_odd(const __grid_constant__ Cg1Maps T, Cg1Args A, int parity);
 __global__ void k_cg1_dots(const __grid_constant__ Cg1Maps T, Cg1Args A, int parity);
 __global__ void k_finalize_cg1(Scalars *S, const double *gathered, int nranks, double *hist, int init);
+
+// poly.cu
+__global__ void k_poly_init(PolyArgs A);
+__global__ void k_poly_step(const __grid_constant__ PolyMaps T, PolyArgs A, int step);
+__global__ void k_poly_last(const __grid_constant__ PolyMaps T, PolyArgs A, int step);
 
 // kernels.cu
 __global__ void k_metrics(int nr, int nt, int np, int bc, const double *rf, const double *tf,

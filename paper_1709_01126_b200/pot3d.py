@@ -24,6 +24,7 @@ SOURCE_SURFACE = 0
 CLOSED_WALL = 1
 PC1 = 1
 PC2 = 2
+PC3 = 3  # Chebyshev-accelerated Jacobi
 
 OK = 0
 NOT_CONVERGED = 1
@@ -60,7 +61,8 @@ class _Runtime(ctypes.Structure):
                 ("alloc", _ALLOC), ("free", _FREE), ("alloc_ctx", ctypes.c_void_p),
                 ("pc2_blocks", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("unroll", ctypes.c_int32), ("loopback_slabs", ctypes.c_int32),
-                ("variant", ctypes.c_int32)]
+                ("variant", ctypes.c_int32), ("poly_degree", ctypes.c_int32),
+                ("poly_ratio", ctypes.c_double)]
 
 
 class _Info(ctypes.Structure):
@@ -192,11 +194,12 @@ class Pot3d:
 
     def __init__(self, r_faces, t_faces, p_faces, br0, bc=SOURCE_SURFACE, pc=PC1, *, rank=0,
                  nranks=1, nccl_id: bytes | None = None, stream=None, pc2_blocks=1, device=None,
-                 unroll=32, torch_allocator=True, loopback_slabs=0, variant=0):
+                 unroll=32, torch_allocator=True, loopback_slabs=0, variant=0, poly=(4, 100.0)):
         """loopback_slabs = k > 1 (single process): the grid is split into k r-slabs on
         this one device, exchanging halos and reductions through the multi-GPU
         peer-memory kernels (include/pot3d.h); arrays are then the whole grid.
-        variant: 0 standard PCG, 1 single-reduction CG1."""
+        variant: 0 standard PCG, 1 single-reduction CG1.
+        pc=3: Chebyshev-accelerated Jacobi with poly = (steps m, interval ratio)."""
         import torch
 
         if not torch.cuda.is_available():
@@ -244,6 +247,7 @@ class Pot3d:
         rt.pc2_blocks = pc2_blocks
         rt.loopback_slabs = int(loopback_slabs)
         rt.variant = int(variant)
+        rt.poly_degree, rt.poly_ratio = int(poly[0]), float(poly[1])
         rt.device = dev
         rt.unroll = unroll
         p_br, keep = _ptr(br0)

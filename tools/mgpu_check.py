@@ -20,18 +20,21 @@ local = int(os.environ.get("LOCAL_RANK", rank))
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 fails = 0
-cases = [("tiny", 1, 1, synth.SOURCE_SURFACE), ("small", 1, 1, synth.SOURCE_SURFACE),
-         ("small", 1, 1, synth.CLOSED_WALL), ("small", 2, 1, synth.SOURCE_SURFACE),
-         ("small", 2, 2, synth.SOURCE_SURFACE), ("small", 2, 1, synth.CLOSED_WALL)]
+cases = [("tiny", 1, 1, synth.SOURCE_SURFACE, 0), ("small", 1, 1, synth.SOURCE_SURFACE, 0),
+         ("small", 1, 1, synth.CLOSED_WALL, 0), ("small", 2, 1, synth.SOURCE_SURFACE, 0),
+         ("small", 2, 2, synth.SOURCE_SURFACE, 0), ("small", 2, 1, synth.CLOSED_WALL, 0)]
 # the thinnest legal slabs: 2 shells per rank
-cases.append(("thin", 1, 1, synth.SOURCE_SURFACE))
-cases.append(("thin", 2, 1, synth.SOURCE_SURFACE))
-for name, pc, blocks, bc in cases:
+cases.append(("thin", 1, 1, synth.SOURCE_SURFACE, 0))
+cases.append(("thin", 2, 1, synth.SOURCE_SURFACE, 0))
+# CG1 (single-reduction PCG) across ranks: NCCL halo + one all-gather
+cases += [("tiny", 1, 1, synth.SOURCE_SURFACE, 1), ("small", 1, 1, synth.CLOSED_WALL, 1),
+          ("thin", 1, 1, synth.SOURCE_SURFACE, 1)]
+for name, pc, blocks, bc, variant in cases:
     c = synth.Config("thin", 2 * world, 17, 33, lmax=4) if name == "thin" else synth.CONFIGS[name]
     rf, tf, pf = c.faces()
     br = c.br0()
     t0 = time.time()
-    with Pot3d(rf, tf, pf, br, bc=bc, pc=pc, rank=rank, nranks=world, pc2_blocks=blocks) as s:
+    with Pot3d(rf, tf, pf, br, bc=bc, pc=pc, rank=rank, nranks=world, pc2_blocks=blocks, variant=variant) as s:
         res = s.solve(rtol=1e-9)
         exch = s.info()["exchange"]
         # a second solve in the same context (new epoch of the peer sequence numbers)
@@ -43,14 +46,14 @@ for name, pc, blocks, bc in cases:
     if rank == 0:
         import oracle
 
-        ref = oracle.solve(rf, tf, pf, br, bc=bc, pc=pc, pc2_blocks=world * blocks, rtol=1e-9)
+        ref = oracle.solve(rf, tf, pf, br, bc=bc, pc=pc, pc2_blocks=world * blocks, rtol=1e-9, variant=variant)
         phi = phi.cpu().numpy()
         rel = np.linalg.norm(phi - ref["x"]) / np.linalg.norm(ref["x"])
         obr, _, _ = oracle.field(rf, tf, pf, br, ref["x"], bc=bc)
         ferr = np.abs(brg.cpu().numpy() - obr).max() / np.abs(obr).max()
         ok = abs(res.iters - ref["iters"]) <= 1 and rel <= 1e-9 and ferr <= 1e-7 and same
         fails += 0 if ok else 1
-        print(f"[{world} ranks] {name} pc{pc} blocks/rank {blocks} bc {bc}: iters {res.iters} "
+        print(f"[{world} ranks] {name} pc{pc}{' cg1' if variant else ''} blocks/rank {blocks} bc {bc}: iters {res.iters} "
               f"(oracle {ref['iters']}) rel {rel:.2e} field {ferr:.2e} true_res "
               f"{res.true_rel_residual:.2e} exchange {exch} repeat {'same' if same else 'DIFF'} "
               f"{'OK' if ok else 'FAIL'} ({time.time() - t0:.1f}s)",
