@@ -362,7 +362,9 @@ def main():
                 ("k_cg1_update_odd", 64 * cells_loc, 0.5, ms_bo)]
     else:
         kern = [("k_pass_a", 24 * cells_loc, 1.0, ms_a)]
-    if pc1 and not cg1:
+    if cg1:
+        pass
+    elif pc1:
         kern += [("k_pass_b_pc1_even", 24 * cells_loc, 0.5, ms_be), ("k_pass_b_pc1_odd", 40 * cells_loc, 0.5, ms_bo)]
     elif info["pc"] == 2:
         kern += [("k_pass_b_pc2", 40 * cells_loc, 1.0, ms_b),
