@@ -553,24 +553,20 @@ __global__ void __launch_bounds__(SWT, 1) k_sweep4(SweepArgs A, int koff, int nt
 // tile above (edge slot); the r neighbour stays in registers.  The scan
 // re-associates the phi recurrence (same operator, rounding of the composed maps).
 // ---------------------------------------------------------------------------
-template <int MODE>
-__global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int ntk4) {
+// FULL: every cell of the tile lies inside the grid (no masks; all tiles but the
+// last theta row and the two phi ends)
+template <int MODE, bool FULL>
+__device__ __forceinline__ void sweepS_body(const SweepArgs &A, int koff, int ntk4, int ticket, double *sred) {
   constexpr bool rev = (MODE == SW_BWD);
   constexpr int PD = SPD;
   const Grid &G = A.G;
   const Metrics &M = A.M;
-  if (A.predicated && A.S->stop) return;
   extern __shared__ __align__(16) double sm4[];
   double *xw = sm4;                         // [2][SWJ][SNR][SV] rows of the previous step
   double *crs = xw + Sw4<MODE>::XW;         // [nbmax] r coupling factor of virtual shell iv
   double *drs = crs + A.nbmax;              // [nbmax] dr of virtual shell iv
-  __shared__ int s_ticket;
-  __shared__ double sred[SWT / 32];
   const int tid = threadIdx.x;
   const int jj = tid / SNR, m = tid % SNR;
-  if (tid == 0) s_ticket = atomicAdd(&A.sync[0], 1);
-  __syncthreads();
-  const int ticket = s_ticket;
   const int b = ticket % A.nblk;
   const int pos = ticket / A.nblk;
   const int2 tl = A.order[pos];
@@ -582,7 +578,7 @@ __global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int nt
     drs[iv] = __ldg(M.dr + ig);
   }
   const int jv = tl.x * SWJ + jj;
-  const bool vrow = jv < G.nt;  // warp-uniform
+  const bool vrow = FULL || jv < G.nt;  // warp-uniform
   const int jc = vrow ? (rev ? G.nt - 1 - jv : jv) : 0;
   const int kv0 = koff + tl.y * SWK + SV * m;        // virtual k of element 0
   const double g = __ldg(M.g + jc), q = __ldg(M.q + jc);
@@ -593,7 +589,7 @@ __global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int nt
 #pragma unroll
   for (int e = 0; e < SV; e++) {
     const int kv = kv0 + e;
-    ve[e] = vrow && kv >= 0 && kv < G.np;
+    ve[e] = FULL || (vrow && kv >= 0 && kv < G.np);
     any |= ve[e];
     full &= ve[e];
     const int k = rev ? G.np - 1 - kv : kv;
@@ -615,6 +611,10 @@ __global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int nt
   double *eb = A.edge + (long long)b * A.ntiles * tstride;
   double *my_bot = eb + my * tstride + (long long)m * A.nbmax * SV;
   double *my_rgt = eb + my * tstride + (long long)SNR * A.nbmax * SV + (long long)jj * A.nbmax * 2;
+  if (FULL) {
+    any = true;
+    full = true;
+  }
   const bool put_bot = (jj == SWJ - 1) && (jv + 1 < G.nt) && any;
   const bool put_rgt = (m == SNR - 1) && vrow && (kv0 + SV < G.np);
   const bool need_j = (jj == 0) && vrow && (jv > 0) && any;
@@ -675,12 +675,16 @@ __global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int nt
         vj[0] = u0.x; vj[1] = u0.y; vj[2] = u1.x; vj[3] = u1.y;
       } else if (need_j) {
         double *slot = up_bot + (long long)ivt * SV;
+        bool waiting = false;  // one test for the usual case: all four values arrived
 #pragma unroll
-        for (int e = 0; e < SV; e++) {
-          double v = rj[u][e];
-          if (ve[e] && is_sent(v)) v = poll_slot(slot + e, v, A.sync + 1, proto);
-          vj[e] = ve[e] ? v : 0.0;
+        for (int e = 0; e < SV; e++) waiting |= (FULL || ve[e]) && is_sent(rj[u][e]);
+        if (waiting) {
+#pragma unroll
+          for (int e = 0; e < SV; e++)
+            if ((FULL || ve[e]) && is_sent(rj[u][e])) rj[u][e] = poll_slot(slot + e, rj[u][e], A.sync + 1, proto);
         }
+#pragma unroll
+        for (int e = 0; e < SV; e++) vj[e] = (FULL || ve[e]) ? rj[u][e] : 0.0;
         stg4_cg(slot, __longlong_as_double((long long)SENT), __longlong_as_double((long long)SENT),
                 __longlong_as_double((long long)SENT), __longlong_as_double((long long)SENT));
       } else {
@@ -706,8 +710,8 @@ __global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int nt
           c = a0[e] + b0[e] * (Ar * wprev[e] + At * vj[e]);
           mul = b0[e] * Ap;
         }
-        cc[e] = ve[e] ? c : 0.0;
-        mm[e] = ve[e] ? mul : 0.0;
+        cc[e] = (FULL || ve[e]) ? c : 0.0;
+        mm[e] = (FULL || ve[e]) ? mul : 0.0;
       }
       // the run's map w_out = C + Mr w_in, then the inclusive scan over the lanes
       double C = cc[0], Mr = mm[0];
@@ -736,9 +740,9 @@ __global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int nt
 #pragma unroll
       for (int e = 0; e < SV; e++) {
         double v = fma(mm[e], vk, cc[e]);
-        v = ve[e] ? v : 0.0;
+        v = (FULL || ve[e]) ? v : 0.0;
         // lanes past the grid take part in the scan with unloaded operands: select, never multiply
-        if (MODE == SW_BWD) acc += ve[e] ? c0[e] * v : 0.0;
+        if (MODE == SW_BWD) acc += (FULL || ve[e]) ? c0[e] * v : 0.0;
         val[e] = v;
         vk = v;
       }
@@ -803,6 +807,23 @@ __global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int nt
         A.local_sum[0] = tot[0];
     }
   }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int ntk4) {
+  if (A.predicated && A.S->stop) return;
+  __shared__ int s_ticket;
+  __shared__ double sred[SWT / 32];
+  if (threadIdx.x == 0) s_ticket = atomicAdd(&A.sync[0], 1);
+  __syncthreads();
+  const int ticket = s_ticket;
+  const int2 tl = A.order[ticket / A.nblk];
+  const int kv_lo = koff + tl.y * SWK;
+  const bool full = (tl.x + 1) * SWJ <= A.G.nt && kv_lo >= 0 && kv_lo + SWK <= A.G.np;
+  if (full)
+    sweepS_body<MODE, true>(A, koff, ntk4, ticket, sred);
+  else
+    sweepS_body<MODE, false>(A, koff, ntk4, ticket, sred);
 }
 
 __global__ void k_fill_u64(unsigned long long *a, long long n, unsigned long long v) {
