@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="large",
-                    choices=["tiny", "small", "medium", "large", "pc2", "pc3", "pc3large", "weak"])
+                    choices=["tiny", "small", "medium", "large", "pc2", "pc3", "pc3large", "batch", "batchsmall",
+                             "weak"])
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
     ap.add_argument("--pc2-blocks", type=int, default=1)
     ap.add_argument("--variant", type=int, default=0, choices=[0, 1],
@@ -67,7 +68,10 @@ def make_config(args, world):
 
 def workload_desc(c, args):
     law = "uniform" if c.uniform else "nonuniform (A13)"
+    k = c.extra.get("nrhs", 1)
     mp = "dipole" if c.lmax == 0 else f"dipole + l<={c.lmax} multipoles seed {c.seed} (A14)"
+    if k > 1:
+        mp = f"a batch of {k} maps: dipole + l<={c.lmax} multipoles seeds {c.seed}-{c.seed + k - 1} (A14)"
     return (f"{c.name} {c.nr}x{c.nt}x{c.np} {law}, {mp}, "
             f"{'source surface' if c.bc == 0 else 'closed wall'}, PC{c.pc}"
             f"{', CG1 single-reduction PCG' if getattr(args, 'variant', 0) else ''}")
@@ -250,9 +254,11 @@ def main():
 
     c = make_config(args, world)
     rf, tf, pf = c.faces()
-    br_np = c.br0((rf, tf, pf))
+    kb = c.extra.get("nrhs", 1)  # a multi-RHS batch: k problems per solve
+    br_np = synth.batch_maps(c, (rf, tf, pf)) if kb > 1 else c.br0((rf, tf, pf))
     s = Pot3d(rf, tf, pf, br_np, bc=c.bc, pc=c.pc, rank=rank, nranks=world,
-              pc2_blocks=args.pc2_blocks, unroll=32, variant=args.variant)  # fresh NCCL id inside
+              pc2_blocks=args.pc2_blocks, unroll=32, variant=args.variant, nrhs=kb)  # fresh NCCL id inside
+    lead = (kb,) if kb > 1 else ()
     s.trace(True)  # in-situ pass durations of the timed solves (%globaltimer, no extra launches)
     info = s.info()
     fixed_iters = args.weak_iters if args.config == "weak" else 0
@@ -262,10 +268,10 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     nbr = info["br_shells"]
-    phi_dev = torch.empty((c.np, c.nt, s.nr_loc), dtype=torch.float64, device=dev)
-    B_dev = (torch.empty((c.np, c.nt, nbr), dtype=torch.float64, device=dev),
-             torch.empty((c.np, c.nt + 1, s.nr_loc), dtype=torch.float64, device=dev),
-             torch.empty((c.np, c.nt, s.nr_loc), dtype=torch.float64, device=dev))
+    phi_dev = torch.empty(lead + (c.np, c.nt, s.nr_loc), dtype=torch.float64, device=dev)
+    B_dev = (torch.empty(lead + (c.np, c.nt, nbr), dtype=torch.float64, device=dev),
+             torch.empty(lead + (c.np, c.nt + 1, s.nr_loc), dtype=torch.float64, device=dev),
+             torch.empty(lead + (c.np, c.nt, s.nr_loc), dtype=torch.float64, device=dev))
     # pinned host buffers: the step's input (Br0) and its results (Phi, B)
     br_h = torch.from_numpy(br_np).pin_memory()
     phi_h = torch.empty(phi_dev.shape, dtype=torch.float64).pin_memory()
@@ -308,7 +314,7 @@ def main():
     barrier()
     w0 = time.perf_counter()
     for ev in evs:
-        iters.append(step(ev).iters)
+        iters.append(int(np.sum(step(ev).iters)))  # a batch: the iterations of all its problems
     barrier()
     wall = time.perf_counter() - w0
     clocks = clk.stop()
@@ -327,7 +333,7 @@ def main():
     # live durations of pass A / pass B inside the last timed solve (last <= 64 iterations);
     # PC1's pass B moves 24 B/cell on even and 40 B/cell on odd iterations (A23)
     k_it, k_ua, k_ub = s.kernel_trace()
-    n_live = len(k_it)
+    n_live = len(k_it) if kb == 1 else 0  # a batch's last iterations cover fewer problems: isolated
 
     # roofline of the dominant kernel: live durations from the timed solve; the
     # same passes launched separately between CUDA events are reported beside them
@@ -336,7 +342,7 @@ def main():
         ms_a_iso = ms_b_iso = ms_pc = 0.0
     else:
         ms_a_iso, ms_b_iso, ms_pc = s.profile(args.profile_iters)
-    cells_loc = s.nr_loc * c.nt * c.np
+    cells_loc = s.nr_loc * c.nt * c.np * kb  # per launch: a batch's passes cover its k problems
     pc1 = info["pc"] == 1
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -398,8 +404,10 @@ def main():
         "config": {
             "workload": workload_desc(c, args),
             "cells": c.n, "grid": [c.nr, c.nt, c.np], "rtol": rtol,
-            "iters_per_step": iters, "fixed_iters": bool(fixed_iters),
-            "step": "rhs(a2) + PCG solve to rtol (a3-a10) + finish + field B (a11)",
+            "iters_per_step": iters, "fixed_iters": bool(fixed_iters), "nrhs": kb,
+            "step": "rhs(a2) + PCG solve to rtol (a3-a10) + finish + field B (a11)" +
+                    (f" for each of the batch's {kb} problems in one loop; value counts the iterations "
+                     f"of every problem" if kb > 1 else ""),
             "parallelism": f"r-slabs x{world}" if world > 1 else "1 GPU",
             "l2": (f"inputs larger than L2: working set {ws / 1e9:.2f} GB per rank > 126 MB L2 (no flush)"
                    if ws > L2_BYTES else
@@ -407,7 +415,7 @@ def main():
         },
         "time_to_solve_s": ms / args.steps / 1e3,
         "cell_updates_per_s": c.n * value,
-        "loop_gbs_algorithmic": per_iter_bytes * world * value / 1e9,
+        "loop_gbs_algorithmic": per_iter_bytes / kb * world * value / 1e9,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic_of(c.name, dom.split(" ")[0]),

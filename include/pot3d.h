@@ -111,6 +111,19 @@ typedef struct {
   int32_t poly_degree;           /* PC3: Chebyshev steps m per apply (2..8); 0 -> 4 */
   double poly_ratio;             /* PC3: the polynomial targets [2/ratio, 2] of D^-1 A's
                                     spectrum (Saad Alg. 12.1); 0 -> 100 */
+  int32_t nrhs;                  /* > 1: a multi-RHS batch (MAS repeats
+                                    equivalent PCG solves): nrhs independent problems
+                                    on the same grid and BC (one boundary map each), solved
+                                    in ONE loop whose fused passes cover all of them per
+                                    launch (grid z = the problem), each with its own scalars
+                                    and convergence test; the loop ends when every problem
+                                    has stopped.  One rank, no loopback slabs, PC1, standard
+                                    PCG (else POT3D_ERR_INVALID).  br0, phi, br, bt, bp then
+                                    hold nrhs consecutive items of the single-problem layout
+                                    (item q at offset q * its size); iters, rel_residual,
+                                    true_rel_residual hold nrhs values; pot3d_history returns
+                                    problem 0's; the diagnostic applies are refused.
+                                    0/1: one problem */
 } pot3d_runtime;
 
 typedef struct {
@@ -129,7 +142,8 @@ typedef struct {
                                     2 peer memory (CUDA IPC over NVLink: the kernels store
                                     halo shells and sums straight into the peers' buffers) */
   int32_t chunks_a, chunks_b;    /* r-chunks per tile column of the two fused passes */
-  int32_t reserved;
+  int32_t nrhs;                  /* problems per solve (pot3d_runtime.nrhs; 1 unless a batch);
+                                    bytes_per_iter then counts all of them */
 } pot3d_info_t;
 
 /* Build the context: metric coefficients (a1), r-slab partition, RHS from
@@ -142,7 +156,10 @@ int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int
 /* Replace the boundary map (a2 re-run); the next pot3d_solve uses it. */
 int pot3d_set_br0(pot3d_ctx *ctx, const double *br0);
 
-/* PCG solve from x0 = 0 (A9).  phi (nullable): this rank's slab, layout above.
+/* PCG solve from x0 = 0 (A9).  phi (nullable): this rank's slab, layout above
+ * (a batch: nrhs consecutive slabs, and iters / rel_residual / true_rel_residual
+ * arrays of nrhs; the status is the first error, else NOT_CONVERGED if any problem
+ * hit maxit).
  * iters: completed alpha-updates; rel_residual: recurrence ||r||/||b||;
  * true_rel_residual (nullable): ||b - A x|| / ||b|| recomputed after the
  * solve.  maxit >= 1.  Returns POT3D_OK, POT3D_NOT_CONVERGED,
@@ -150,6 +167,18 @@ int pot3d_set_br0(pot3d_ctx *ctx, const double *br0);
  * Closed wall: Phi is returned in the zero volume-weighted-mean gauge. */
 int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t *iters,
                 double *rel_residual, double *true_rel_residual);
+
+/* Warm start -- repeated solves (MAS repeats equivalent PCG solves,
+ * P:33): the same PCG from a given x0 instead of 0 (r_0 = b - A x0; the stopping test
+ * stays ||r_k|| <= rtol ||b||, A9; iters counts this solve's iterations, 0 if x0
+ * already meets it; hist[0] = ||r_0|| / ||b||).  x0: the layout of phi (a batch: nrhs
+ * items), host or device, copied in; NULL = start from the context's last solution
+ * (kept across pot3d_set_br0 and pot3d_field -- the time-series use: a new map, the
+ * previous Phi; POT3D_ERR_STATE if a diagnostic call has run since).  One rank, no
+ * loopback slabs (POT3D_ERR_INVALID otherwise); b = 0 still returns Phi = 0.
+ * Outputs and status as pot3d_solve. */
+int pot3d_solve_from(pot3d_ctx *ctx, const double *x0, double rtol, int64_t maxit, double *phi,
+                     int64_t *iters, double *rel_residual, double *true_rel_residual);
 
 /* B = grad Phi of the last solution on staggered faces (a11, A16); nullable
  * outputs are skipped.  POT3D_ERR_STATE before a successful solve. */

@@ -18,6 +18,12 @@ Parity status of each function:
   pcg (CG1)        pinned: the same SPEC 2x2 / random SPD / brute-force pins,
                    and exact-arithmetic equivalence with the standard
                    variant (iterates agree to rounding, iterations +-1).
+  pcg (warm, X0)   pinned: x0 = 0 reproduces the cold loop bitwise; the SPEC 2x2
+                   from its exact solution stops at 0 iterations and from
+                   another x0 terminates in <= 2; on random SPD
+                   systems warm(x0) equals x0 + cold(b - A x0) with the
+                   tolerance rescaled (the same Krylov sequence, to rounding);
+                   a POT3D map solved from its own converged Phi stops at 0.
   cheb_apply (PC3) pinned: the closed form (I - R_m(D^-1 A)) A^-1 with the
                    Chebyshev residual polynomial on random SPD matrices.
   solve (PC1/PC2)  pinned: dense brute force, closed form, the survey's
@@ -69,6 +75,7 @@ _lib = None
 LINOP = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                          ctypes.POINTER(ctypes.c_double))
 STANDARD = 0   # orc_pcg variants: standard two-reduction PCG
+X0 = 16        # orc_pcg flag: x holds x0 on entry (warm start, A28)
 CG1 = 1        # Chronopoulos-Gear single-reduction PCG
 
 
@@ -214,14 +221,19 @@ def cheb_apply(A, inv_d, r, m, a, b=2.0):
 
 
 def solve(rf, tf, pf, br0, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1, rtol=1e-9, maxit=100000,
-          history=False, variant=STANDARD, poly=POLY_DEFAULT):
+          history=False, variant=STANDARD, poly=POLY_DEFAULT, x0=None):
     """Oracle PCG solve.  Returns dict(x, iters, rel_res, true_rel_res, status[, hist]).
     variant: STANDARD or CG1 (Chronopoulos-Gear).
-    pc: 1 Jacobi, 2 block ILU0, 3 Chebyshev-accelerated Jacobi (poly = (m, b/a))."""
+    pc: 1 Jacobi, 2 block ILU0, 3 Chebyshev-accelerated Jacobi (poly = (m, b/a)).
+    x0 (np, nt, nr): warm start from x0 instead of 0 (orc_pcg flag X0, A28)."""
     set_poly(*poly)
     rf, tf, pf, br0 = _f(rf), _f(tf), _f(pf), _f(br0)
     nr, nt, np_ = len(rf) - 1, len(tf) - 1, len(pf) - 1
-    x = np.zeros(nr * nt * np_)
+    x = np.zeros(nr * nt * np_) if x0 is None else _f(x0).reshape(-1).copy()
+    if x0 is not None:
+        if x.size != nr * nt * np_:
+            raise ValueError("x0 must have nr*nt*np entries")
+        variant = int(variant) | X0
     it = np.zeros(1, dtype=np.int64)
     rr = np.zeros(1)
     tr = np.zeros(1)
@@ -236,11 +248,11 @@ def solve(rf, tf, pf, br0, bc=SOURCE_SURFACE, pc=1, pc2_blocks=1, rtol=1e-9, max
     return out
 
 
-def pcg(A, b, rtol=1e-9, maxit=1000, minv=None, variant=STANDARD, history=False):
+def pcg(A, b, rtol=1e-9, maxit=1000, minv=None, variant=STANDARD, history=False, x0=None):
     """The oracle's PCG loop (orc_pcg) on a caller operator: A is a dense
     matrix or a callable x -> A x, minv (optional) a callable r -> M^-1 r.
     Used for the SPEC worked example and random SPD systems.
-    Returns dict(x, iters, rel_res, status[, hist])."""
+    x0: warm start (flag X0).  Returns dict(x, iters, rel_res, status[, hist])."""
     b = _f(b).reshape(-1)
     n = b.size
     fa = (lambda v: A @ v) if isinstance(A, np.ndarray) else A
@@ -253,7 +265,9 @@ def pcg(A, b, rtol=1e-9, maxit=1000, minv=None, variant=STANDARD, history=False)
         return LINOP(cb)
 
     ca, cm = wrap(fa), wrap(fm)
-    x = np.zeros(n)
+    x = np.zeros(n) if x0 is None else _f(x0).reshape(-1).copy()
+    if x0 is not None:
+        variant = int(variant) | X0
     it = np.zeros(1, dtype=np.int64)
     rr = np.zeros(1)
     hist = np.zeros(int(maxit) + 1) if history else None

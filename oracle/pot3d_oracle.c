@@ -587,11 +587,19 @@ static double dot(int64_t n, const double *x, const double *y) {
 /*         alpha = gamma'/den; gamma = gamma'.                               */
 /* In exact arithmetic both variants produce the same iterates.              */
 /*                                                                           */
+/* Flag ORC_PCG_X0 (or-ed into variant) -- warm start, the "repeated solves" */
+/* of SURVEY.md §8(f)-3 (MAS repeats equivalent PCG solves; DESIGN.md  */
+/* reading A28): x holds x0 on entry and the loop starts from r = b - A x0   */
+/* instead of x0 = 0, r = b; everything after that line is unchanged (the    */
+/* stopping test stays ||r|| <= rtol ||b||).  If x0 already meets it the     */
+/* solve stops with iters = 0; b = 0 still returns x = 0.            */
+/*                                                                           */
 /* status: 0 converged, 1 maxit reached, -4 indefinite.                      */
 /* hist (nullable, maxit+1 doubles): ||r_k||/||b|| for k = 0..iters.          */
 /* ------------------------------------------------------------------------ */
 #define ORC_PCG_STANDARD 0
 #define ORC_PCG_CG1 1
+#define ORC_PCG_X0 16
 
 int orc_pcg(int64_t N, orc_linop A, void *actx, orc_linop Minv, void *mctx, const double *b,
             double rtol, int64_t maxit, int variant, double *x, int64_t *iters,
@@ -602,13 +610,25 @@ int orc_pcg(int64_t N, orc_linop A, void *actx, orc_linop Minv, void *mctx, cons
   double *q = malloc(sizeof(double) * N);  /* q = A p (standard) / w = A u (CG1) */
   double *s = variant == ORC_PCG_CG1 ? malloc(sizeof(double) * N) : NULL;
   int status = 0, conv = 0;
-  for (int64_t m = 0; m < N; m++) { x[m] = 0.0; r[m] = b[m]; }
+  const int warm = (variant & ORC_PCG_X0) != 0;
+  variant &= ~ORC_PCG_X0;
+  if (warm) {                        /* r = b - A x0 */
+    A(actx, x, r);
+    for (int64_t m = 0; m < N; m++) r[m] = b[m] - r[m];
+  } else {
+    for (int64_t m = 0; m < N; m++) { x[m] = 0.0; r[m] = b[m]; }
+  }
   const double bnorm = sqrt(dot(N, b, b));
   int64_t k = 0;
-  double rnorm = bnorm;
-  if (hist) hist[0] = bnorm > 0 ? 1.0 : 0.0;
+  double rnorm = warm ? sqrt(dot(N, r, r)) : bnorm;
+  if (hist) hist[0] = bnorm > 0 ? rnorm / bnorm : 0.0;
   if (bnorm == 0.0) { /* b = 0 -> Phi = 0 */
+    for (int64_t m = 0; m < N; m++) x[m] = 0.0;
     *iters = 0; *rel_res = 0.0;
+    goto done;
+  }
+  if (warm && rnorm <= rtol * bnorm) { /* x0 already meets the test */
+    *iters = 0; *rel_res = rnorm / bnorm;
     goto done;
   }
   const double t_loop = now_s();

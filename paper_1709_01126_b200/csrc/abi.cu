@@ -32,6 +32,7 @@ struct pot3d_ctx {
   bool pdl = true;    // programmatic dependent launch for the loop kernels (POT3D_PDL=0: off)
   int edge_blocks = 148 * 4;  // grid of the edge-shell kernel (POT3D_EDGE_BLOCKS)
   bool edge_in_a = true;      // pass A's first block row builds the edge shells (POT3D_EDGE_IN_A=0: kernel)
+  int pcj = 1, pck = 1;       // fused passes: clusters of pcj x pck neighbouring tiles (POT3D_CLUSTER)
   int device = 0;
   double r0 = 1.0;
   Grid G{};
@@ -95,8 +96,19 @@ struct pot3d_ctx {
   std::vector<pot3d_ctx *> slabs;
   bool member = false;  // a slab context of a loopback group (no NCCL)
   std::vector<pot3d_ctx *> *group = nullptr;  // member: the group's slab list
+  // multi-RHS batch (pot3d_runtime.nrhs = k > 1): this context is the
+  // batch handle and `rhs` are k single-problem contexts on its stream whose x, r, p
+  // vectors and scalars are stacked (rhs[q] at offset q), so one TMA descriptor and one
+  // launch of each fused pass cover the batch (blockIdx.z = RHS).  rhs[0] (nrhs = k)
+  // owns the graph, the per-RHS partials of the batched passes and the stacked histories.
+  std::vector<pot3d_ctx *> rhs;
+  int nrhs = 1;
+  double *zpartials = nullptr;
+  size_t zpart_len = 0;
   // state
   bool solved = false;
+  bool has_x = false;  // x holds the last solve's Phi (a warm start may begin from it)
+  bool warm = false;   // the next solve_begin starts from x0 = the current x (pot3d_solve_from)
   int64_t last_iters = 0;
   std::string err;
 };
@@ -208,6 +220,36 @@ cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_
   cfg.attrs = pdl ? at : nullptr;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+// A fused pass (k_pass_a*, k_pass_b_*): grid.x becomes the tile count of a.G (padded to
+// whole clusters) and the launch carries the cluster dimension a.G.cj * a.G.ck.
+cudaError_t launch_pass(bool pdl, void (*k)(const TMaps, PassArgs, int), dim3 grid, size_t smem,
+                        cudaStream_t s, const TMaps &T, const PassArgs &a, int parity) {
+  cudaLaunchConfig_t cfg = {};
+  grid.x = pass_tiles(a.G);
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    n++;
+  }
+  const int cs = std::max(a.G.cj, 1) * std::max(a.G.ck, 1);
+  if (cs > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cs;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    n++;
+  }
+  cfg.attrs = n ? at : nullptr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, k, T, a, parity);
 }
 
 bool is_device_ptr(const void *p) {
@@ -402,7 +444,8 @@ int make_map(pot3d_ctx *ctx, CUtensorMap *m, double *base, unsigned b0, unsigned
     return POT3D_ERR_CUDA;
   }
   const Grid &G = ctx->G;
-  cuuint64_t dims[3] = {(cuuint64_t)G.PK, (cuuint64_t)G.nt, (cuuint64_t)G.nr_loc + 2};
+  // a batch leader's descriptors span the k stacked vectors (nr_loc + 2 planes each)
+  cuuint64_t dims[3] = {(cuuint64_t)G.PK, (cuuint64_t)G.nt, (cuuint64_t)(G.nr_loc + 2) * ctx->nrhs};
   cuuint64_t strides[2] = {(cuuint64_t)G.PK * 8, (cuuint64_t)G.plane * 8};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t es[3] = {1, 1, 1};
@@ -443,6 +486,8 @@ int make_maps(pot3d_ctx *ctx) {
 PassArgs make_args(pot3d_ctx *ctx, int parity) {
   PassArgs a{};
   a.G = ctx->G;
+  a.G.cj = ctx->pcj;
+  a.G.ck = ctx->pck;
   a.M = ctx->M;
   a.S = ctx->S;
   a.r = ctx->r;
@@ -455,6 +500,11 @@ PassArgs make_args(pot3d_ctx *ctx, int parity) {
   a.hist = ctx->hist;
   a.finalize = ctx->nranks == 1 ? 1 : 0;
   a.local_sum = ctx->local_sum;
+  if (ctx->nrhs > 1) {  // batch leader: per-RHS partials and histories (pass_common.cuh)
+    a.partials = ctx->zpartials;
+    a.pstride = (long long)ctx->zpart_len;
+    a.hstride = ctx->hist_len;
+  }
   return a;
 }
 
@@ -607,8 +657,7 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
   };
   auto pass_b = [ctx, grdb, parity](PassArgs bx) -> Step {
     return [=]() -> int {
-      CK(launch_k(ctx->pdl, kern_b(ctx, parity), grdb, dim3(NTHREADS), SMEM_B, ctx->stream, ctx->tmaps, bx,
-                  parity));
+      CK(launch_pass(ctx->pdl, kern_b(ctx, parity), grdb, SMEM_B, ctx->stream, ctx->tmaps, bx, parity));
       MARK("passB");
       ctx->n_enq++;
       return 0;
@@ -628,8 +677,8 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
     // 84.9 us per iteration with 3 chunks vs 89.1 with the single-GPU choice of 1
     if (ax.G.nchunks < 3 && G.nr_loc >= 6) ax.G.nchunks = 3;
     st.push_back([=]() -> int {
-      CK(launch_k(ctx->pdl, kern_a(ctx), dim3(G.ntj * G.ntk, ax.G.nchunks + 1), dim3(NTHREADS), SMEM_A,
-                  ctx->stream, ctx->tmaps, ax, parity));
+      CK(launch_pass(ctx->pdl, kern_a(ctx), dim3(0, ax.G.nchunks + 1), SMEM_A, ctx->stream, ctx->tmaps, ax,
+                     parity));
       MARK("passA");
       ctx->n_enq++;
       return 0;
@@ -652,7 +701,7 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
   PassArgs ax = a;
   ax.G.part = 3;
   st.push_back([=]() -> int {
-    CK(launch_k(ctx->pdl, kern_a(ctx), grd, dim3(NTHREADS), SMEM_A, ctx->stream, ctx->tmaps, ax, parity));
+    CK(launch_pass(ctx->pdl, kern_a(ctx), grd, SMEM_A, ctx->stream, ctx->tmaps, ax, parity));
     MARK("passA");
     ctx->n_enq++;
     return 0;
@@ -723,10 +772,10 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   }
   const Grid &G = ctx->G;
   PassArgs a = make_args(ctx, parity);
-  dim3 grd(G.ntj * G.ntk, G.nchunks);
+  dim3 grd(G.ntj * G.ntk, G.nchunks, ctx->nrhs);  // batch: blockIdx.z = right-hand side
   PassArgs ab = a;  // pass B: its own r-chunking
   ab.G.nchunks = ctx->nchunks_b;
-  dim3 grdb(G.ntj * G.ntk, ctx->nchunks_b);
+  dim3 grdb(G.ntj * G.ntk, ctx->nchunks_b, ctx->nrhs);
   const bool pc2 = ctx->pc == 2;
   const bool multi = ctx->nranks > 1;
   if (ctx->xfer) {
@@ -751,7 +800,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     TRY(halo_exchange(ctx, ctx->P[parity ^ 1], ctx->comm_stream));
     CK(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
     const int nci = std::max(1, std::min(G.nchunks, G.nr_loc - 2));
-    const int ntl = G.ntj * G.ntk;
+    const int ntl = pass_tiles(a.G);
     PassArgs ai = a, ae = a;
     ai.G.part = 1;
     ai.G.nchunks = nci;
@@ -760,14 +809,12 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     ae.G.part = 2;
     ae.G.blk_off = ntl * nci;
     ae.G.blk_total = ntl * (nci + 2);
-    CK(launch_k(false, kern_a(ctx), dim3(ntl, nci), dim3(NTHREADS), SMEM_A, ctx->stream, ctx->tmaps, ai,
-                parity));
+    CK(launch_pass(false, kern_a(ctx), dim3(ntl, nci), SMEM_A, ctx->stream, ctx->tmaps, ai, parity));
     ctx->n_enq++;
     MARK("passA_interior");
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
     MARK("halo_wait");
-    CK(launch_k(false, kern_a(ctx), dim3(ntl, 2), dim3(NTHREADS), SMEM_A, ctx->stream, ctx->tmaps, ae,
-                parity));
+    CK(launch_pass(false, kern_a(ctx), dim3(ntl, 2), SMEM_A, ctx->stream, ctx->tmaps, ae, parity));
     ctx->n_enq++;
     MARK("passA_edge");
   } else {
@@ -779,8 +826,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
       ctx->n_enq++;
       TRY(halo_exchange(ctx, ctx->P[parity ^ 1]));
     }
-    CK(launch_k(ctx->pdl && !multi, kern_a(ctx), grd, dim3(NTHREADS), SMEM_A,
-                ctx->stream, ctx->tmaps, a, parity));
+    CK(launch_pass(ctx->pdl && !multi, kern_a(ctx), grd, SMEM_A, ctx->stream, ctx->tmaps, a, parity));
     ctx->n_enq++;
   }
   if (multi) {
@@ -791,8 +837,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     ctx->n_enq++;
     MARK("finalize_alpha");
   }
-  CK(launch_k(ctx->pdl && !multi, kern_b(ctx, parity), grdb, dim3(NTHREADS), SMEM_B,
-              ctx->stream, ctx->tmaps, ab, parity));
+  CK(launch_pass(ctx->pdl && !multi, kern_b(ctx, parity), grdb, SMEM_B, ctx->stream, ctx->tmaps, ab, parity));
     ctx->n_enq++;
   MARK("passB");
   if (multi) {
@@ -996,14 +1041,44 @@ int ensure_hist(pot3d_ctx *ctx, int64_t maxit, bool &stale) {
   return 0;
 }
 
+// batch: one buffer of k histories (stride hist_len, the passes' hstride)
+int ensure_hist_batch(pot3d_ctx *lead, std::vector<pot3d_ctx *> &M, int64_t maxit, bool &stale) {
+  pot3d_ctx *ctx = lead;
+  const int64_t hlen = std::min<int64_t>(maxit + 1, (int64_t)1 << 24);
+  if (hlen > lead->hist_len) {
+    double *h = nullptr;
+    TRY(dalloc(lead, &h, (size_t)hlen * M.size()));
+    for (size_t q = 0; q < M.size(); q++) {
+      M[q]->hist = h + q * hlen;
+      M[q]->hist_len = hlen;
+    }
+    stale = true;
+  }
+  return 0;
+}
+
+struct PinnedScalars {  // pinned host mirror of n device scalar blocks, freed on every path
+  Scalars *p = nullptr;
+  ~PinnedScalars() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
 int build_graph_group(pot3d_ctx *h);
 
-// x0 = 0, r = b, p = 0 (A9), the device scalars, PC2: z0 = M^-1 b, local init sums
+// x0 = 0, r = b, p = 0 (A9), the device scalars, PC2: z0 = M^-1 b, local init sums.
+// Warm start (ctx->warm, pot3d_solve_from): x holds x0 (interior cells), r = b - A x0.
 int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit) {
   const Grid &G = ctx->G;
   cudaStream_t s = ctx->stream;
   const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
-  CK(cudaMemsetAsync(ctx->x, 0, cells * sizeof(double), s));
+  const bool warm = ctx->warm;
+  if (!warm) {
+    CK(cudaMemsetAsync(ctx->x, 0, cells * sizeof(double), s));
+  } else {  // the ghost shells of x0 are zero for the apply (the BCs are folded, A7)
+    CK(cudaMemsetAsync(ctx->x + sidx(G, -1), 0, G.plane * sizeof(double), s));
+    CK(cudaMemsetAsync(ctx->x + sidx(G, G.nr_loc), 0, G.plane * sizeof(double), s));
+  }
   CK(cudaMemsetAsync(ctx->r, 0, cells * sizeof(double), s));
   CK(cudaMemsetAsync(ctx->P[0], 0, cells * sizeof(double), s));
   CK(cudaMemsetAsync(ctx->P[1], 0, cells * sizeof(double), s));
@@ -1026,7 +1101,18 @@ int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit) {
   h0.maxit = (long long)maxit;  // the history keeps the first hist_len entries
   h0.hist_len = ctx->hist_len;
   CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
-  // z0 = M^-1 b, rho0 = b.z0, ||b|| (a10 init)
+  if (warm) {
+    // ||b|| from r = b (the stopping test stays relative to b, A9), then r = b - A x0
+    // over every cell and its periodic ghost columns (a stencil operand of pass A)
+    k_init_dots<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, ctx->partials, 1, ctx->local_sum, 0,
+                                        nullptr, 0, nullptr);
+    k_apply<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->x, ctx->r, ctx->bshell, G.i0 == 0 ? 0 : -1000, nullptr,
+                                    nullptr, nullptr);
+    k_fix_ghost_cols<<<(G.nr_loc * ctx->nt + 255) / 256, 256, 0, s>>>(G, ctx->r, 0, G.nr_loc);
+    CK(cudaGetLastError());
+    ctx->n_launch += 3;
+  }
+  // z0 = M^-1 r0, rho0 = r0.z0, ||b|| (a10 init)
   if (ctx->pc == 2) {
     int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
                        s, false);
@@ -1036,7 +1122,8 @@ int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit) {
   }
   if (ctx->pc == 3) TRY(poly_apply(ctx, 0, false));  // z0 = M^-1 b
   k_init_dots<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, ctx->partials, ctx->nranks == 1,
-                                      ctx->local_sum, ctx->pc >= 2, ctx->z);
+                                      ctx->local_sum, ctx->pc >= 2, ctx->z, warm ? 1 : 0,
+                                      warm ? ctx->hist : nullptr);
   CK(cudaGetLastError());
   ctx->n_launch++;
   if (ctx->pc == 1) {
@@ -1056,7 +1143,9 @@ int solve_init_end(pot3d_ctx *ctx) {
     CK(cudaGetLastError());
     ctx->n_launch++;
   }
-  if (ctx->hist) {
+  if (ctx->warm) {  // hist[0] = ||r_0|| / ||b|| was written by k_init_dots
+    ctx->warm = false;
+  } else if (ctx->hist) {
     double one = 1.0;
     CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
   }
@@ -1139,11 +1228,15 @@ int loop_status(pot3d_ctx *ctx, pot3d_ctx *rep) {
 int solve_run(pot3d_ctx *h, std::vector<pot3d_ctx *> &M, double rtol, int64_t maxit) {
   pot3d_ctx *ctx = h;
   cudaStream_t s = h->stream;
+  const bool batch = h->nrhs > 1;  // h: the batch leader, M: its k problems
   bool stale = false;
-  for (pot3d_ctx *m : M) TRY(ensure_hist(m, maxit, stale));
-  if (stale) TRY(M.size() > 1 ? build_graph_group(h) : build_graph(h));  // graph captured the old hist
+  if (batch)
+    TRY(ensure_hist_batch(h, M, maxit, stale));
+  else
+    for (pot3d_ctx *m : M) TRY(ensure_hist(m, maxit, stale));
+  if (stale) TRY(M.size() > 1 && !batch ? build_graph_group(h) : build_graph(h));  // graph captured the old hist
   for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit));
-  if (M.size() > 1 || M[0]->nranks > 1) TRY(gather_all(M));
+  if (!batch && (M.size() > 1 || M[0]->nranks > 1)) TRY(gather_all(M));
   for (pot3d_ctx *m : M) TRY(solve_init_end(m));
   if (M[0]->variant == 1) {  // CG1: w_0 = A u_0, delta_0 -> alpha_0 (the same steps, phase by phase)
     std::vector<std::vector<Step>> st;
@@ -1158,18 +1251,26 @@ int solve_run(pot3d_ctx *h, std::vector<pot3d_ctx *> &M, double rtol, int64_t ma
       }
   }
   pot3d_ctx *m0 = M[0];
-  CK(cudaMemcpyAsync(m0->hS, m0->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  // the stop flags: one scalar block, or the leader's k stacked blocks of a batch (the
+  // loop runs until every right-hand side has stopped; a stopped one's blocks return)
+  const int nS = batch ? h->nrhs : 1;
+  PinnedScalars hs2;
+  CK(cudaMallocHost(&hs2.p, 3 * nS * sizeof(Scalars)));
+  auto all_stop = [nS](const Scalars *v) {
+    for (int q = 0; q < nS; q++)
+      if (!v[q].stop) return false;
+    return true;
+  };
+  CK(cudaMemcpyAsync(hs2.p + 2 * nS, m0->S, nS * sizeof(Scalars), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   int64_t launched = 0;
-  if (!m0->hS->stop) {
+  if (!all_stop(hs2.p + 2 * nS)) {
     cudaEvent_t ev[2];
-    Scalars *hs2 = nullptr;
-    CK(cudaMallocHost(&hs2, 2 * sizeof(Scalars)));
     cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
     CK(cudaGraphLaunch(h->gexec, s));
     h->n_launch += h->graph_nodes;
-    CK(cudaMemcpyAsync(&hs2[0], m0->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs2.p, m0->S, nS * sizeof(Scalars), cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(ev[0], s));
     launched++;
     int cur = 0;
@@ -1178,18 +1279,17 @@ int solve_run(pot3d_ctx *h, std::vector<pot3d_ctx *> &M, double rtol, int64_t ma
       if (more) {
         CK(cudaGraphLaunch(h->gexec, s));
         h->n_launch += h->graph_nodes;
-        CK(cudaMemcpyAsync(&hs2[cur ^ 1], m0->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hs2.p + (cur ^ 1) * nS, m0->S, nS * sizeof(Scalars), cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(ev[cur ^ 1], s));
         launched++;
       }
       CK(cudaEventSynchronize(ev[cur]));
-      if (hs2[cur].stop || !more) break;
+      if (all_stop(hs2.p + cur * nS) || !more) break;
       cur ^= 1;
     }
     CK(cudaStreamSynchronize(s));
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
-    cudaFreeHost(hs2);
   }
   for (pot3d_ctx *m : M) {
     CK(cudaMemcpyAsync(m->hS, m->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
@@ -1253,6 +1353,20 @@ int pot3d_nccl_unique_id(void *out128) {
 
 int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   if (!ctx || !info) return POT3D_ERR_INVALID;
+  if (!ctx->rhs.empty()) {  // batch: the leader's geometry, the batch's bytes and launches
+    pot3d_info(ctx->rhs[0], info);
+    info->bytes_per_iter *= (int64_t)ctx->rhs.size();
+    info->device_bytes = (int64_t)ctx->dev_bytes;
+    info->kernel_launches = 0;
+    pot3d_info_t mi{};
+    for (const pot3d_ctx *m : ctx->rhs) {
+      pot3d_info(m, &mi);
+      info->device_bytes += mi.device_bytes;
+      info->kernel_launches += mi.kernel_launches;
+    }
+    info->nrhs = (int32_t)ctx->rhs.size();
+    return 0;
+  }
   if (!ctx->slabs.empty()) {  // loopback group: the whole grid on one device
     pot3d_info_t mi{};
     *info = pot3d_info_t{};
@@ -1273,6 +1387,7 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
     info->exchange = 3;  // peer-memory exchange between the slabs of one device
     info->chunks_a = ctx->slabs[0]->G.nchunks;
     info->chunks_b = ctx->slabs[0]->nchunks_b;
+    info->nrhs = 1;
     return 0;
   }
   info->i0 = ctx->G.i0;
@@ -1298,12 +1413,23 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   info->exchange = ctx->nranks == 1 ? 0 : (ctx->xfer ? 2 : 1);
   info->chunks_a = ctx->G.nchunks;
   info->chunks_b = ctx->nchunks_b;
-  info->reserved = 0;
+  info->nrhs = 1;
   return 0;
 }
 
 int pot3d_set_br0(pot3d_ctx *ctx, const double *br0) {
   if (!ctx || !br0) return POT3D_ERR_INVALID;
+  if (!ctx->rhs.empty()) {  // batch: k consecutive maps
+    for (size_t q = 0; q < ctx->rhs.size(); q++) {
+      int rc = pot3d_set_br0(ctx->rhs[q], br0 + q * (size_t)ctx->nt * ctx->np);
+      if (rc) {
+        ctx->err = ctx->rhs[q]->err;
+        return rc;
+      }
+    }
+    ctx->solved = false;
+    return 0;
+  }
   if (!ctx->slabs.empty()) {
     for (pot3d_ctx *m : ctx->slabs) {
       int rc = pot3d_set_br0(m, br0);
@@ -1350,8 +1476,15 @@ int pot3d_set_br0(pot3d_ctx *ctx, const double *br0) {
   return 0;
 }
 
+// batch member (setup_batch): its slices of the handle's stacked vectors and scalars
+struct BatchSlot {
+  double *x, *r, *P0, *P1;
+  Scalars *S;
+};
+
 static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int32_t pc,
-                     const pot3d_runtime *rt, pot3d_ctx **out, bool member) {
+                     const pot3d_runtime *rt, pot3d_ctx **out, bool member,
+                     const BatchSlot *slot = nullptr) {
   if (!out) return POT3D_ERR_INVALID;
   *out = nullptr;
   pot3d_ctx *ctx = new pot3d_ctx();
@@ -1412,6 +1545,10 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
     ctx->pdl = !(e && atoi(e) == 0);
     const char *eb = getenv("POT3D_EDGE_BLOCKS");
     if (eb && atoi(eb) > 0) ctx->edge_blocks = atoi(eb);
+    const char *ec = getenv("POT3D_CLUSTER");  // "JxK": clusters of J x K tiles for the fused passes
+    if (ec && sscanf(ec, "%dx%d", &ctx->pcj, &ctx->pck) != 2) ctx->pcj = ctx->pck = 1;
+    ctx->pcj = std::max(1, std::min(ctx->pcj, 8));
+    ctx->pck = std::max(1, std::min(ctx->pck, 8 / ctx->pcj));
     const char *ea = getenv("POT3D_EDGE_IN_A");
     // loopback slabs: the separate edge-shell kernel (no spin on a sibling's blocks
     // inside one launch)
@@ -1538,7 +1675,12 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
 
   // vectors with ghost shells
   const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
-  DA(ctx->x, cells); DA(ctx->r, cells);
+  if (slot) {
+    ctx->x = slot->x;
+    ctx->r = slot->r;
+  } else {
+    DA(ctx->x, cells); DA(ctx->r, cells);
+  }
   {
     const char *xe = getenv("POT3D_XFER");
     ctx->xfer_want = member || (ctx->nranks > 1 && ctx->nranks <= MAXR && !(xe && atoi(xe) == 0));
@@ -1548,6 +1690,9 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
         (rc = ipc_alloc(ctx, &ctx->mail, 1)))
       return fail(rc);
     if (cudaMemsetAsync(ctx->mail, 0, sizeof(Mailbox), ctx->stream)) { ctx->err = "memset"; return fail(POT3D_ERR_CUDA); }
+  } else if (slot) {
+    ctx->P[0] = slot->P0;
+    ctx->P[1] = slot->P1;
   } else {
     DA(ctx->P[0], cells); DA(ctx->P[1], cells);
   }
@@ -1569,9 +1714,15 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
     }
   }
   DA(ctx->bshell, G.plane + 16); DA(ctx->br_dev, G.plane + 16); DA(ctx->mean2, 2);
-  DA(ctx->S, 1);
+  if (slot)
+    ctx->S = slot->S;
+  else
+    DA(ctx->S, 1);
+  Grid Gc = G;  // the fused passes' tile count (clusters pad it)
+  Gc.cj = ctx->pcj;
+  Gc.ck = ctx->pck;
   ctx->partials_len = 4 * (size_t)std::max<long long>(
-      (long long)G.ntj * G.ntk * (std::max(G.nchunks, ctx->nchunks_b) + 3), 65536);
+      (long long)pass_tiles(Gc) * (std::max(G.nchunks, ctx->nchunks_b) + 3), 65536);
   DA(ctx->partials, ctx->partials_len);
   DA(ctx->local_sum, 4);
   DA(ctx->gathered, 4 * (size_t)ctx->nranks + 4);  // 2 (PCG) or 4 (CG1) doubles per rank
@@ -1627,7 +1778,7 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   {
     int rc2 = make_maps(ctx);
     if (rc2) return fail(rc2);
-    if (!member) rc2 = build_graph(ctx);  // loopback: one graph for the whole group
+    if (!member && !slot) rc2 = build_graph(ctx);  // loopback / batch: the group's graph
     if (rc2) return fail(rc2);
   }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
@@ -1740,28 +1891,117 @@ static int setup_group(const pot3d_grid *grid, const double *br0, int32_t outer_
   return 0;
 }
 
+// Multi-RHS batch (pot3d_runtime.nrhs = k > 1): k single-problem contexts on the
+// handle's stream over one stacked allocation of x, r, p_0, p_1 and the scalars; the
+// leader rhs[0] launches each fused pass once for all k (grid z = k).
+static int setup_batch(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int32_t pc,
+                       const pot3d_runtime *rt, pot3d_ctx **out) {
+  *out = nullptr;
+  const int k = rt->nrhs;
+  pot3d_ctx *h = new pot3d_ctx();
+  pot3d_ctx *ctx = h;
+  auto fail = [&](int rc) {
+    g_setup_error = h->err;
+    for (pot3d_ctx *m : h->rhs) pot3d_destroy(m);
+    h->rhs.clear();
+    dfree_all(h);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return rc;
+  };
+  if (!grid || !br0 || !grid->r_faces || !grid->t_faces || !grid->p_faces || grid->nr < 2 || grid->nt < 2 ||
+      grid->np < 2) {
+    h->err = "null argument or cell counts < 2 (S:45)";
+    return fail(POT3D_ERR_INVALID);
+  }
+  if (rt->nranks > 1 || rt->loopback_slabs > 1 || pc != POT3D_PC1 || rt->variant != 0 || k > 65535) {
+    h->err = "nrhs > 1 runs on one rank (no loopback slabs) with PC1 and standard PCG, nrhs <= 65535";
+    return fail(POT3D_ERR_INVALID);
+  }
+  h->nr = grid->nr;
+  h->nt = grid->nt;
+  h->np = grid->np;
+  h->bc = outer_bc;
+  h->pc = h->pc_req = pc;
+  h->ualloc = rt->alloc;
+  h->ufree = rt->free;
+  h->actx = rt->alloc_ctx;
+  if (rt->device >= 0)
+    h->device = rt->device;
+  else
+    cudaGetDevice(&h->device);
+  if (cudaSetDevice(h->device) != cudaSuccess) {
+    h->err = "cudaSetDevice failed";
+    return fail(POT3D_ERR_CUDA);
+  }
+  if (rt->cuda_stream) {
+    h->stream = (cudaStream_t)rt->cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamDefault) != cudaSuccess) {
+      h->err = "cudaStreamCreate failed";
+      return fail(POT3D_ERR_CUDA);
+    }
+    h->own_stream = true;
+  }
+  // the single-problem layout (setup_one): PK physical columns, nr + 2 planes
+  const long long PK = round_up(h->np + COFF + 1, 16);
+  const size_t cells = (size_t)(h->nr + 2) * h->nt * PK;
+  double *X = nullptr, *R = nullptr, *P0 = nullptr, *P1 = nullptr;
+  Scalars *S = nullptr;
+  int rc = 0;
+  if ((rc = dalloc(h, &X, cells * k)) || (rc = dalloc(h, &R, cells * k)) || (rc = dalloc(h, &P0, cells * k)) ||
+      (rc = dalloc(h, &P1, cells * k)) || (rc = dalloc(h, &S, (size_t)k)))
+    return fail(rc);
+  const size_t nmap = (size_t)h->nt * h->np;
+  for (int q = 0; q < k; q++) {
+    BatchSlot sl{X + q * cells, R + q * cells, P0 + q * cells, P1 + q * cells, S + q};
+    pot3d_runtime Rq = *rt;
+    Rq.nrhs = 1;
+    Rq.device = h->device;
+    Rq.cuda_stream = h->stream;
+    pot3d_ctx *m = nullptr;
+    rc = setup_one(grid, br0 + q * nmap, outer_bc, pc, &Rq, &m, false, &sl);
+    if (rc) {
+      h->err = "RHS " + std::to_string(q) + ": " + g_setup_error;
+      return fail(rc);
+    }
+    h->rhs.push_back(m);
+  }
+  pot3d_ctx *lead = h->rhs[0];
+  lead->nrhs = k;
+  lead->zpart_len = lead->partials_len;
+  if ((rc = dalloc(lead, &lead->zpartials, lead->partials_len * k))) {
+    h->err = lead->err;
+    return fail(rc);
+  }
+  if ((rc = make_maps(lead)) || (rc = build_graph(lead))) {
+    h->err = lead->err;
+    return fail(rc);
+  }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
+    h->err = std::string("batch setup: ") + cudaGetErrorString(cudaGetLastError());
+    return fail(POT3D_ERR_CUDA);
+  }
+  *out = h;
+  return 0;
+}
+
 int pot3d_setup(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int32_t pc,
                 const pot3d_runtime *rt, pot3d_ctx **out) {
   if (!out) return POT3D_ERR_INVALID;
+  if (rt && rt->nrhs > 1) return setup_batch(grid, br0, outer_bc, pc, rt, out);
   if (rt && rt->loopback_slabs > 1) return setup_group(grid, br0, outer_bc, pc, rt, out);
   return setup_one(grid, br0, outer_bc, pc, rt, out, false);
 }
 
-int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t *iters,
-                double *rel_residual, double *true_rel_residual) {
-  if (!ctx) return POT3D_ERR_INVALID;
-  if (!(rtol >= 0.0) || maxit < 1) {
-    ctx->err = "rtol must be >= 0 and maxit >= 1";
-    return POT3D_ERR_INVALID;
-  }
-  CK(cudaSetDevice(ctx->device));
-  std::vector<pot3d_ctx *> M = members(ctx);
-  for (pot3d_ctx *m : M) m->solved = false;
-  ctx->solved = false;
-  int rc = solve_run(ctx, M, rtol, maxit);
-  if (rc < 0) return rc;
+// after the loop: the deferred x update, the closed-wall gauge, the true residual, Phi
+// to the user and the status (one problem: one context, or the slabs of a group)
+static int finish_solve(pot3d_ctx *ctx, std::vector<pot3d_ctx *> &M, double *phi, int64_t *iters,
+                        double *rel_residual, double *true_rel_residual) {
   const Scalars hs = *M[0]->hS;
   cudaStream_t s = ctx->stream;
+  if (!(hs.bnorm > 0))  // b = 0 -> Phi = 0, also from a warm start's x0
+    for (pot3d_ctx *m : M) CK(cudaMemsetAsync(m->x, 0, (size_t)(m->G.nr_loc + 2) * m->G.plane * sizeof(double), s));
   const int nbi = 148 * 4;
   for (pot3d_ctx *m : M) {
     // PC1 defers the x update of even iterations to the next (odd) pass B (A23): when the
@@ -1810,18 +2050,101 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
   ctx->last_iters = hs.iter;
   for (pot3d_ctx *m : M) {
     m->last_iters = hs.iter;
-    m->solved = true;
+    m->solved = m->has_x = true;
   }
-  ctx->solved = true;
+  ctx->solved = ctx->has_x = true;
   // a fallen-back solve that did not converge reports NOT_CONVERGED; the fallback
   // itself stays visible through pot3d_info().pc != the requested pc
   if (hs.status == 1) return POT3D_NOT_CONVERGED;
   return ctx->pc != ctx->pc_req ? POT3D_PC2_FELL_BACK : POT3D_OK;
 }
 
+// a batch: one loop for all k problems, then each finished as a single problem with its
+// slice of the outputs; the status is the first error, else NOT_CONVERGED if any hit maxit
+static int solve_batch(pot3d_ctx *h, double rtol, int64_t maxit, double *phi, int64_t *iters,
+                       double *rel_residual, double *true_rel_residual) {
+  pot3d_ctx *ctx = h;
+  CK(cudaSetDevice(h->device));
+  std::vector<pot3d_ctx *> &M = h->rhs;
+  for (pot3d_ctx *m : M) m->solved = m->has_x = false;
+  int rc = solve_run(M[0], M, rtol, maxit);
+  if (rc < 0) {
+    h->err = M[0]->err;
+    return rc;
+  }
+  const long long ncell = (long long)h->nr * h->nt * h->np;
+  int worst = POT3D_OK;
+  for (size_t q = 0; q < M.size(); q++) {
+    std::vector<pot3d_ctx *> one{M[q]};
+    rc = finish_solve(M[q], one, phi ? phi + q * ncell : nullptr, iters ? iters + q : nullptr,
+                      rel_residual ? rel_residual + q : nullptr,
+                      true_rel_residual ? true_rel_residual + q : nullptr);
+    if (rc < 0) {
+      h->err = M[q]->err;
+      return rc;
+    }
+    if (rc == POT3D_NOT_CONVERGED) worst = rc;
+  }
+  h->last_iters = M[0]->last_iters;
+  h->solved = true;
+  return worst;
+}
+
+int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t *iters,
+                double *rel_residual, double *true_rel_residual) {
+  if (!ctx) return POT3D_ERR_INVALID;
+  if (!(rtol >= 0.0) || maxit < 1) {
+    ctx->err = "rtol must be >= 0 and maxit >= 1";
+    return POT3D_ERR_INVALID;
+  }
+  if (!ctx->rhs.empty()) return solve_batch(ctx, rtol, maxit, phi, iters, rel_residual, true_rel_residual);
+  CK(cudaSetDevice(ctx->device));
+  std::vector<pot3d_ctx *> M = members(ctx);
+  for (pot3d_ctx *m : M) m->solved = m->has_x = false;
+  ctx->solved = ctx->has_x = false;
+  int rc = solve_run(ctx, M, rtol, maxit);
+  if (rc < 0) return rc;
+  return finish_solve(ctx, M, phi, iters, rel_residual, true_rel_residual);
+}
+
+int pot3d_solve_from(pot3d_ctx *ctx, const double *x0, double rtol, int64_t maxit, double *phi, int64_t *iters,
+                     double *rel_residual, double *true_rel_residual) {
+  if (!ctx) return POT3D_ERR_INVALID;
+  if (ctx->nranks > 1 || !ctx->slabs.empty()) {
+    ctx->err = "pot3d_solve_from runs on one rank (no loopback slabs)";
+    return POT3D_ERR_INVALID;
+  }
+  if (!(rtol >= 0.0) || maxit < 1) {
+    ctx->err = "rtol must be >= 0 and maxit >= 1";
+    return POT3D_ERR_INVALID;
+  }
+  CK(cudaSetDevice(ctx->device));
+  std::vector<pot3d_ctx *> M = ctx->rhs.empty() ? std::vector<pot3d_ctx *>{ctx} : ctx->rhs;
+  const size_t ncell = (size_t)ctx->nr * ctx->nt * ctx->np;
+  for (size_t q = 0; q < M.size(); q++) {
+    pot3d_ctx *m = M[q];
+    if (x0) {
+      std::vector<pot3d_ctx *> one{m};
+      int rc = cells_in(m, one, x0 + q * ncell, [](pot3d_ctx *c) { return c->x + c->G.plane; });
+      if (rc) {
+        ctx->err = m->err;
+        return rc;
+      }
+    } else if (!m->has_x) {
+      ctx->err = "pot3d_solve_from(x0 = NULL): no solution in the context (a diagnostic call since the last solve)";
+      return POT3D_ERR_STATE;
+    }
+  }
+  for (pot3d_ctx *m : M) m->warm = true;
+  int rc = pot3d_solve(ctx, rtol, maxit, phi, iters, rel_residual, true_rel_residual);
+  for (pot3d_ctx *m : M) m->warm = false;
+  return rc;
+}
+
 int64_t pot3d_history(pot3d_ctx *ctx, double *hist, int64_t len) {
   if (!ctx || !hist) return POT3D_ERR_INVALID;
   if (!ctx->slabs.empty()) ctx = ctx->slabs[0];  // every slab holds the same history
+  if (!ctx->rhs.empty()) ctx = ctx->rhs[0];      // batch: the first problem's
   if (!ctx->hist) return POT3D_ERR_STATE;
   int64_t n = std::min<int64_t>(std::min<int64_t>(len, ctx->last_iters + 1), ctx->hist_len);
   if (cudaMemcpy(hist, ctx->hist, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
@@ -1833,6 +2156,19 @@ int64_t pot3d_history(pot3d_ctx *ctx, double *hist, int64_t len) {
 
 int pot3d_field(pot3d_ctx *ctx, double *br, double *bt, double *bp) {
   if (!ctx) return POT3D_ERR_INVALID;
+  if (!ctx->rhs.empty()) {  // batch: k consecutive fields of the single-problem layout
+    const size_t nc = (size_t)ctx->nr * ctx->nt * ctx->np;
+    const size_t nbr = (size_t)(ctx->nr + 1) * ctx->nt * ctx->np, nbt = (size_t)ctx->nr * (ctx->nt + 1) * ctx->np;
+    for (size_t q = 0; q < ctx->rhs.size(); q++) {
+      int rc = pot3d_field(ctx->rhs[q], br ? br + q * nbr : nullptr, bt ? bt + q * nbt : nullptr,
+                           bp ? bp + q * nc : nullptr);
+      if (rc) {
+        ctx->err = ctx->rhs[q]->err;
+        return rc;
+      }
+    }
+    return 0;
+  }
   if (!ctx->solved) {
     ctx->err = "pot3d_field before a successful pot3d_solve";
     return POT3D_ERR_STATE;
@@ -1896,6 +2232,10 @@ int pot3d_field(pot3d_ctx *ctx, double *br, double *bt, double *bp) {
 
 int pot3d_apply_fused(pot3d_ctx *ctx, const double *x, double *y, int32_t which) {
   if (!ctx || !x || !y || which < 0 || which > 2) return POT3D_ERR_INVALID;
+  if (!ctx->rhs.empty()) {
+    ctx->err = "diagnostic applies run on single-problem contexts (not a batch)";
+    return POT3D_ERR_INVALID;
+  }
   if (which == 1 && ctx->pc != POT3D_PC1) {
     ctx->err = "pot3d_apply_fused(which=1) needs a PC1 context";
     return POT3D_ERR_INVALID;
@@ -1939,22 +2279,21 @@ int pot3d_apply_fused(pot3d_ctx *ctx, const double *x, double *y, int32_t which)
     a.hist = nullptr;
     if (which == 2) {
       a.q_probe = m->x;
-      CK(launch_k(false, k_pass_a_probe, dim3(G.ntj * G.ntk, G.nchunks), dim3(NTHREADS), SMEM_A, s, m->tmaps,
-                  a, 0));
+      CK(launch_pass(false, k_pass_a_probe, dim3(0, G.nchunks), SMEM_A, s, m->tmaps, a, 0));
     } else {
       a.G.nchunks = m->nchunks_b;
-      CK(launch_k(false, which == 0 ? k_pass_b_pc2 : k_pass_b_pc1_even, dim3(G.ntj * G.ntk, m->nchunks_b),
-                  dim3(NTHREADS), SMEM_B, s, m->tmaps, a, 0));
+      CK(launch_pass(false, which == 0 ? k_pass_b_pc2 : k_pass_b_pc1_even, dim3(0, m->nchunks_b), SMEM_B, s,
+                     m->tmaps, a, 0));
     }
     m->n_launch++;
-    m->solved = false;
+    m->solved = m->has_x = false;
   }
   if (which == 2)
     TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->x + m->G.plane; }, y));
   else
     TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->r + m->G.plane; }, y));
   CK(cudaStreamSynchronize(s));
-  ctx->solved = false;
+  ctx->solved = ctx->has_x = false;
   return 0;
 }
 
@@ -1962,6 +2301,10 @@ int pot3d_apply(pot3d_ctx *ctx, const double *x, double *y) { return pot3d_apply
 
 int pot3d_precond(pot3d_ctx *ctx, const double *rin, double *zout) {
   if (!ctx || !rin || !zout) return POT3D_ERR_INVALID;
+  if (!ctx->rhs.empty()) {
+    ctx->err = "diagnostic applies run on single-problem contexts (not a batch)";
+    return POT3D_ERR_INVALID;
+  }
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   std::vector<pot3d_ctx *> M = members(ctx);
@@ -1992,17 +2335,25 @@ int pot3d_precond(pot3d_ctx *ctx, const double *rin, double *zout) {
       CK(cudaGetLastError());
       m->n_launch++;
     }
-    m->solved = false;
+    m->solved = m->has_x = false;
   }
   TRY(cells_out(ctx, M, [](pot3d_ctx *m) { return (const double *)m->P[1] + m->G.plane; }, zout));
   CK(cudaStreamSynchronize(s));
-  ctx->solved = false;
+  ctx->solved = ctx->has_x = false;
   return 0;
 }
 
 int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_pass_b,
                   double *ms_precond) {
   if (!ctx || iters < 1) return POT3D_ERR_INVALID;
+  if (!ctx->rhs.empty()) {  // batch: the leader's launches over all k problems
+    pot3d_ctx *lead = ctx->rhs[0];
+    int rc = pot3d_profile(lead, iters, ms_pass_a, ms_pass_b, ms_precond);
+    if (rc) ctx->err = lead->err;
+    for (pot3d_ctx *m : ctx->rhs) m->solved = m->has_x = false;
+    ctx->solved = ctx->has_x = false;
+    return rc;
+  }
   if (!ctx->slabs.empty() || ctx->variant != 0) {
     ctx->err = "profiling runs the standard PCG passes of one slab context (not a loopback group, not CG1)";
     return POT3D_ERR_INVALID;
@@ -2010,35 +2361,42 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   const Grid &G = ctx->G;
-  // continue the recurrences of the current state without a stopping test
-  CK(cudaMemcpyAsync(ctx->hS, ctx->S, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  // continue the recurrences of the current state without a stopping test (a batch
+  // leader: all k scalar blocks, on the first problem's iteration parity)
+  const int nS = ctx->nrhs;
+  std::vector<Scalars> hv(nS);
+  CK(cudaMemcpyAsync(hv.data(), ctx->S, nS * sizeof(Scalars), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  Scalars h = *ctx->hS;
-  h.stop = 0;
-  h.status = 0;
-  h.rtol = 0.0;
-  h.maxit = h.iter + iters + 1;
-  if (!(h.rho != 0.0)) h.rho = 1.0;
-  if (!(h.bnorm > 0.0)) h.bnorm = 1.0;
-  *ctx->hS = h;
-  CK(cudaMemcpyAsync(ctx->S, ctx->hS, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+  const long long it0 = hv[0].iter;
+  for (Scalars &v : hv) {
+    v.stop = 0;
+    v.status = 0;
+    v.rtol = 0.0;
+    v.iter = it0;
+    v.maxit = it0 + iters + 1;
+    if (!(v.rho != 0.0)) v.rho = 1.0;
+    if (!(v.bnorm > 0.0)) v.bnorm = 1.0;
+  }
+  const Scalars h = hv[0];
+  CK(cudaMemcpyAsync(ctx->S, hv.data(), nS * sizeof(Scalars), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
   cudaEvent_t ev[4];
   for (auto &e : ev) CK(cudaEventCreate(&e));
   double ta = 0, tb = 0, tp = 0;
   const bool pc2 = ctx->pc == 2;
-  dim3 grd(G.ntj * G.ntk, G.nchunks);
+  dim3 grd(G.ntj * G.ntk, G.nchunks, nS);
   for (int it = 0; it < iters; it++) {
     const int par = (int)((h.iter + it) & 1);
     PassArgs a = make_args(ctx, par);
     a.hist = nullptr;
     a.finalize = 1;
     CK(cudaEventRecord(ev[0], s));
-    CK(launch_k(false, kern_a(ctx), grd, dim3(NTHREADS), SMEM_A, s, ctx->tmaps, a, par));
+    CK(launch_pass(false, kern_a(ctx), grd, SMEM_A, s, ctx->tmaps, a, par));
     CK(cudaEventRecord(ev[1], s));
     PassArgs ab = a;
     ab.G.nchunks = ctx->nchunks_b;
-    dim3 grdb(G.ntj * G.ntk, ctx->nchunks_b);
-    CK(launch_k(false, kern_b(ctx, par), grdb, dim3(NTHREADS), SMEM_B, s, ctx->tmaps, ab, par));
+    dim3 grdb(G.ntj * G.ntk, ctx->nchunks_b, nS);
+    CK(launch_pass(false, kern_b(ctx, par), grdb, SMEM_B, s, ctx->tmaps, ab, par));
     CK(cudaEventRecord(ev[2], s));
     ctx->n_launch += 2;
     if (ctx->pc == 3) {
@@ -2061,12 +2419,16 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
   if (ms_pass_a) *ms_pass_a = ta / iters;
   if (ms_pass_b) *ms_pass_b = tb / iters;
   if (ms_precond) *ms_precond = tp / iters;
-  ctx->solved = false;
+  ctx->solved = ctx->has_x = false;
   return 0;
 }
 
 int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *names, int32_t nmax) {
   if (!ctx || iters < 1 || !ms || !names || nmax < 1) return POT3D_ERR_INVALID;
+  if (!ctx->rhs.empty()) {
+    ctx->err = "diagnostic applies run on single-problem contexts (not a batch)";
+    return POT3D_ERR_INVALID;
+  }
   if (!ctx->slabs.empty() || ctx->variant != 0) {
     ctx->err = "profiling runs the standard PCG passes of one slab context (not a loopback group, not CG1)";
     return POT3D_ERR_INVALID;
@@ -2124,13 +2486,14 @@ int pot3d_profile_iteration(pot3d_ctx *ctx, int32_t iters, double *ms, char *nam
   }
   strncpy(names, all.c_str(), 1023);
   names[1023] = 0;
-  ctx->solved = false;
+  ctx->solved = ctx->has_x = false;
   return n;
 }
 
 int pot3d_trace_enable(pot3d_ctx *ctx, int32_t on) {
   if (!ctx) return POT3D_ERR_INVALID;
   for (pot3d_ctx *m : ctx->slabs) m->trace_on = on != 0;
+  for (pot3d_ctx *m : ctx->rhs) m->trace_on = on != 0;
   ctx->trace_on = on != 0;
   return 0;
 }
@@ -2138,6 +2501,7 @@ int pot3d_trace_enable(pot3d_ctx *ctx, int32_t on) {
 int pot3d_kernel_times(pot3d_ctx *ctx, double *us_pass_a, double *us_pass_b, int32_t *n) {
   if (!ctx || !us_pass_a || !us_pass_b || !n) return POT3D_ERR_INVALID;
   if (!ctx->slabs.empty()) ctx = ctx->slabs[0];
+  if (!ctx->rhs.empty()) ctx = ctx->rhs[0];  // batch: the leader's launches
   *n = 0;
   if (!ctx->trace) {
     ctx->err = "tracing not enabled (pot3d_trace_enable before pot3d_solve)";
@@ -2166,6 +2530,7 @@ int pot3d_kernel_times(pot3d_ctx *ctx, double *us_pass_a, double *us_pass_b, int
 int pot3d_kernel_trace(pot3d_ctx *ctx, int64_t *iter, double *us_pass_a, double *us_pass_b, int32_t len) {
   if (!ctx || !iter || !us_pass_a || !us_pass_b || len < 1) return POT3D_ERR_INVALID;
   if (!ctx->slabs.empty()) ctx = ctx->slabs[0];
+  if (!ctx->rhs.empty()) ctx = ctx->rhs[0];
   if (!ctx->trace) {
     ctx->err = "tracing not enabled (pot3d_trace_enable before pot3d_solve)";
     return POT3D_ERR_STATE;
@@ -2194,6 +2559,8 @@ int pot3d_destroy(pot3d_ctx *ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (pot3d_ctx *m : ctx->slabs) pot3d_destroy(m);
   ctx->slabs.clear();
+  for (pot3d_ctx *m : ctx->rhs) pot3d_destroy(m);
+  ctx->rhs.clear();
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->pc2) pc2_destroy(ctx->pc2, ctx->ufree, ctx->actx);
   ipc_release(ctx);

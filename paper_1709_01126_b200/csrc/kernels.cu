@@ -278,10 +278,13 @@ __global__ void k_finalize_mail(Scalars *S, const PeerTab *peers, int kind, int 
 
 // ---------------------------------------------------------------------------
 // Init: rho_0 = b . D^-1 b (PC1) and ||b||^2 over this rank's cells.
-// r already holds b.  Grid-stride over cells.
+// r already holds b.  Grid-stride over cells.  Warm start (keep_b, one rank): r holds
+// r_0 = b - A x0 and S->bnorm = ||b|| already; rr = ||r_0||^2, the loop stops at once
+// if ||r_0|| <= rtol ||b|| (A9), hist0[0] = ||r_0|| / ||b||.
 // ---------------------------------------------------------------------------
 __global__ void k_init_dots(Grid G, Metrics M, Scalars *S, const double *r, double *partials,
-                            int finalize, double *local_sum, int use_z, const double *z) {
+                            int finalize, double *local_sum, int use_z, const double *z, int keep_b,
+                            double *hist0) {
   __shared__ double sred[64];
   double a0 = 0.0, a1 = 0.0;
   const long long ncell = (long long)G.nr_loc * G.nt * G.np;
@@ -309,14 +312,20 @@ __global__ void k_init_dots(Grid G, Metrics M, Scalars *S, const double *r, doub
   if (grid_sum<2>(v, partials, &S->counter[2], sred, tot) && threadIdx.x == 0) {
     if (finalize) {
       S->rho = tot[0];
-      S->bnorm = sqrt(tot[1]);
+      if (!keep_b) S->bnorm = sqrt(tot[1]);
       S->rr = tot[1];
       S->iter = 0;
       S->beta = 0.0;
       S->alpha = 0.0;
       S->alpha_prev = 0.0;
       S->status = 0;
-      S->stop = (tot[1] == 0.0) ? 1 : 0;
+      if (keep_b) {
+        const double bn = S->bnorm, rn = sqrt(tot[1]);
+        S->stop = (bn == 0.0 || rn <= S->rtol * bn) ? 1 : 0;
+        if (hist0) hist0[0] = bn > 0.0 ? rn / bn : 0.0;
+      } else {
+        S->stop = (tot[1] == 0.0) ? 1 : 0;
+      }
     } else {
       local_sum[0] = tot[0];
       local_sum[1] = tot[1];

@@ -29,6 +29,12 @@ __device__ __forceinline__ void chunk_bounds(const Grid &G, int c, int &c0, int 
   c1 = c0 + base + (c < rem ? 1 : 0);
 }
 
+// Multi-RHS batches (pot3d_runtime.nrhs): blockIdx.z is the right-hand
+// side.  Its vectors are stacked along the plane axis (each nr_loc + 2 planes, so one TMA
+// descriptor covers the batch), its scalars are S[z], its partials and residual history
+// PassArgs::pstride / hstride doubles further on.  Plane offset of this block's RHS:
+__device__ __forceinline__ int rhs_planes(const Grid &G) { return (int)blockIdx.z * (G.nr_loc + 2); }
+
 __device__ __forceinline__ int pass_bid(const Grid &G) {
   return G.blk_off + blockIdx.x + gridDim.x * blockIdx.y;
 }
@@ -120,15 +126,18 @@ struct TileThread {
   long long rowoff[RPW]; // j*PK + (k0-1+2*lane) + COFF, row clamped into the grid
   bool st0, st1;         // element 0/1 is an interior column of this tile inside the grid
   bool gr0, gr1, gl0, gl1;  // element 0/1 holds k = 0 (right-ghost dup) / k = np-1 (left ghost)
+  bool valid;            // a tile of the grid (false: a cluster padding block, Grid::cj/ck)
 };
 
 __device__ __forceinline__ TileThread tile_thread(const Grid &G) {
   TileThread t;
   t.lane = threadIdx.x & 31;
   t.w = threadIdx.x >> 5;
-  const int tile = blockIdx.x;
-  t.j0 = (tile % G.ntj) * TJ;
-  t.k0 = (tile / G.ntj) * TK;
+  int tj, tk;
+  tile_of(G, blockIdx.x, tj, tk);
+  t.valid = (tj < G.ntj) && (tk < G.ntk);
+  t.j0 = tj * TJ;
+  t.k0 = tk * TK;
   // part 3: all shells, the two chunks touching a ghost shell scheduled last (their
   // blocks wait for the neighbours' halo, which meanwhile arrives in peer memory)
   int cy = blockIdx.y - G.role_rows;
@@ -160,8 +169,10 @@ __device__ __forceinline__ TileThread tile_thread(const Grid &G) {
 // periodic seam (no masks, no ghost-column duplicates): block-uniform, selects the
 // FAST instantiation of the passes.
 __device__ __forceinline__ bool tile_fast(const Grid &G) {
-  const int k0 = (blockIdx.x / G.ntj) * TK;
-  return k0 >= TK && k0 + TK <= G.np;
+  int tj, tk;
+  tile_of(G, blockIdx.x, tj, tk);
+  const int k0 = tk * TK;
+  return tj < G.ntj && k0 >= TK && k0 + TK <= G.np;
 }
 
 // Store of a lane's column pair (interior elements only) with the periodic

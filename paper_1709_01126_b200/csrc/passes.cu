@@ -65,7 +65,7 @@ template <bool PROBE, bool FAST>
 __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, int parity, PassShared &sh) {
   const Grid &G = A.G;
   const Metrics &M = A.M;
-  Scalars *S = A.S;
+  Scalars *S = A.S + blockIdx.z;  // batch: the right-hand side of this block (pass_common.cuh)
   if (G.role_rows && blockIdx.y == 0) {
     // edge role (peer memory): p_k on the two edge shells, locally and into the
     // neighbours' ghost shells, then the halo flags -- scheduled first, beside the
@@ -99,6 +99,8 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   load_planes(pls, M, ig0, L + 2);
   const int cs = 2 + 2 * t.lane;  // smem index of element 0
   const long long PL = G.plane;
+  const int zp = rhs_planes(G);   // batch: TMA plane offset / element offset of this RHS
+  const long long vo = zp * PL;
   const void *map_src = &T.src_h;
   const void *map_old = &T.p_h[parity];
   const void *map_new = &T.p_h[parity ^ 1];
@@ -124,11 +126,11 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
           }
         }
         mbar_arrive_expect_tx(&sm.bar[st], STAGE_BYTES / 2);
-        tma_load_3d(&sm.r[st][0][0], map_new, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
+        tma_load_3d(&sm.r[st][0][0], map_new, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, zp + il + 1);
       } else {
         mbar_arrive_expect_tx(&sm.bar[st], STAGE_BYTES);
-        tma_load_3d(&sm.r[st][0][0], map_src, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
-        tma_load_3d(&sm.p[st][0][0], map_old, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
+        tma_load_3d(&sm.r[st][0][0], map_src, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, zp + il + 1);
+        tma_load_3d(&sm.p[st][0][0], map_old, &sm.bar[st], t.k0 - 3 + COFF, t.j0 - 1, zp + il + 1);
       }
     }
   };
@@ -148,129 +150,131 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
   pdl_trigger();
   pdl_wait();
   if (S->stop) return;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_mark(S, TR_A0);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) trace_mark(A.S, TR_A0);
   const double beta = S->beta;
-  if (threadIdx.x == 0) {
-    issue(0, 0);
-    issue(1, 1);
-  }
-
-  const double2 Z2 = make_double2(0.0, 0.0);
-  double2 R[3][RPW];  // p_k of planes q (R[q%3]), q-1, q-2 of this lane's cells
-#pragma unroll
-  for (int u = 0; u < 3; u++)
-#pragma unroll
-    for (int e = 0; e < RPW; e++) R[u][e] = Z2;
-  double *g_pn = A.p_new + (long long)t.c0 * PL;  // + rowoff[e]: p_k at plane q (il = c0-1+q)
   double acc = 0.0;
-  unsigned ph = 0;  // mbarrier parity of the current group of 3 planes
+  if (t.valid) {  // a cluster padding block only joins the reduction
+    if (threadIdx.x == 0) {
+      issue(0, 0);
+      issue(1, 1);
+    }
 
-  // per-thread constants of the stencil: smem offsets of the theta neighbours
-  // (clamped on the tile's outer rows, which skip the stencil) and the column masks
-  // (FAST tiles: every column is an interior cell)
-  int up_off[RPW], dn_off[RPW];
+    const double2 Z2 = make_double2(0.0, 0.0);
+    double2 R[3][RPW];  // p_k of planes q (R[q%3]), q-1, q-2 of this lane's cells
 #pragma unroll
-  for (int e = 0; e < RPW; e++) {
-    const int r = t.row[e];
-    up_off[e] = (r == 0) ? 0 : -SROW;
-    dn_off[e] = (r == TR - 1) ? 0 : SROW;
-  }
-  const bool m0 = FAST || t.st0, m1 = FAST || t.st1;
-  const bool halo_lane = (t.lane == 0) || (t.lane == 31);
-  const int hcol = (t.lane == 0) ? 1 : SROW - 2;  // smem column of this lane's halo column
+    for (int u = 0; u < 3; u++)
+#pragma unroll
+      for (int e = 0; e < RPW; e++) R[u][e] = Z2;
+    double *g_pn = A.p_new + vo + (long long)t.c0 * PL;  // + rowoff[e]: p_k at plane q (il = c0-1+q)
+    unsigned ph = 0;  // mbarrier parity of the current group of 3 planes
 
-  // One plane step.  STENCIL = false only for q = 0, 1 (peeled), so the steady
-  // state is one basic block: the transform's fp64 chains (plane q) and the
-  // stencil of plane q-1 are independent and can be interleaved by the scheduler.
-#if POT3D_A_FLUX
-  double2 fl[RPW];  // upper r flux arp (c - ip) of the last stencil plane, per row and cell
-#endif
-  auto step = [&](auto U, auto STENCIL, int q, auto FIRST) {
-    constexpr int u = decltype(U)::value;       // stage, slot and register set of plane q
-    constexpr bool do_st = decltype(STENCIL)::value;
-    constexpr bool first = decltype(FIRST)::value;  // first stencil plane of the chunk
-    (void)first;
-    constexpr int um = (u + 2) % 3, umm = (u + 1) % 3;
-    __syncthreads();  // stage um and slot u are free
-    if (threadIdx.x == 0) issue(q + 2, um);
-    const int il = t.c0 - 1 + q;
-    const bool ghost = (il < 0) || (il >= G.nr_loc);
-    const bool store = (q >= 1) && (q <= L);
-    const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
-    const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
-    const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
-    const PlaneC Ps = plane_at(pls, do_st ? q - 1 : q);
-    mbar_wait(&sm.bar[u], ph);
-    // ---- transform plane il -> p_k = z + beta p_{k-1} (ghost shells: the final p_k) ----
+    // per-thread constants of the stencil: smem offsets of the theta neighbours
+    // (clamped on the tile's outer rows, which skip the stencil) and the column masks
+    // (FAST tiles: every column is an interior cell)
+    int up_off[RPW], dn_off[RPW];
 #pragma unroll
     for (int e = 0; e < RPW; e++) {
       const int r = t.row[e];
-      const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[u][r][cs]);
-      const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[u][r][cs]);  // unused on ghosts
-      double2 pn;
-      pn.x = selp(rv.x, fma(beta, pv.x, rv.x), ghost);
-      pn.y = selp(rv.y, fma(beta, pv.y, rv.y), ghost);
-      R[u][e] = pn;
-      *reinterpret_cast<double2 *>(&sm.pn[u][r][cs]) = pn;
-      if (halo_lane) {  // the halo columns k0-2 (lane 0) and k0+63 (lane 31)
-        const double hr = sm.r[u][r][hcol], hp = sm.p[u][r][hcol];
-        sm.pn[u][r][hcol] = selp(hr, fma(beta, hp, hr), ghost);
-      }
-      if (store && t.stencil[e]) {
-        POT3D_CHK(S, in_range(g_pn + t.rowoff[e], A.p_new, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
-        store_pair<FAST>(g_pn + t.rowoff[e], t, G.np, pn, false);
-      }
+      up_off[e] = (r == 0) ? 0 : -SROW;
+      dn_off[e] = (r == TR - 1) ? 0 : SROW;
     }
-    g_pn += PL;
-    // ---- stencil of plane il-1 (its slot was completed before this barrier) ----
-    if (do_st) {
-      const double *sb = &sm.pn[um][0][0];
+    const bool m0 = FAST || t.st0, m1 = FAST || t.st1;
+    const bool halo_lane = (t.lane == 0) || (t.lane == 31);
+    const int hcol = (t.lane == 0) ? 1 : SROW - 2;  // smem column of this lane's halo column
+
+    // One plane step.  STENCIL = false only for q = 0, 1 (peeled), so the steady
+    // state is one basic block: the transform's fp64 chains (plane q) and the
+    // stencil of plane q-1 are independent and can be interleaved by the scheduler.
+  #if POT3D_A_FLUX
+    double2 fl[RPW];  // upper r flux arp (c - ip) of the last stencil plane, per row and cell
+  #endif
+    auto step = [&](auto U, auto STENCIL, int q, auto FIRST) {
+      constexpr int u = decltype(U)::value;       // stage, slot and register set of plane q
+      constexpr bool do_st = decltype(STENCIL)::value;
+      constexpr bool first = decltype(FIRST)::value;  // first stencil plane of the chunk
+      (void)first;
+      constexpr int um = (u + 2) % 3, umm = (u + 1) % 3;
+      __syncthreads();  // stage um and slot u are free
+      if (threadIdx.x == 0) issue(q + 2, um);
+      const int il = t.c0 - 1 + q;
+      const bool ghost = (il < 0) || (il >= G.nr_loc);
+      const bool store = (q >= 1) && (q <= L);
+      const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
+      const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
+      const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
+      const PlaneC Ps = plane_at(pls, do_st ? q - 1 : q);
+      mbar_wait(&sm.bar[u], ph);
+      // ---- transform plane il -> p_k = z + beta p_{k-1} (ghost shells: the final p_k) ----
 #pragma unroll
       for (int e = 0; e < RPW; e++) {
-        if (!t.stencil[e]) continue;  // halo rows (warp-uniform)
         const int r = t.row[e];
-        const double *so = sb + r * SROW + cs;
-        const double2 c = R[um][e];
-        const double2 up = (RPW == 2 && e == 1) ? R[um][0] : *reinterpret_cast<const double2 *>(so + up_off[e]);
-        const double2 dn = (RPW == 2 && e == 0) ? R[um][RPW - 1] : *reinterpret_cast<const double2 *>(so + dn_off[e]);
-        const double lf = so[-1], rt = so[2];
-#if POT3D_A_FLUX
-        // lower r flux: computed on the chunk's first stencil plane, then the negated
-        // upper flux of the previous plane
-        const double fdx = first ? Ps.arm * (c.x - R[umm][e].x) : -fl[e].x;
-        const double fdy = first ? Ps.arm * (c.y - R[umm][e].y) : -fl[e].y;
-        const double q0 = stencil7f(c.x, R[u][e].x, fdx, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e], fl[e].x);
-        const double q1 = stencil7f(c.y, R[u][e].y, fdy, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e], fl[e].y);
-#else
-        const double q0 = stencil7(c.x, R[u][e].x, R[umm][e].x, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e]);
-        const double q1 = stencil7(c.y, R[u][e].y, R[umm][e].y, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e]);
-#endif
-        acc += (m0 ? c.x * q0 : 0.0) + (m1 ? c.y * q1 : 0.0);
-        // diagnostic instantiation only (pot3d_apply_fused which = 2): q of plane il-1
-        if (PROBE) store_pair<FAST>(A.q_probe + (long long)il * PL + t.rowoff[e], t, G.np, make_double2(q0, q1), false);
+        const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[u][r][cs]);
+        const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[u][r][cs]);  // unused on ghosts
+        double2 pn;
+        pn.x = selp(rv.x, fma(beta, pv.x, rv.x), ghost);
+        pn.y = selp(rv.y, fma(beta, pv.y, rv.y), ghost);
+        R[u][e] = pn;
+        *reinterpret_cast<double2 *>(&sm.pn[u][r][cs]) = pn;
+        if (halo_lane) {  // the halo columns k0-2 (lane 0) and k0+63 (lane 31)
+          const double hr = sm.r[u][r][hcol], hp = sm.p[u][r][hcol];
+          sm.pn[u][r][hcol] = selp(hr, fma(beta, hp, hr), ghost);
+        }
+        if (store && t.stencil[e]) {
+          POT3D_CHK(S, in_range(g_pn + t.rowoff[e], A.p_new + vo, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
+          store_pair<FAST>(g_pn + t.rowoff[e], t, G.np, pn, false);
+        }
       }
-    }
-  };
+      g_pn += PL;
+      // ---- stencil of plane il-1 (its slot was completed before this barrier) ----
+      if (do_st) {
+        const double *sb = &sm.pn[um][0][0];
+#pragma unroll
+        for (int e = 0; e < RPW; e++) {
+          if (!t.stencil[e]) continue;  // halo rows (warp-uniform)
+          const int r = t.row[e];
+          const double *so = sb + r * SROW + cs;
+          const double2 c = R[um][e];
+          const double2 up = (RPW == 2 && e == 1) ? R[um][0] : *reinterpret_cast<const double2 *>(so + up_off[e]);
+          const double2 dn = (RPW == 2 && e == 0) ? R[um][RPW - 1] : *reinterpret_cast<const double2 *>(so + dn_off[e]);
+          const double lf = so[-1], rt = so[2];
+  #if POT3D_A_FLUX
+          // lower r flux: computed on the chunk's first stencil plane, then the negated
+          // upper flux of the previous plane
+          const double fdx = first ? Ps.arm * (c.x - R[umm][e].x) : -fl[e].x;
+          const double fdy = first ? Ps.arm * (c.y - R[umm][e].y) : -fl[e].y;
+          const double q0 = stencil7f(c.x, R[u][e].x, fdx, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e], fl[e].x);
+          const double q1 = stencil7f(c.y, R[u][e].y, fdy, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e], fl[e].y);
+  #else
+          const double q0 = stencil7(c.x, R[u][e].x, R[umm][e].x, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e]);
+          const double q1 = stencil7(c.y, R[u][e].y, R[umm][e].y, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e]);
+  #endif
+          acc += (m0 ? c.x * q0 : 0.0) + (m1 ? c.y * q1 : 0.0);
+          // diagnostic instantiation only (pot3d_apply_fused which = 2): q of plane il-1
+          if (PROBE) store_pair<FAST>(A.q_probe + (long long)il * PL + t.rowoff[e], t, G.np, make_double2(q0, q1), false);
+        }
+      }
+    };
 
-  const int last = L + 1;  // >= 2
-  step(IC<0>{}, std::false_type{}, 0, std::false_type{});
-  step(IC<1>{}, std::false_type{}, 1, std::false_type{});
-  step(IC<2>{}, std::true_type{}, 2, std::true_type{});
-  ph ^= 1u;
-#pragma unroll 1
-  for (int q = 3; q <= last; q += 3) {
-    step(IC<0>{}, std::true_type{}, q, std::false_type{});
-    if (q + 1 > last) break;
-    step(IC<1>{}, std::true_type{}, q + 1, std::false_type{});
-    if (q + 2 > last) break;
-    step(IC<2>{}, std::true_type{}, q + 2, std::false_type{});
+    const int last = L + 1;  // >= 2
+    step(IC<0>{}, std::false_type{}, 0, std::false_type{});
+    step(IC<1>{}, std::false_type{}, 1, std::false_type{});
+    step(IC<2>{}, std::true_type{}, 2, std::true_type{});
     ph ^= 1u;
-  }
+#pragma unroll 1
+    for (int q = 3; q <= last; q += 3) {
+      step(IC<0>{}, std::true_type{}, q, std::false_type{});
+      if (q + 1 > last) break;
+      step(IC<1>{}, std::true_type{}, q + 1, std::false_type{});
+      if (q + 2 > last) break;
+      step(IC<2>{}, std::true_type{}, q + 2, std::false_type{});
+      ph ^= 1u;
+    }
 
+  }
   double v[1] = {acc}, tot[1];
-  if (grid_sum<1>(v, A.partials, &S->counter[0], sred, tot, pass_bid(G), pass_nb(G)) &&
+  if (grid_sum<1>(v, A.partials + blockIdx.z * A.pstride, &S->counter[0], sred, tot, pass_bid(G), pass_nb(G)) &&
       threadIdx.x == 0) {
-    trace_mark(S, TR_A1);
+    trace_max(A.S, TR_A1);  // batch: the end of the last right-hand side
     if (A.finalize)
       finalize_alpha(S, tot[0]);
     else if (A.peers)
@@ -290,7 +294,7 @@ template <bool USE_Z, int XM, bool FAST>
 __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, int parity, PassShared &sh) {
   const Grid &G = A.G;
   const Metrics &M = A.M;
-  Scalars *S = A.S;
+  Scalars *S = A.S + blockIdx.z;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemB &sm = *reinterpret_cast<SmemB *>(smem_raw);
   double *sred = sh.sred;
@@ -304,6 +308,8 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   load_planes(pls, M, ig0, L + 2);
   const int cs = 2 + 2 * t.lane;
   const long long PL = G.plane;
+  const int zp = rhs_planes(G);
+  const long long vo = zp * PL;
   const void *map_p = &T.p_h[parity ^ 1];
   const void *map_r = &T.r_i;
   const void *map_x = &T.x_i;
@@ -318,10 +324,10 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
       const int il = t.c0 - 1 + qi;
       const bool rown = (qi >= 1) && (qi <= L);
       mbar_arrive_expect_tx(&sm.bar[si], rown ? PB + (XM == XM_SKIP ? 1 : 2) * RB : PB);
-      tma_load_3d(&sm.pn[si][0][0], map_p, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
+      tma_load_3d(&sm.pn[si][0][0], map_p, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, zp + il + 1);
       if (rown) {
-        tma_load_3d(&sm.r[si][0][0], map_r, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
-        if (XM != XM_SKIP) tma_load_3d(&sm.x[si][0][0], map_x, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
+        tma_load_3d(&sm.r[si][0][0], map_r, &sm.bar[si], t.k0 - 1 + COFF, t.j0, zp + il + 1);
+        if (XM != XM_SKIP) tma_load_3d(&sm.x[si][0][0], map_x, &sm.bar[si], t.k0 - 1 + COFF, t.j0, zp + il + 1);
       }
     }
     ++qi;
@@ -335,107 +341,110 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
   pdl_trigger();
   pdl_wait();
   if (S->stop) return;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_mark(S, TR_B0);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) trace_mark(A.S, TR_B0);
   const double alpha = S->alpha;
   // XM_PAIR: c = alpha_{k-1} / beta_{k-1}; cp = c + alpha_k multiplies p_k, -c multiplies z_k
   const double cpair = (XM == XM_PAIR) ? S->alpha_prev / S->beta : 0.0;
   const double cp = (XM == XM_PAIR) ? cpair + alpha : alpha;
-  if (threadIdx.x == 0)
-    for (int s = 0; s < NS_B - 2; s++) issue();
-
-  const double2 Z2 = make_double2(0.0, 0.0);
-  double2 pm[RPW], pc[RPW], pn[RPW];
-#pragma unroll
-  for (int e = 0; e < RPW; e++) pm[e] = pc[e] = pn[e] = Z2;
   double acc_rz = 0.0, acc_rr = 0.0;
-  double *g_w = A.r_out + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: r of plane c0
-  double *g_x = A.x + (long long)(t.c0 + 1) * PL;      // + rowoff[e]: x of plane c0
-  int st = 0, so = NS_B - 1;                           // stages of planes q and q-1
-  unsigned ph = 0;
+  if (t.valid) {  // a cluster padding block only joins the reduction
+    if (threadIdx.x == 0)
+      for (int s = 0; s < NS_B - 2; s++) issue();
+
+    const double2 Z2 = make_double2(0.0, 0.0);
+    double2 pm[RPW], pc[RPW], pn[RPW];
+#pragma unroll
+    for (int e = 0; e < RPW; e++) pm[e] = pc[e] = pn[e] = Z2;
+    double *g_w = A.r_out + vo + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: r of plane c0
+    double *g_x = A.x + vo + (long long)(t.c0 + 1) * PL;      // + rowoff[e]: x of plane c0
+    int st = 0, so = NS_B - 1;                           // stages of planes q and q-1
+    unsigned ph = 0;
 
 #pragma unroll 1
-  for (int q = 0; q <= L + 1; q++) {
-    __syncthreads();  // stage (q-2)%NS_B is free
-    if (threadIdx.x == 0) issue();
-    const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
-    const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
-    const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
-    const PlaneC P = plane_at(pls, q >= 1 ? q - 1 : 0);  // stencil plane il-1
-    mbar_wait(&sm.bar[st], ph);
+    for (int q = 0; q <= L + 1; q++) {
+      __syncthreads();  // stage (q-2)%NS_B is free
+      if (threadIdx.x == 0) issue();
+      const double2 dp = *reinterpret_cast<const double2 *>(&tcs.dp[cs]);
+      const double2 ap = *reinterpret_cast<const double2 *>(&tcs.app[cs]);
+      const double2 am = *reinterpret_cast<const double2 *>(&tcs.apm[cs]);
+      const PlaneC P = plane_at(pls, q >= 1 ? q - 1 : 0);  // stencil plane il-1
+      mbar_wait(&sm.bar[st], ph);
 #pragma unroll
-    for (int e = 0; e < RPW; e++) pn[e] = *reinterpret_cast<const double2 *>(&sm.pn[st][t.row[e]][cs]);
-    if (q >= 2) {
-      const double *sb = &sm.pn[so][0][0];
+      for (int e = 0; e < RPW; e++) pn[e] = *reinterpret_cast<const double2 *>(&sm.pn[st][t.row[e]][cs]);
+      if (q >= 2) {
+        const double *sb = &sm.pn[so][0][0];
+#pragma unroll
+        for (int e = 0; e < RPW; e++) {
+          if (!t.stencil[e]) continue;
+          const int r = t.row[e];
+          const double *sr = sb + r * SROW + cs;
+          const double2 up = (RPW == 2 && e == 1) ? pc[0] : *reinterpret_cast<const double2 *>(sr - SROW);
+          const double2 dn = (RPW == 2 && e == 0) ? pc[RPW - 1] : *reinterpret_cast<const double2 *>(sr + SROW);
+          const double lf = sr[-1], rt = sr[2];
+          const double q0 = stencil7(pc[e].x, pn[e].x, pm[e].x, dn.x, up.x, pc[e].y, lf, dp.x, ap.x, am.x, P, rw[e]);
+          const double q1 = stencil7(pc[e].y, pn[e].y, pm[e].y, dn.y, up.y, rt, pc[e].x, dp.y, ap.y, am.y, P, rw[e]);
+          const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[so][r - 1][2 * t.lane]);
+          double2 rn, xn;  // rn: the stored vector after the update (PC1: z, PC2: r)
+          if (XM != XM_SKIP) {
+            const double2 xv = *reinterpret_cast<const double2 *>(&sm.x[so][r - 1][2 * t.lane]);
+            if (XM == XM_PAIR) {
+              xn.x = fma(cp, pc[e].x, fma(-cpair, rv.x, xv.x));
+              xn.y = fma(cp, pc[e].y, fma(-cpair, rv.y, xv.y));
+            } else {
+              xn.x = fma(alpha, pc[e].x, xv.x);
+              xn.y = fma(alpha, pc[e].y, xv.y);
+            }
+          }
+          if (USE_Z) {
+            rn.x = fma(-alpha, q0, rv.x);
+            rn.y = fma(-alpha, q1, rv.y);
+            acc_rr += (m0 ? rn.x * rn.x : 0.0) + (m1 ? rn.y * rn.y : 0.0);
+          } else {
+            // z_{k+1} = z_k - alpha D^-1 q;  r_{k+1} = D z_{k+1}
+            const DiagRow d = diag_row(P, rw[e]);
+            const double d0 = diag_at(dp.x, d, ap.x, am.x), d1 = diag_at(dp.y, d, ap.y, am.y);
+            rn.x = fma(-alpha, jacobi(q0, d0), rv.x);
+            rn.y = fma(-alpha, jacobi(q1, d1), rv.y);
+            const double s0 = d0 * rn.x, s1 = d1 * rn.y;
+            acc_rz += (m0 ? s0 * rn.x : 0.0) + (m1 ? s1 * rn.y : 0.0);
+            acc_rr += (m0 ? s0 * s0 : 0.0) + (m1 ? s1 * s1 : 0.0);
+          }
+          POT3D_CHK(S, in_range(g_w + t.rowoff[e], A.r_out + vo, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
+          POT3D_CHK(S, XM == XM_SKIP || in_range(g_x + t.rowoff[e], A.x + vo, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
+          store_pair<FAST>(g_w + t.rowoff[e], t, G.np, rn, true);
+          if (XM != XM_SKIP) {
+            if (FAST || (t.st0 && t.st1)) {
+              __stcs(reinterpret_cast<double2 *>(g_x + t.rowoff[e]), xn);
+            } else {
+              if (t.st0) g_x[t.rowoff[e]] = xn.x;
+              if (t.st1) g_x[t.rowoff[e] + 1] = xn.y;
+            }
+          }
+        }
+        g_w += PL;
+        g_x += PL;
+      }
 #pragma unroll
       for (int e = 0; e < RPW; e++) {
-        if (!t.stencil[e]) continue;
-        const int r = t.row[e];
-        const double *sr = sb + r * SROW + cs;
-        const double2 up = (RPW == 2 && e == 1) ? pc[0] : *reinterpret_cast<const double2 *>(sr - SROW);
-        const double2 dn = (RPW == 2 && e == 0) ? pc[RPW - 1] : *reinterpret_cast<const double2 *>(sr + SROW);
-        const double lf = sr[-1], rt = sr[2];
-        const double q0 = stencil7(pc[e].x, pn[e].x, pm[e].x, dn.x, up.x, pc[e].y, lf, dp.x, ap.x, am.x, P, rw[e]);
-        const double q1 = stencil7(pc[e].y, pn[e].y, pm[e].y, dn.y, up.y, rt, pc[e].x, dp.y, ap.y, am.y, P, rw[e]);
-        const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[so][r - 1][2 * t.lane]);
-        double2 rn, xn;  // rn: the stored vector after the update (PC1: z, PC2: r)
-        if (XM != XM_SKIP) {
-          const double2 xv = *reinterpret_cast<const double2 *>(&sm.x[so][r - 1][2 * t.lane]);
-          if (XM == XM_PAIR) {
-            xn.x = fma(cp, pc[e].x, fma(-cpair, rv.x, xv.x));
-            xn.y = fma(cp, pc[e].y, fma(-cpair, rv.y, xv.y));
-          } else {
-            xn.x = fma(alpha, pc[e].x, xv.x);
-            xn.y = fma(alpha, pc[e].y, xv.y);
-          }
-        }
-        if (USE_Z) {
-          rn.x = fma(-alpha, q0, rv.x);
-          rn.y = fma(-alpha, q1, rv.y);
-          acc_rr += (m0 ? rn.x * rn.x : 0.0) + (m1 ? rn.y * rn.y : 0.0);
-        } else {
-          // z_{k+1} = z_k - alpha D^-1 q;  r_{k+1} = D z_{k+1}
-          const DiagRow d = diag_row(P, rw[e]);
-          const double d0 = diag_at(dp.x, d, ap.x, am.x), d1 = diag_at(dp.y, d, ap.y, am.y);
-          rn.x = fma(-alpha, jacobi(q0, d0), rv.x);
-          rn.y = fma(-alpha, jacobi(q1, d1), rv.y);
-          const double s0 = d0 * rn.x, s1 = d1 * rn.y;
-          acc_rz += (m0 ? s0 * rn.x : 0.0) + (m1 ? s1 * rn.y : 0.0);
-          acc_rr += (m0 ? s0 * s0 : 0.0) + (m1 ? s1 * s1 : 0.0);
-        }
-        POT3D_CHK(S, in_range(g_w + t.rowoff[e], A.r_out, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
-        POT3D_CHK(S, XM == XM_SKIP || in_range(g_x + t.rowoff[e], A.x, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
-        store_pair<FAST>(g_w + t.rowoff[e], t, G.np, rn, true);
-        if (XM != XM_SKIP) {
-          if (FAST || (t.st0 && t.st1)) {
-            __stcs(reinterpret_cast<double2 *>(g_x + t.rowoff[e]), xn);
-          } else {
-            if (t.st0) g_x[t.rowoff[e]] = xn.x;
-            if (t.st1) g_x[t.rowoff[e] + 1] = xn.y;
-          }
-        }
+        pm[e] = pc[e];
+        pc[e] = pn[e];
       }
-      g_w += PL;
-      g_x += PL;
+      so = st;
+      st = wrap_inc(st, NS_B);
+      ph ^= (st == 0);
     }
-#pragma unroll
-    for (int e = 0; e < RPW; e++) {
-      pm[e] = pc[e];
-      pc[e] = pn[e];
-    }
-    so = st;
-    st = wrap_inc(st, NS_B);
-    ph ^= (st == 0);
-  }
 
+  }
   double v[2] = {acc_rz, acc_rr}, tot[2];
-  if (grid_sum<2>(v, A.partials, &S->counter[1], sred, tot, pass_bid(G), pass_nb(G)) &&
+  if (grid_sum<2>(v, A.partials + blockIdx.z * A.pstride, &S->counter[1], sred, tot, pass_bid(G), pass_nb(G)) &&
       threadIdx.x == 0) {
-    trace_mark(S, TR_B1);
+    trace_max(A.S, TR_B1);
+    double *hist = A.hist ? A.hist + blockIdx.z * A.hstride : nullptr;
     if (A.finalize) {
       if (USE_Z)
-        finalize_rr(S, tot[1], A.hist);  // PC2: rho' comes from the sweeps
+        finalize_rr(S, tot[1], hist);  // PC2: rho' comes from the sweeps
       else
-        finalize_beta(S, tot[0], tot[1], A.hist);
+        finalize_beta(S, tot[0], tot[1], hist);
     } else if (A.fold) {
       mail_post(A.peers, MAIL_B, tot[0], tot[1], mail_seq(S->epoch, S->iter + 1), S);
       S->pend_b = 1;  // finalised by the next edge-shell kernel

@@ -270,7 +270,7 @@ constexpr int SWK = SV * SNR;    // 128 phi columns per tile
 constexpr int SWJ = POT3D_SWJ;   // tile rows
 constexpr int SWT = SWJ * SNR;   // 256 threads
 #ifndef POT3D_SPD
-#define POT3D_SPD 2
+#define POT3D_SPD 1
 #endif
 constexpr int SPD = POT3D_SPD;   // register prefetch depth (steps)
 

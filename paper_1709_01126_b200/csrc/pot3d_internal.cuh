@@ -177,7 +177,29 @@ struct Grid {
   int blk_off, blk_total;  // this launch's blocks within a reduction spanning launches
   int role_rows;           // pass A, peer memory: the first block row builds the edge shells
                            // of p_k and sends them to the neighbours (no edge-shell kernel)
+  int cj, ck;              // fused passes: thread-block clusters of cj x ck neighbouring tiles
+                           // (0/1: none; pot3d_ctx::pcj/pck, POT3D_CLUSTER)
 };
+
+// Tiles of a fused pass launch: blockIdx.x -> (tile row tj, tile column tk).  Without
+// clusters tiles run theta-fastest; with cj x ck clusters, consecutive blocks form one
+// cluster of neighbouring tiles (the grid is padded to whole clusters: blocks past the
+// grid only join the reductions), so tiles sharing halo rows / columns run side by side.
+__host__ __device__ inline int pass_tiles(const Grid &G) {
+  const int cj = G.cj > 1 ? G.cj : 1, ck = G.ck > 1 ? G.ck : 1;
+  return ((G.ntj + cj - 1) / cj) * ((G.ntk + ck - 1) / ck) * cj * ck;
+}
+__host__ __device__ inline void tile_of(const Grid &G, int b, int &tj, int &tk) {
+  const int cj = G.cj > 1 ? G.cj : 1, ck = G.ck > 1 ? G.ck : 1;
+  if (cj * ck == 1) {
+    tj = b % G.ntj;
+    tk = b / G.ntj;
+    return;
+  }
+  const int cs = cj * ck, cid = b / cs, lid = b - cid * cs, nsj = (G.ntj + cj - 1) / cj;
+  tj = (cid % nsj) * cj + lid % cj;
+  tk = (cid / nsj) * ck + lid / cj;
+}
 
 // Physical column of logical phi index k is k + COFF: physical 0 is the
 // periodic ghost copy of k = np-1 and physical np+1 the ghost copy of k = 0
@@ -223,6 +245,8 @@ struct PassArgs {
   int fold;             // peer memory, PC1: pass B posts its sums and leaves their
                         // finalisation (convergence, beta) to the next edge-shell kernel
   double *q_probe;      // k_pass_a_probe only: q = A p_k (cell layout)
+  long long pstride;    // batch (gridDim.z > 1): partials / history of RHS z start
+  long long hstride;    // z * pstride / z * hstride doubles after partials / hist
 };
 
 // CG1 (cg1.cu): TMA descriptors and arguments.  u ping-pongs between U[0], U[1] (K1
@@ -305,7 +329,8 @@ __global__ void k_finalize_beta(Scalars *S, const double *gathered, int nranks, 
 __global__ void k_finalize_rr(Scalars *S, const double *gathered, int nranks, double *hist);
 __global__ void k_finalize_rho(Scalars *S, const double *gathered, int nranks);
 __global__ void k_init_dots(Grid G, Metrics M, Scalars *S, const double *r, double *partials,
-                            int finalize, double *local_sum, int use_z, const double *z);
+                            int finalize, double *local_sum, int use_z, const double *z, int keep_b,
+                            double *hist0);
 __global__ void k_init_finalize(Scalars *S, const double *gathered, int nranks);
 __global__ void k_apply(Grid G, Metrics M, const double *x, double *y, const double *bshell,
                         int b_il, Scalars *S, double *partials, double *local_sum);

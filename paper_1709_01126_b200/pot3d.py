@@ -32,7 +32,7 @@ PC2_FELL_BACK = 2
 STATUS_NAMES = {0: "ok", 1: "not_converged", 2: "pc2_fell_back", -1: "invalid", -2: "cuda",
                 -3: "nccl", -4: "indefinite", -5: "oom", -6: "state"}
 
-EXPORTS = ["pot3d_setup", "pot3d_set_br0", "pot3d_solve", "pot3d_field", "pot3d_apply", "pot3d_apply_fused", "pot3d_kernel_trace",
+EXPORTS = ["pot3d_setup", "pot3d_set_br0", "pot3d_solve", "pot3d_solve_from", "pot3d_field", "pot3d_apply", "pot3d_apply_fused", "pot3d_kernel_trace",
            "pot3d_precond", "pot3d_history", "pot3d_info", "pot3d_profile",
            "pot3d_profile_iteration", "pot3d_trace_enable", "pot3d_kernel_times",
            "pot3d_nccl_unique_id",
@@ -62,7 +62,7 @@ class _Runtime(ctypes.Structure):
                 ("pc2_blocks", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("unroll", ctypes.c_int32), ("loopback_slabs", ctypes.c_int32),
                 ("variant", ctypes.c_int32), ("poly_degree", ctypes.c_int32),
-                ("poly_ratio", ctypes.c_double)]
+                ("poly_ratio", ctypes.c_double), ("nrhs", ctypes.c_int32)]
 
 
 class _Info(ctypes.Structure):
@@ -72,7 +72,7 @@ class _Info(ctypes.Structure):
                 ("bytes_per_iter", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("exchange", ctypes.c_int32),
                 ("chunks_a", ctypes.c_int32), ("chunks_b", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("nrhs", ctypes.c_int32)]
 
 
 _lib = None
@@ -98,6 +98,7 @@ def library(build_if_missing: bool = True):
                               ctypes.POINTER(_Runtime), ctypes.POINTER(vp)]
     L.pot3d_set_br0.argtypes = [vp, vp]
     L.pot3d_solve.argtypes = [vp, ctypes.c_double, ctypes.c_int64, vp, i64, d, d]
+    L.pot3d_solve_from.argtypes = [vp, vp, ctypes.c_double, ctypes.c_int64, vp, i64, d, d]
     L.pot3d_field.argtypes = [vp, vp, vp, vp]
     L.pot3d_apply.argtypes = [vp, vp, vp]
     L.pot3d_precond.argtypes = [vp, vp, vp]
@@ -194,12 +195,15 @@ class Pot3d:
 
     def __init__(self, r_faces, t_faces, p_faces, br0, bc=SOURCE_SURFACE, pc=PC1, *, rank=0,
                  nranks=1, nccl_id: bytes | None = None, stream=None, pc2_blocks=1, device=None,
-                 unroll=32, torch_allocator=True, loopback_slabs=0, variant=0, poly=(4, 100.0)):
+                 unroll=32, torch_allocator=True, loopback_slabs=0, variant=0, poly=(4, 100.0), nrhs=1):
         """loopback_slabs = k > 1 (single process): the grid is split into k r-slabs on
         this one device, exchanging halos and reductions through the multi-GPU
         peer-memory kernels (include/pot3d.h); arrays are then the whole grid.
         variant: 0 standard PCG, 1 single-reduction CG1.
-        pc=3: Chebyshev-accelerated Jacobi with poly = (steps m, interval ratio)."""
+        pc=3: Chebyshev-accelerated Jacobi with poly = (steps m, interval ratio).
+        nrhs = k > 1: a multi-RHS batch (SURVEY §8(f)-3) -- br0 holds k maps (k, np, nt);
+        solve() returns phi (k, np, nt, nr) and per-problem iteration counts and
+        residuals; field() arrays gain the leading k."""
         import torch
 
         if not torch.cuda.is_available():
@@ -248,6 +252,7 @@ class Pot3d:
         rt.loopback_slabs = int(loopback_slabs)
         rt.variant = int(variant)
         rt.poly_degree, rt.poly_ratio = int(poly[0]), float(poly[1])
+        rt.nrhs = int(nrhs)
         rt.device = dev
         rt.unroll = unroll
         p_br, keep = _ptr(br0)
@@ -260,6 +265,8 @@ class Pot3d:
         self.bc, self.pc_requested = bc, pc
         inf = self.info()
         self.i0, self.i1, self.nr_loc = inf["i0"], inf["i1"], inf["nr_loc"]
+        self.nrhs = inf["nrhs"]
+        self._lead = (self.nrhs,) if self.nrhs > 1 else ()  # batch: the leading axis
 
     # -- helpers ----------------------------------------------------------
     def _check(self, rc):
@@ -285,23 +292,35 @@ class Pot3d:
         self._check(self._L.pot3d_set_br0(self._ctx, p))
 
     def solve(self, rtol=1e-9, maxit=100000, want_phi=True, true_residual=True, out="numpy",
-              phi=None):
+              phi=None, x0=None, warm=False):
+        """PCG from x0 = 0 (pot3d_solve); x0 (array of phi's shape) or warm=True (the
+        context's last solution) start from there instead (pot3d_solve_from)."""
         if want_phi and phi is None:
-            phi = self._out((self.np, self.nt, self.nr_loc), out)
+            phi = self._out(self._lead + (self.np, self.nt, self.nr_loc), out)
         p_phi = _ptr(phi)[0] if phi is not None else None
-        it = ctypes.c_int64(0)
-        rr = ctypes.c_double(0)
-        tr = ctypes.c_double(0)
-        rc = self._L.pot3d_solve(self._ctx, float(rtol), int(maxit), p_phi, ctypes.byref(it),
-                                 ctypes.byref(rr), ctypes.byref(tr) if true_residual else None)
+        k = max(1, self.nrhs)
+        it = np.zeros(k, dtype=np.int64)
+        rr = np.zeros(k)
+        tr = np.full(k, np.nan)
+        outs = (p_phi, it.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                rr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if true_residual else None)
+        if x0 is not None or warm:
+            p0, keep = _ptr(x0) if x0 is not None else (None, None)
+            rc = self._L.pot3d_solve_from(self._ctx, p0, float(rtol), int(maxit), *outs)
+            del keep
+        else:
+            rc = self._L.pot3d_solve(self._ctx, float(rtol), int(maxit), *outs)
         self._check(rc)
-        return SolveResult(phi, it.value, rr.value, tr.value if true_residual else float("nan"), rc)
+        if self.nrhs > 1:
+            return SolveResult(phi, it, rr, tr, rc)
+        return SolveResult(phi, int(it[0]), float(rr[0]), float(tr[0]), rc)
 
     def field(self, out="numpy"):
         inf = self.info()
-        br = self._out((self.np, self.nt, inf["br_shells"]), out)
-        bt = self._out((self.np, self.nt + 1, self.nr_loc), out)
-        bp = self._out((self.np, self.nt, self.nr_loc), out)
+        br = self._out(self._lead + (self.np, self.nt, inf["br_shells"]), out)
+        bt = self._out(self._lead + (self.np, self.nt + 1, self.nr_loc), out)
+        bp = self._out(self._lead + (self.np, self.nt, self.nr_loc), out)
         self._check(self._L.pot3d_field(self._ctx, _ptr(br)[0], _ptr(bt)[0], _ptr(bp)[0]))
         return br, bt, bp
 

@@ -150,7 +150,18 @@ CONFIGS = {
     "pc2": Config("pc2", 151, 301, 601, pc=2, note="BASELINE configs[3]: PC2 block ILU0"),
     "pc3": Config("pc3", 151, 301, 601, pc=3, note="SURVEY 8(f)-2: Chebyshev-accelerated Jacobi"),
     "pc3large": Config("pc3large", 301, 601, 1201, pc=3, note="SURVEY 8(f)-2 on the large grid"),
+    "batch": Config("batch", 151, 301, 601, note="SURVEY 8(f)-3: 4 magnetograms (seeds 1-4) per solve",
+                    extra={"nrhs": 4}),
+    "batchsmall": Config("batchsmall", 42, 62, 122, note="SURVEY 8(f)-3 on a latency-bound grid: 8 maps",
+                         extra={"nrhs": 8}),
 }
+
+
+def batch_maps(c: Config, faces=None) -> np.ndarray:
+    """The k = c.extra["nrhs"] maps of a batch config: seeds seed .. seed+k-1 (A14)."""
+    rf, tf, pf = faces if faces is not None else c.faces()
+    k = c.extra.get("nrhs", 1)
+    return np.stack([br0_map(tf, pf, c.lmax, c.seed + q) for q in range(k)])
 
 
 def weak_config(gpus: int) -> Config:

@@ -266,3 +266,74 @@ def test_pc3_symmetric_and_effective(oracle_lib):
     ref = oracle_lib.solve(rf, tf, pf, c.br0(), rtol=1e-12)
     assert o["status"] == 0
     assert np.linalg.norm(o["x"] - ref["x"]) <= 1e-8 * np.linalg.norm(ref["x"])
+
+
+# ---------------------------------------------------------------------------
+# warm start (orc_pcg flag X0, SURVEY §8(f)-3 "repeated solves", A28)
+# ---------------------------------------------------------------------------
+def test_warm_start_from_zero_is_the_cold_loop(oracle_lib):
+    """x0 = 0 through the X0 path (r = b - A 0) gives the cold loop bitwise."""
+    c = synth.CONFIGS["tiny"]
+    rf, tf, pf = c.faces()
+    br = synth.br0_map(tf, pf, 4, 3)
+    cold = oracle_lib.solve(rf, tf, pf, br, rtol=1e-9, history=True)
+    warm = oracle_lib.solve(rf, tf, pf, br, rtol=1e-9, history=True, x0=np.zeros_like(cold["x"]))
+    assert warm["iters"] == cold["iters"] and np.array_equal(warm["x"], cold["x"])
+    assert np.array_equal(warm["hist"], cold["hist"])
+
+
+def test_warm_start_spec_2x2(oracle_lib):
+    """SPEC worked example: from the exact solution the loop stops at
+    once (iters 0, x unchanged); from x0 = (1, -1) it terminates in <= n = 2."""
+    A = np.array([[4.0, 1.0], [1.0, 3.0]])
+    b = np.array([1.0, 2.0])
+    exact = np.array([1.0 / 11.0, 7.0 / 11.0])
+    r = oracle_lib.pcg(A, b, rtol=1e-12, x0=exact)
+    assert r["iters"] == 0 and r["status"] == 0 and np.array_equal(r["x"], exact)
+    r = oracle_lib.pcg(A, b, rtol=1e-12, x0=np.array([1.0, -1.0]), history=True)
+    assert r["status"] == 0 and r["iters"] <= 2
+    assert np.allclose(r["x"], exact, rtol=0, atol=1e-14)
+    # hist[0] = ||b - A x0|| / ||b||
+    assert r["hist"][0] == pytest.approx(np.linalg.norm(b - A @ np.array([1.0, -1.0])) / np.linalg.norm(b),
+                                         rel=1e-15)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_warm_start_is_a_shifted_cold_solve(oracle_lib, seed):
+    """PCG from x0 on (A, b) builds the same Krylov sequence as PCG from 0 on
+    (A, b - A x0): x_k = x0 + e_k.  With the tolerance rescaled by
+    ||b|| / ||b - A x0|| both stop at the same iteration and agree to rounding.
+    A wrong r_0 (b, or A x0 - b) or a test against ||r_0|| breaks it."""
+    rng = np.random.default_rng(seed)
+    n = 40
+    Q = rng.standard_normal((n, n))
+    A = Q @ Q.T + n * np.eye(n) * 0.05
+    b = rng.standard_normal(n)
+    x0 = rng.standard_normal(n)
+    d = np.diag(A).copy()
+    minv = lambda v: v / d  # noqa: E731
+    warm = oracle_lib.pcg(A, b, rtol=1e-10, maxit=500, minv=minv, x0=x0)
+    r0 = b - A @ x0
+    cold = oracle_lib.pcg(A, r0, rtol=1e-10 * np.linalg.norm(b) / np.linalg.norm(r0), maxit=500, minv=minv)
+    assert warm["status"] == 0 and cold["status"] == 0
+    assert abs(warm["iters"] - cold["iters"]) <= 1
+    assert np.linalg.norm(warm["x"] - (x0 + cold["x"])) <= 1e-9 * np.linalg.norm(warm["x"])
+    assert np.linalg.norm(b - A @ warm["x"]) <= 1.5e-10 * np.linalg.norm(b)
+
+
+def test_warm_start_pot3d_converged_and_perturbed_map(oracle_lib):
+    """A map solved from its own converged Phi stops at 0 iterations; a nearby
+    map (the time-series use) converges from the previous Phi in fewer
+    iterations to the same solution as its cold solve."""
+    c = synth.CONFIGS["tiny"]
+    rf, tf, pf = synth.grid(c.nr, c.nt, c.np)
+    br = synth.br0_map(tf, pf, 6, 4)
+    a = oracle_lib.solve(rf, tf, pf, br, rtol=1e-9)
+    again = oracle_lib.solve(rf, tf, pf, br, rtol=1e-9, x0=a["x"])
+    assert again["iters"] == 0 and np.array_equal(again["x"], a["x"])
+    br2 = br + 0.01 * synth.br0_map(tf, pf, 6, 5)
+    cold = oracle_lib.solve(rf, tf, pf, br2, rtol=1e-9)
+    warm = oracle_lib.solve(rf, tf, pf, br2, rtol=1e-9, x0=a["x"])
+    assert warm["status"] == 0 and warm["iters"] < cold["iters"]
+    assert np.linalg.norm(warm["x"] - cold["x"]) <= 1e-7 * np.linalg.norm(cold["x"])
+    assert warm["true_rel_res"] <= 1.5e-9

@@ -8,7 +8,7 @@ from paper_1709_01126_b200 import build  # noqa: E402
 VARIANTS = {
     "swj4": ["POT3D_SWJ=4"],
     "swj16": ["POT3D_SWJ=16"],
-    "spd1": ["POT3D_SPD=1"],
+    "spd2": ["POT3D_SPD=2"],
     "spd3": ["POT3D_SPD=3"],
     "spd4": ["POT3D_SPD=4"],
     "pd3": [],

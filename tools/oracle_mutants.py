@@ -41,6 +41,12 @@ MUTANTS = {
         "double den = delta - gamma_new / alpha;"),
     "pcg_beta_inverted": (
         "double beta = rho_new / rho;", "double beta = rho / rho_new;"),
+    "warm_r0_ignores_x0": (
+        "for (int64_t m = 0; m < N; m++) r[m] = b[m] - r[m];",
+        "for (int64_t m = 0; m < N; m++) r[m] = b[m];"),
+    "warm_norm_of_r0_not_b": (
+        "const double bnorm = sqrt(dot(N, b, b));\n  int64_t k = 0;",
+        "const double bnorm = sqrt(dot(N, r, r));\n  int64_t k = 0;"),
     "rhs_sign": (
         "= -c * br[j + (int64_t)nt * k] * dr1;", "= c * br[j + (int64_t)nt * k] * dr1;"),
 }
