@@ -449,9 +449,21 @@ int make_map(pot3d_ctx *ctx, CUtensorMap *m, double *base, unsigned b0, unsigned
   cuuint64_t strides[2] = {(cuuint64_t)G.PK * 8, (cuuint64_t)G.plane * 8};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t es[3] = {1, 1, 1};
+  // L2 promotion of the boxes' misses: 64 B for the haloed boxes (their halo columns
+  // straddle the neighbour tiles' sectors; large pass A: ncu DRAM reads 4.3 -> 3.9 GB,
+  // 1004 -> 978 us live), 128 B for the interior boxes.  POT3D_L2PROMO = 0 / 64 / 128 /
+  // 256 overrides the haloed boxes' choice (A/B only).
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  if (b0 == SROW) {
+    const char *e = getenv("POT3D_L2PROMO");
+    const int v = e ? atoi(e) : 64;
+    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                   : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                             : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  }
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     ctx->err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
     return POT3D_ERR_CUDA;

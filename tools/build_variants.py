@@ -6,6 +6,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1709_01126_b200 import build  # noqa: E402
 
 VARIANTS = {
+    "tj30": ["POT3D_TJ=30", "POT3D_MINB=1"],          # 512-thread tiles of 30 rows, 1 block/SM
+    "tj22": ["POT3D_TJ=22", "POT3D_MINB=1"],          # 384 threads
+    "tj30r4": ["POT3D_TJ=30", "POT3D_RPW=4", "POT3D_MINB=1"],  # 256 threads, 4 rows per lane
     "swj4": ["POT3D_SWJ=4"],
     "swj16": ["POT3D_SWJ=16"],
     "spd2": ["POT3D_SPD=2"],
