@@ -117,8 +117,10 @@ typedef struct {
                                     in ONE loop whose fused passes cover all of them per
                                     launch (grid z = the problem), each with its own scalars
                                     and convergence test; the loop ends when every problem
-                                    has stopped.  One rank, no loopback slabs, PC1, standard
-                                    PCG (else POT3D_ERR_INVALID).  br0, phi, br, bt, bp then
+                                    has stopped (PC2: the k problems' ILU sweeps share one
+                                    launch per sweep, their wavefronts interleaved).  One
+                                    rank, no loopback slabs, PC1 or PC2, standard PCG (else
+                                    POT3D_ERR_INVALID).  br0, phi, br, bt, bp then
                                     hold nrhs consecutive items of the single-problem layout
                                     (item q at offset q * its size); iters, rel_residual,
                                     true_rel_residual hold nrhs values; pot3d_history returns

@@ -864,8 +864,11 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   }
   if (ctx->pc == 3) TRY(poly_apply(ctx, 1, true));
   if (pc2) {
-    int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, multi ? 0 : 1,
-                       ctx->local_sum, ctx->stream, true);
+    // a batch leader: the sweeps of all nrhs problems in one launch per sweep
+    const long long vst = ctx->nrhs > 1 ? (long long)(G.nr_loc + 2) * G.plane : 0;
+    int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->nrhs > 1 ? ctx->zpartials : ctx->partials,
+                       multi ? 0 : 1, ctx->local_sum, ctx->stream, true, nullptr, ctx->nrhs, vst,
+                       (long long)ctx->zpart_len);
     TRY(nk);
     CK(cudaGetLastError());
     ctx->n_enq += nk;
@@ -1490,8 +1493,9 @@ int pot3d_set_br0(pot3d_ctx *ctx, const double *br0) {
 
 // batch member (setup_batch): its slices of the handle's stacked vectors and scalars
 struct BatchSlot {
-  double *x, *r, *P0, *P1;
+  double *x, *r, *P0, *P1, *z;  // z: PC2 (the sweeps' output, pass A's staged vector)
   Scalars *S;
+  int q, k;                     // problem q of k (the leader q = 0 sets up the batched sweeps)
 };
 
 static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc, int32_t pc,
@@ -1708,7 +1712,10 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   } else {
     DA(ctx->P[0], cells); DA(ctx->P[1], cells);
   }
-  if (pc == POT3D_PC2 || pc == POT3D_PC3) DA(ctx->z, cells);
+  if (slot && slot->z)
+    ctx->z = slot->z;
+  else if (pc == POT3D_PC2 || pc == POT3D_PC3)
+    DA(ctx->z, cells);
   if (pc == POT3D_PC3) {
     DA(ctx->p_res, cells); DA(ctx->p_d[0], cells); DA(ctx->p_d[1], cells); DA(ctx->p_x, cells);
     for (double *p : {ctx->p_res, ctx->p_d[0], ctx->p_d[1], ctx->p_x})
@@ -1764,7 +1771,8 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
     std::vector<int> lb(ctx->pc2_blocks + 1);
     for (int b = 0; b < ctx->pc2_blocks; b++) lb[b] = bi0[ctx->rank * ctx->pc2_blocks + b] - G.i0;
     lb[ctx->pc2_blocks] = G.nr_loc;
-    rc = pc2_create(&ctx->pc2, G, ctx->pc2_blocks, lb.data(), ctx->ualloc, ctx->actx, ctx->stream);
+    rc = pc2_create(&ctx->pc2, G, ctx->pc2_blocks, lb.data(), ctx->ualloc, ctx->actx, ctx->stream,
+                    slot && slot->q == 0 ? slot->k : 1);
     if (rc) { ctx->err = "pc2_create failed"; return fail(POT3D_ERR_OOM); }
     double minpiv = 0;
     rc = pc2_factor(ctx->pc2, ctx->M, ctx->stream, &minpiv);
@@ -1926,8 +1934,9 @@ static int setup_batch(const pot3d_grid *grid, const double *br0, int32_t outer_
     h->err = "null argument or cell counts < 2 (S:45)";
     return fail(POT3D_ERR_INVALID);
   }
-  if (rt->nranks > 1 || rt->loopback_slabs > 1 || pc != POT3D_PC1 || rt->variant != 0 || k > 65535) {
-    h->err = "nrhs > 1 runs on one rank (no loopback slabs) with PC1 and standard PCG, nrhs <= 65535";
+  if (rt->nranks > 1 || rt->loopback_slabs > 1 || (pc != POT3D_PC1 && pc != POT3D_PC2) || rt->variant != 0 ||
+      k > 65535) {
+    h->err = "nrhs > 1 runs on one rank (no loopback slabs) with PC1 or PC2 and standard PCG, nrhs <= 65535";
     return fail(POT3D_ERR_INVALID);
   }
   h->nr = grid->nr;
@@ -1958,15 +1967,17 @@ static int setup_batch(const pot3d_grid *grid, const double *br0, int32_t outer_
   // the single-problem layout (setup_one): PK physical columns, nr + 2 planes
   const long long PK = round_up(h->np + COFF + 1, 16);
   const size_t cells = (size_t)(h->nr + 2) * h->nt * PK;
-  double *X = nullptr, *R = nullptr, *P0 = nullptr, *P1 = nullptr;
+  double *X = nullptr, *R = nullptr, *P0 = nullptr, *P1 = nullptr, *Z = nullptr;
   Scalars *S = nullptr;
   int rc = 0;
   if ((rc = dalloc(h, &X, cells * k)) || (rc = dalloc(h, &R, cells * k)) || (rc = dalloc(h, &P0, cells * k)) ||
-      (rc = dalloc(h, &P1, cells * k)) || (rc = dalloc(h, &S, (size_t)k)))
+      (rc = dalloc(h, &P1, cells * k)) || (rc = dalloc(h, &S, (size_t)k)) ||
+      (pc == POT3D_PC2 && (rc = dalloc(h, &Z, cells * k))))
     return fail(rc);
   const size_t nmap = (size_t)h->nt * h->np;
   for (int q = 0; q < k; q++) {
-    BatchSlot sl{X + q * cells, R + q * cells, P0 + q * cells, P1 + q * cells, S + q};
+    BatchSlot sl{X + q * cells, R + q * cells, P0 + q * cells, P1 + q * cells, Z ? Z + q * cells : nullptr, S + q,
+                 q, k};
     pot3d_runtime Rq = *rt;
     Rq.nrhs = 1;
     Rq.device = h->device;
@@ -2415,8 +2426,9 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
       TRY(poly_apply(ctx, 1, false));
     }
     if (pc2) {
-      int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 1, ctx->local_sum,
-                         s, true);
+      const long long vst = nS > 1 ? (long long)(G.nr_loc + 2) * G.plane : 0;
+      int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, nS > 1 ? ctx->zpartials : ctx->partials, 1,
+                         ctx->local_sum, s, true, nullptr, nS, vst, (long long)ctx->zpart_len);
       TRY(nk);
       ctx->n_launch += nk;
     }

@@ -62,7 +62,8 @@ struct Pc2 {
   int2 *d_orderS;           // k_sweepS: tiles by estimated start step tj*SWJ + tk
   bool scan;                // k_sweepS (default) or k_sweep4 (POT3D_PC2_SWEEP=4)
   double *edge4;
-  long long edge4_len;
+  long long edge4_len;      // all problems' slots (nrhs x the per-problem slots)
+  int nrhs;                 // problems per sweep launch (a batch leader: pot3d_runtime.nrhs)
   std::vector<void *> allocs;
   size_t bytes;
 };
@@ -86,6 +87,8 @@ struct SweepArgs {
   int finalize;      // BWD: 1 single rank (rho/beta), 0 local_sum
   double *local_sum;
   const PeerTab *peers;  // BWD, nranks > 1 with peer memory: post r.z to every mailbox
+  int nrhs;              // k_sweepS of a batch: problems per launch (tickets interleave them)
+  long long vstride, pstride;  // a batch: doubles between the problems' vectors / partials
 };
 
 // Tile-edge handoff without flags or fences: the bottom row / right column of
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(SWT, 1) k_sweep4(SweepArgs A, int koff, int nt
   if (__syncthreads_or(proto) && tid == 0) atomicOr(&A.sync[1], 2);  // protocol error
   if (MODE == SW_BWD) {
     double v[1] = {acc}, tot[1];
-    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket) && tid == 0) {
+    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket, A.nblk * A.ntiles) && tid == 0) {
       if (A.finalize)
         finalize_rho(A.S, tot[0]);
       else if (A.peers)
@@ -798,7 +801,7 @@ __device__ __forceinline__ void sweepS_body(const SweepArgs &A, int koff, int nt
   if (__syncthreads_or(proto) && tid == 0) atomicOr(&A.sync[1], 2);
   if (MODE == SW_BWD) {
     double v[1] = {acc}, tot[1];
-    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket) && tid == 0) {
+    if (grid_sum<1>(v, A.partials, &A.S->counter[2], sred, tot, ticket, A.nblk * A.ntiles) && tid == 0) {
       if (A.finalize)
         finalize_rho(A.S, tot[0]);
       else if (A.peers)
@@ -809,14 +812,28 @@ __device__ __forceinline__ void sweepS_body(const SweepArgs &A, int koff, int nt
   }
 }
 
+// A batch (A.nrhs > 1): ticket t is problem t % nrhs's ticket t / nrhs, so the
+// problems' wavefronts advance side by side and every wait is still on a tile of the
+// same problem taken earlier; a stopped problem's CTAs leave after their ticket.
 template <int MODE>
 __global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int ntk4) {
-  if (A.predicated && A.S->stop) return;
+  if (A.nrhs <= 1 && A.predicated && A.S->stop) return;
   __shared__ int s_ticket;
   __shared__ double sred[SWT / 32];
   if (threadIdx.x == 0) s_ticket = atomicAdd(&A.sync[0], 1);
   __syncthreads();
-  const int ticket = s_ticket;
+  int ticket = s_ticket;
+  if (A.nrhs > 1) {
+    const int q = ticket % A.nrhs;
+    ticket /= A.nrhs;
+    A.S += q;
+    if (A.predicated && A.S->stop) return;
+    A.r += q * A.vstride;
+    A.z += q * A.vstride;
+    A.partials += q * A.pstride;
+    A.edge_len /= A.nrhs;
+    A.edge += q * A.edge_len;
+  }
   const int2 tl = A.order[ticket / A.nblk];
   const int kv_lo = koff + tl.y * SWK;
   const bool full = (tl.x + 1) * SWJ <= A.G.nt && kv_lo >= 0 && kv_lo + SWK <= A.G.np;
@@ -833,7 +850,9 @@ __global__ void k_fill_u64(unsigned long long *a, long long n, unsigned long lon
 }
 
 // periodic ghost columns of z (read by the TMA boxes of pass A)
-__global__ void k_pc2_ghost(Grid G, double *a, const Scalars *S, int predicated) {
+__global__ void k_pc2_ghost(Grid G, double *a, const Scalars *S, int predicated, long long vstride) {
+  S += blockIdx.y;  // a batch: problem blockIdx.y
+  a += blockIdx.y * vstride;
   if (predicated && S->stop) return;
   const long long rows = (long long)G.nr_loc * G.nt;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < rows;
@@ -859,9 +878,10 @@ static void *p_alloc(Pc2 *P, size_t bytes, void *(*alloc)(size_t, void *), void 
 }
 
 int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
-               void *(*alloc)(size_t, void *), void *actx, cudaStream_t s) {
+               void *(*alloc)(size_t, void *), void *actx, cudaStream_t s, int nrhs) {
   Pc2 *P = new Pc2();
   P->G = G;
+  P->nrhs = std::max(nrhs, 1);
   P->nblk = nblocks_local;
   P->ntj = (G.nt + WJ - 1) / WJ;
   P->ntk = (G.np + WK - 1) / WK;
@@ -886,7 +906,7 @@ int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
   P->ntj4 = (G.nt + SWJ - 1) / SWJ;
   P->ntk4 = std::max((G.np - P->koff_f + SWK - 1) / SWK, (G.np - P->koff_b + SWK - 1) / SWK);
   P->ntiles4 = P->ntj4 * P->ntk4;
-  P->edge4_len = (long long)P->nblk * P->ntiles4 * P->nbmax * (SNR * SV + SWJ * 2);
+  P->edge4_len = (long long)P->nblk * P->ntiles4 * P->nbmax * (SNR * SV + SWJ * 2) * P->nrhs;
   P->d_order4 = (int2 *)p_alloc(P, sizeof(int2) * P->ntiles4, alloc, actx);
   P->d_orderS = (int2 *)p_alloc(P, sizeof(int2) * P->ntiles4, alloc, actx);
   P->edge4 = (double *)p_alloc(P, sizeof(double) * P->edge4_len, alloc, actx);
@@ -995,29 +1015,40 @@ int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host)
 static thread_local std::string g_pc2_err;
 
 int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, double *partials,
-              int finalize, double *local_sum, cudaStream_t s, bool iteration, const PeerTab *peers) {
+              int finalize, double *local_sum, cudaStream_t s, bool iteration, const PeerTab *peers,
+              int nrhs, long long vstride, long long pstride) {
   const int pred = iteration ? 1 : 0;
+  const int nk = std::max(nrhs, 1);
+  if (nk > P->nrhs || (nk > 1 && !P->scan)) {
+    g_pc2_err = "PC2 batch: the sweeps were set up for fewer problems (or POT3D_PC2_SWEEP=4)";
+    return -1;
+  }
   SweepArgs a = sweep_args(P, M, S, r, z, partials, pred, finalize, local_sum);
+  a.nrhs = nk;
+  a.vstride = vstride;
+  a.pstride = pstride;
   a.peers = iteration ? peers : nullptr;
   if (!iteration) a.finalize = 0, a.local_sum = local_sum;
   // run-vectorised / row-scan sweeps: their own tile order and edge slots
   a.order = P->scan ? P->d_orderS : P->d_order4;
   a.edge = P->edge4;
-  a.edge_len = P->edge4_len;
+  a.edge_len = P->edge4_len / P->nrhs * nk;  // the slots of the nk problems
   a.ntiles = P->ntiles4;
   cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);  // ticket only (flags accumulate)
   if (P->scan)
-    k_sweepS<SW_FWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_FWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_f, P->ntk4);
+    k_sweepS<SW_FWD><<<P->nblk * P->ntiles4 * nk, SWT, Sw4<SW_FWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_f,
+                                                                                               P->ntk4);
   else
     k_sweep4<SW_FWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_FWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_f, P->ntk4);
   cudaMemsetAsync(P->d_sync, 0, sizeof(int), s);
   if (P->scan)
-    k_sweepS<SW_BWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_BWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_b, P->ntk4);
+    k_sweepS<SW_BWD><<<P->nblk * P->ntiles4 * nk, SWT, Sw4<SW_BWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_b,
+                                                                                               P->ntk4);
   else
     k_sweep4<SW_BWD><<<P->nblk * P->ntiles4, SWT, Sw4<SW_BWD>::SMEM + 16 * P->nbmax, s>>>(a, P->koff_b, P->ntk4);
   const Grid &G = P->G;
-  k_pc2_ghost<<<(unsigned)std::min<long long>(((long long)G.nr_loc * G.nt + 255) / 256, 4096), 256, 0,
-                s>>>(G, z, S, pred);
+  k_pc2_ghost<<<dim3((unsigned)std::min<long long>(((long long)G.nr_loc * G.nt + 255) / 256, 4096), nk), 256,
+                0, s>>>(G, z, S, pred, vstride);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_pc2_err = std::string("PC2 sweep launch: ") + cudaGetErrorString(e);

@@ -358,14 +358,18 @@ __global__ void k_finalize_mail(Scalars *S, const PeerTab *peers, int kind, int 
 
 // pc2.cu -- PC2 (block ILU0 = D-ILU, A11) with tiled sync-free wavefront sweeps
 struct Pc2;
+// nrhs > 1: the sweeps of a batch leader cover nrhs problems per launch (edge slots per
+// problem; pot3d_runtime.nrhs, abi.cu setup_batch)
 int pc2_create(Pc2 **out, const Grid &G, int nblocks_local, const int *block_l0,
-               void *(*alloc)(size_t, void *), void *actx, cudaStream_t s);
+               void *(*alloc)(size_t, void *), void *actx, cudaStream_t s, int nrhs = 1);
 int pc2_factor(Pc2 *P, const Metrics &M, cudaStream_t s, double *min_pivot_host);
 // z = M^-1 r; partial r.z -> finalize (single rank: rho/beta update, mode iteration) or
 // local_sum[0]; `iteration` selects the predicated in-loop variant.
+// A batch (nrhs > 1, the Pc2 created for it): problem q's r, z start q * vstride doubles
+// on, its scalars are S[q], its partials q * pstride doubles on.
 int pc2_apply(Pc2 *P, const Metrics &M, Scalars *S, const double *r, double *z, double *partials,
               int finalize, double *local_sum, cudaStream_t s, bool iteration,
-              const PeerTab *peers = nullptr);
+              const PeerTab *peers = nullptr, int nrhs = 1, long long vstride = 0, long long pstride = 0);
 void pc2_destroy(Pc2 *P, void (*fr)(void *, void *), void *actx);
 int pc2_status(Pc2 *P, cudaStream_t s);
 size_t pc2_bytes(const Pc2 *P);

@@ -154,6 +154,8 @@ CONFIGS = {
                     extra={"nrhs": 4}),
     "batchsmall": Config("batchsmall", 42, 62, 122, note="SURVEY 8(f)-3 on a latency-bound grid: 8 maps",
                          extra={"nrhs": 8}),
+    "batchpc2": Config("batchpc2", 151, 301, 601, pc=2, note="SURVEY 8(f)-3 with PC2: 4 maps, interleaved sweeps",
+                       extra={"nrhs": 4}),
 }
 
 

@@ -160,8 +160,35 @@ def test_batch_medium_sampled_against_oracle():
         assert res.iters[q] == one.iters and np.array_equal(res.phi[q], one.phi), q
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("blocks", [1, 3])
+def test_batch_pc2_equals_single_solves(blocks):
+    """PC2 batches: the sweeps of all problems run in one launch per sweep, their
+    wavefronts interleaved ticket by ticket (pc2.cu k_sweepS); each problem equals
+    its single PC2 solve bitwise and the oracle's block ILU0 solve within its spread."""
+    from paper_1709_01126_b200 import Pot3d
+
+    c = synth.CONFIGS["small"]
+    rf, tf, pf = c.faces()
+    br = maps(tf, pf, [1, 5, 6])
+    br[2] *= 0.0  # a problem that stops at once beside two that run
+    with Pot3d(rf, tf, pf, br, pc=2, pc2_blocks=blocks, nrhs=3) as s:
+        assert s.info()["pc"] == 2
+        res = s.solve(rtol=1e-9)
+        again = s.solve(rtol=1e-9)
+    assert res.status == 0 and res.iters[2] == 0 and not res.phi[2].any()
+    assert np.array_equal(again.phi, res.phi) and np.array_equal(again.iters, res.iters)
+    for q in range(2):
+        with Pot3d(rf, tf, pf, br[q], pc=2, pc2_blocks=blocks) as one:
+            r1 = one.solve(rtol=1e-9)
+        assert res.iters[q] == r1.iters and np.array_equal(res.phi[q], r1.phi), q
+        ref = oracle.solve(rf, tf, pf, br[q], pc=2, pc2_blocks=blocks, rtol=1e-9)
+        assert abs(int(res.iters[q]) - ref["iters"]) <= 2, (q, res.iters[q], ref["iters"])
+        assert np.linalg.norm(res.phi[q] - ref["x"]) <= 1e-9 * np.linalg.norm(ref["x"])
+
+
 def test_batch_rejects_unsupported_combinations():
-    """nrhs > 1 is single-rank PC1 standard PCG: other combinations are refused
+    """nrhs > 1 is single-rank PC1 / PC2 standard PCG: other combinations are refused
     with POT3D_ERR_INVALID before any device work (runs without a GPU)."""
     from paper_1709_01126_b200 import pot3d as P
 
@@ -170,7 +197,7 @@ def test_batch_rejects_unsupported_combinations():
     br = np.zeros((2, 8, 6))
     dp = ctypes.POINTER(ctypes.c_double)
     g = P._Grid(4, 6, 8, rf.ctypes.data_as(dp), tf.ctypes.data_as(dp), pf.ctypes.data_as(dp))
-    for field, val, pc in (("variant", 1, 1), ("loopback_slabs", 2, 1), ("nranks", 2, 1), (None, 0, 2), (None, 0, 3)):
+    for field, val, pc in (("variant", 1, 1), ("loopback_slabs", 2, 1), ("nranks", 2, 1), (None, 0, 3)):
         rt = P._Runtime()
         rt.nranks, rt.nrhs, rt.device = 1, 2, -1
         if field:
