@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="large",
                     choices=["tiny", "small", "medium", "large", "pc2", "pc3", "pc3large", "batch", "batchsmall", "batchpc2",
+                             "batchpc3",
                              "weak"])
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
     ap.add_argument("--pc2-blocks", type=int, default=1)

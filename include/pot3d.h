@@ -118,9 +118,9 @@ typedef struct {
                                     launch (grid z = the problem), each with its own scalars
                                     and convergence test; the loop ends when every problem
                                     has stopped (PC2: the k problems' ILU sweeps share one
-                                    launch per sweep, their wavefronts interleaved).  One
-                                    rank, no loopback slabs, PC1 or PC2, standard PCG (else
-                                    POT3D_ERR_INVALID).  br0, phi, br, bt, bp then
+                                    launch per sweep, their wavefronts interleaved; PC3: the
+                                    Chebyshev steps too).  One rank, no loopback slabs,
+                                    standard PCG (else POT3D_ERR_INVALID).  br0, phi, br, bt, bp then
                                     hold nrhs consecutive items of the single-problem layout
                                     (item q at offset q * its size); iters, rel_residual,
                                     true_rel_residual hold nrhs values; pot3d_history returns

@@ -740,8 +740,9 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
   return st;
 }
 
-// PC3: z = M^-1 r (ctx->r -> ctx->z), the partial r.z to rho/beta (finalize) or local_sum
-int poly_apply(pot3d_ctx *ctx, int finalize, bool iteration) {
+// PC3: z = M^-1 r (ctx->r -> ctx->z), the partial r.z to rho/beta (finalize) or local_sum.
+// nz: problems covered (a batch leader's loop and profile: nrhs; the start of a solve: 1)
+int poly_apply(pot3d_ctx *ctx, int finalize, bool iteration, int nz = 1) {
   const Grid &G = ctx->G;
   PolyArgs a{};
   a.G = G;
@@ -758,14 +759,15 @@ int poly_apply(pot3d_ctx *ctx, int finalize, bool iteration) {
     a.c1[k] = ctx->p_c1[k];
     a.c2[k] = ctx->p_c2[k];
   }
-  a.partials = ctx->partials;
+  a.partials = nz > 1 ? ctx->zpartials : ctx->partials;
+  a.pstride = nz > 1 ? (long long)ctx->zpart_len : 0;
   a.local_sum = ctx->local_sum;
   a.finalize = finalize;
   a.predicated = iteration ? 1 : 0;
   const bool pdl = ctx->pdl && iteration;
-  CK(launch_k(pdl, k_poly_init, dim3(148 * 8), dim3(256), 0, ctx->stream, a));
+  CK(launch_k(pdl, k_poly_init, dim3(148 * 8, nz), dim3(256), 0, ctx->stream, a));
   a.G.nchunks = ctx->nchunks_b;
-  const dim3 grd(G.ntj * G.ntk, ctx->nchunks_b);
+  const dim3 grd(G.ntj * G.ntk, ctx->nchunks_b, nz);
   for (int k = 1; k < ctx->poly_m; k++)
     CK(launch_k(pdl, k + 1 == ctx->poly_m ? k_poly_last : k_poly_step, grd, dim3(NTHREADS), SMEM_P, ctx->stream,
                 ctx->pmaps, a, k));
@@ -862,7 +864,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     CK(cudaGetLastError());
     ctx->n_enq++;
   }
-  if (ctx->pc == 3) TRY(poly_apply(ctx, 1, true));
+  if (ctx->pc == 3) TRY(poly_apply(ctx, 1, true, ctx->nrhs));
   if (pc2) {
     // a batch leader: the sweeps of all nrhs problems in one launch per sweep
     const long long vst = ctx->nrhs > 1 ? (long long)(G.nr_loc + 2) * G.plane : 0;
@@ -1493,7 +1495,8 @@ int pot3d_set_br0(pot3d_ctx *ctx, const double *br0) {
 
 // batch member (setup_batch): its slices of the handle's stacked vectors and scalars
 struct BatchSlot {
-  double *x, *r, *P0, *P1, *z;  // z: PC2 (the sweeps' output, pass A's staged vector)
+  double *x, *r, *P0, *P1, *z;  // z: PC2 / PC3 (M^-1 r, pass A's staged vector)
+  double *pres, *pd0, *pd1, *px;  // PC3: the Chebyshev steps' res, d_0, d_1, z_k
   Scalars *S;
   int q, k;                     // problem q of k (the leader q = 0 sets up the batched sweeps)
 };
@@ -1717,7 +1720,14 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   else if (pc == POT3D_PC2 || pc == POT3D_PC3)
     DA(ctx->z, cells);
   if (pc == POT3D_PC3) {
-    DA(ctx->p_res, cells); DA(ctx->p_d[0], cells); DA(ctx->p_d[1], cells); DA(ctx->p_x, cells);
+    if (slot) {
+      ctx->p_res = slot->pres;
+      ctx->p_d[0] = slot->pd0;
+      ctx->p_d[1] = slot->pd1;
+      ctx->p_x = slot->px;
+    } else {
+      DA(ctx->p_res, cells); DA(ctx->p_d[0], cells); DA(ctx->p_d[1], cells); DA(ctx->p_x, cells);
+    }
     for (double *p : {ctx->p_res, ctx->p_d[0], ctx->p_d[1], ctx->p_x})
       if (cudaMemsetAsync(p, 0, cells * sizeof(double), ctx->stream)) { ctx->err = "memset"; return fail(POT3D_ERR_CUDA); }
     // Saad Alg. 12.1 coefficients on [a, b] = [2 / ratio, 2] (the oracle's arithmetic)
@@ -1934,9 +1944,8 @@ static int setup_batch(const pot3d_grid *grid, const double *br0, int32_t outer_
     h->err = "null argument or cell counts < 2 (S:45)";
     return fail(POT3D_ERR_INVALID);
   }
-  if (rt->nranks > 1 || rt->loopback_slabs > 1 || (pc != POT3D_PC1 && pc != POT3D_PC2) || rt->variant != 0 ||
-      k > 65535) {
-    h->err = "nrhs > 1 runs on one rank (no loopback slabs) with PC1 or PC2 and standard PCG, nrhs <= 65535";
+  if (rt->nranks > 1 || rt->loopback_slabs > 1 || rt->variant != 0 || k > 65535) {
+    h->err = "nrhs > 1 runs on one rank (no loopback slabs) with standard PCG, nrhs <= 65535";
     return fail(POT3D_ERR_INVALID);
   }
   h->nr = grid->nr;
@@ -1968,16 +1977,20 @@ static int setup_batch(const pot3d_grid *grid, const double *br0, int32_t outer_
   const long long PK = round_up(h->np + COFF + 1, 16);
   const size_t cells = (size_t)(h->nr + 2) * h->nt * PK;
   double *X = nullptr, *R = nullptr, *P0 = nullptr, *P1 = nullptr, *Z = nullptr;
+  double *PR = nullptr, *PD0 = nullptr, *PD1 = nullptr, *PX = nullptr;
   Scalars *S = nullptr;
   int rc = 0;
   if ((rc = dalloc(h, &X, cells * k)) || (rc = dalloc(h, &R, cells * k)) || (rc = dalloc(h, &P0, cells * k)) ||
       (rc = dalloc(h, &P1, cells * k)) || (rc = dalloc(h, &S, (size_t)k)) ||
-      (pc == POT3D_PC2 && (rc = dalloc(h, &Z, cells * k))))
+      (pc >= POT3D_PC2 && (rc = dalloc(h, &Z, cells * k))) ||
+      (pc == POT3D_PC3 && ((rc = dalloc(h, &PR, cells * k)) || (rc = dalloc(h, &PD0, cells * k)) ||
+                           (rc = dalloc(h, &PD1, cells * k)) || (rc = dalloc(h, &PX, cells * k)))))
     return fail(rc);
+  auto at = [&](double *base, int q) { return base ? base + q * cells : nullptr; };
   const size_t nmap = (size_t)h->nt * h->np;
   for (int q = 0; q < k; q++) {
-    BatchSlot sl{X + q * cells, R + q * cells, P0 + q * cells, P1 + q * cells, Z ? Z + q * cells : nullptr, S + q,
-                 q, k};
+    BatchSlot sl{at(X, q),  at(R, q),   at(P0, q),  at(P1, q), at(Z, q), at(PR, q),
+                 at(PD0, q), at(PD1, q), at(PX, q), S + q,    q,        k};
     pot3d_runtime Rq = *rt;
     Rq.nrhs = 1;
     Rq.device = h->device;
@@ -2423,7 +2436,7 @@ int pot3d_profile(pot3d_ctx *ctx, int32_t iters, double *ms_pass_a, double *ms_p
     CK(cudaEventRecord(ev[2], s));
     ctx->n_launch += 2;
     if (ctx->pc == 3) {
-      TRY(poly_apply(ctx, 1, false));
+      TRY(poly_apply(ctx, 1, false, nS));
     }
     if (pc2) {
       const long long vst = nS > 1 ? (long long)(G.nr_loc + 2) * G.plane : 0;

@@ -109,6 +109,41 @@ __device__ __forceinline__ double stencil7f(double c, double ip, double Fd, doub
          P.dr * R.q * (appk * (c - kp) + apmk * (c - km));
 }
 
+// The stencil with one theta face term tj and one phi face term tk already formed by
+// the neighbouring cell of the same thread (FAST tiles, face_terms below): the other
+// theta neighbour jo with coefficient ajo, the other phi neighbour ko with ako.
+__device__ __forceinline__ double stencil7s(double c, double ip, double im, double tj, double ajo, double jo,
+                                            double tk, double ako, double ko, double dpk, const PlaneC &P,
+                                            const RowC &R) {
+  return dpk * (R.g * (P.arp * (c - ip) + P.arm * (c - im) + P.ss * c) + P.dr * fma(ajo, c - jo, tj)) +
+         P.dr * R.q * fma(ako, c - ko, tk);
+}
+// ... and with the r flux shared as in stencil7f
+__device__ __forceinline__ double stencil7fs(double c, double ip, double Fd, double tj, double ajo, double jo,
+                                             double tk, double ako, double ko, double dpk, const PlaneC &P,
+                                             const RowC &R, double &Fu) {
+  Fu = P.arp * (c - ip);
+  return dpk * (R.g * (Fu + Fd + P.ss * c) + P.dr * fma(ajo, c - jo, tj)) + P.dr * R.q * fma(ako, c - ko, tk);
+}
+
+// A thread's 2 x 2 cells (rows e = 0, 1; columns x, y) share their inner faces: the theta
+// face between the rows, atp_j (c_j - c_{j+1}), is -(atm_{j+1} (c_{j+1} - c_j)) exactly
+// (atm_{j+1} == atp_j bitwise, k_metrics), and the phi face app_k (c_k - c_{k+1}) is
+// -(apm_{k+1} (c_{k+1} - c_k)).  Valid on FAST tiles (every row and column an interior
+// grid line away from the poles' halo rows and the periodic seam).
+struct FaceTerms {
+  double tx, ty;   // theta face between row 0 and row 1, columns x and y (row 0's view)
+  double p0, p1;   // phi face between x and y, rows 0 and 1 (x's view)
+};
+__device__ __forceinline__ FaceTerms face_terms(double2 c0, double2 c1, const RowC &R0, double appx) {
+  FaceTerms f;
+  f.tx = R0.atp * (c0.x - c1.x);
+  f.ty = R0.atp * (c0.y - c1.y);
+  f.p0 = appx * (c0.x - c0.y);
+  f.p1 = appx * (c1.x - c1.y);
+  return f;
+}
+
 // Statically allocated shared state of a pass (declared once per kernel, so the
 // FAST and general instantiations of a body share it).
 struct PassShared {
@@ -166,13 +201,14 @@ __device__ __forceinline__ TileThread tile_thread(const Grid &G) {
 }
 
 // A tile whose 64 columns k0-1 .. k0+62 are all interior cells away from the
-// periodic seam (no masks, no ghost-column duplicates): block-uniform, selects the
-// FAST instantiation of the passes.
+// periodic seam (no masks, no ghost-column duplicates) and whose haloed rows are all
+// grid rows: block-uniform, selects the FAST instantiation of the passes.
 __device__ __forceinline__ bool tile_fast(const Grid &G) {
   int tj, tk;
   tile_of(G, blockIdx.x, tj, tk);
-  const int k0 = tk * TK;
-  return tj < G.ntj && k0 >= TK && k0 + TK <= G.np;
+  const int k0 = tk * TK, j0 = tj * TJ;
+  // every haloed row j0-1 .. j0+TJ a grid row too (the shared theta faces, face_terms)
+  return tj < G.ntj && k0 >= TK && k0 + TK <= G.np && j0 >= 1 && j0 + TJ <= G.nt - 1;
 }
 
 // Store of a lane's column pair (interior elements only) with the periodic

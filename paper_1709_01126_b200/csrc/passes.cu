@@ -185,9 +185,9 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
     // One plane step.  STENCIL = false only for q = 0, 1 (peeled), so the steady
     // state is one basic block: the transform's fp64 chains (plane q) and the
     // stencil of plane q-1 are independent and can be interleaved by the scheduler.
-  #if POT3D_A_FLUX
+#if POT3D_A_FLUX
     double2 fl[RPW];  // upper r flux arp (c - ip) of the last stencil plane, per row and cell
-  #endif
+#endif
     auto step = [&](auto U, auto STENCIL, int q, auto FIRST) {
       constexpr int u = decltype(U)::value;       // stage, slot and register set of plane q
       constexpr bool do_st = decltype(STENCIL)::value;
@@ -228,6 +228,8 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
       // ---- stencil of plane il-1 (its slot was completed before this barrier) ----
       if (do_st) {
         const double *sb = &sm.pn[um][0][0];
+        // FAST tiles: the faces between the thread's two rows and two columns, once
+        const FaceTerms ft = face_terms(R[um][0], R[um][RPW - 1], rw[0], ap.x);
 #pragma unroll
         for (int e = 0; e < RPW; e++) {
           if (!t.stencil[e]) continue;  // halo rows (warp-uniform)
@@ -237,17 +239,28 @@ __device__ __forceinline__ void pass_a_body(const TMaps &T, const PassArgs &A, i
           const double2 up = (RPW == 2 && e == 1) ? R[um][0] : *reinterpret_cast<const double2 *>(so + up_off[e]);
           const double2 dn = (RPW == 2 && e == 0) ? R[um][RPW - 1] : *reinterpret_cast<const double2 *>(so + dn_off[e]);
           const double lf = so[-1], rt = so[2];
-  #if POT3D_A_FLUX
+#if POT3D_A_FLUX
           // lower r flux: computed on the chunk's first stencil plane, then the negated
           // upper flux of the previous plane
           const double fdx = first ? Ps.arm * (c.x - R[umm][e].x) : -fl[e].x;
           const double fdy = first ? Ps.arm * (c.y - R[umm][e].y) : -fl[e].y;
-          const double q0 = stencil7f(c.x, R[u][e].x, fdx, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e], fl[e].x);
-          const double q1 = stencil7f(c.y, R[u][e].y, fdy, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e], fl[e].y);
-  #else
+          double q0, q1;
+          if (FAST && RPW == 2) {  // the shared theta / phi faces (face_terms)
+            const double pk = e == 0 ? ft.p0 : ft.p1;
+            const double2 jo = e == 0 ? up : dn;  // the theta neighbour outside the thread
+            const double ajo = e == 0 ? rw[0].atm : rw[RPW - 1].atp;
+            q0 = stencil7fs(c.x, R[u][e].x, fdx, e == 0 ? ft.tx : -ft.tx, ajo, jo.x, pk, am.x, lf, dp.x, Ps, rw[e],
+                            fl[e].x);
+            q1 = stencil7fs(c.y, R[u][e].y, fdy, e == 0 ? ft.ty : -ft.ty, ajo, jo.y, -pk, ap.y, rt, dp.y, Ps, rw[e],
+                            fl[e].y);
+          } else {
+            q0 = stencil7f(c.x, R[u][e].x, fdx, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e], fl[e].x);
+            q1 = stencil7f(c.y, R[u][e].y, fdy, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e], fl[e].y);
+          }
+#else
           const double q0 = stencil7(c.x, R[u][e].x, R[umm][e].x, dn.x, up.x, c.y, lf, dp.x, ap.x, am.x, Ps, rw[e]);
           const double q1 = stencil7(c.y, R[u][e].y, R[umm][e].y, dn.y, up.y, rt, c.x, dp.y, ap.y, am.y, Ps, rw[e]);
-  #endif
+#endif
           acc += (m0 ? c.x * q0 : 0.0) + (m1 ? c.y * q1 : 0.0);
           // diagnostic instantiation only (pot3d_apply_fused which = 2): q of plane il-1
           if (PROBE) store_pair<FAST>(A.q_probe + (long long)il * PL + t.rowoff[e], t, G.np, make_double2(q0, q1), false);
@@ -373,6 +386,7 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
       for (int e = 0; e < RPW; e++) pn[e] = *reinterpret_cast<const double2 *>(&sm.pn[st][t.row[e]][cs]);
       if (q >= 2) {
         const double *sb = &sm.pn[so][0][0];
+        const FaceTerms ft = face_terms(pc[0], pc[RPW - 1], rw[0], ap.x);  // FAST: shared faces
 #pragma unroll
         for (int e = 0; e < RPW; e++) {
           if (!t.stencil[e]) continue;
@@ -381,8 +395,19 @@ __device__ __forceinline__ void pass_b_body(const TMaps &T, const PassArgs &A, i
           const double2 up = (RPW == 2 && e == 1) ? pc[0] : *reinterpret_cast<const double2 *>(sr - SROW);
           const double2 dn = (RPW == 2 && e == 0) ? pc[RPW - 1] : *reinterpret_cast<const double2 *>(sr + SROW);
           const double lf = sr[-1], rt = sr[2];
-          const double q0 = stencil7(pc[e].x, pn[e].x, pm[e].x, dn.x, up.x, pc[e].y, lf, dp.x, ap.x, am.x, P, rw[e]);
-          const double q1 = stencil7(pc[e].y, pn[e].y, pm[e].y, dn.y, up.y, rt, pc[e].x, dp.y, ap.y, am.y, P, rw[e]);
+          double q0, q1;
+          if (FAST && RPW == 2) {
+            const double pk = e == 0 ? ft.p0 : ft.p1;
+            const double2 jo = e == 0 ? up : dn;
+            const double ajo = e == 0 ? rw[0].atm : rw[RPW - 1].atp;
+            q0 = stencil7s(pc[e].x, pn[e].x, pm[e].x, e == 0 ? ft.tx : -ft.tx, ajo, jo.x, pk, am.x, lf, dp.x, P,
+                           rw[e]);
+            q1 = stencil7s(pc[e].y, pn[e].y, pm[e].y, e == 0 ? ft.ty : -ft.ty, ajo, jo.y, -pk, ap.y, rt, dp.y, P,
+                           rw[e]);
+          } else {
+            q0 = stencil7(pc[e].x, pn[e].x, pm[e].x, dn.x, up.x, pc[e].y, lf, dp.x, ap.x, am.x, P, rw[e]);
+            q1 = stencil7(pc[e].y, pn[e].y, pm[e].y, dn.y, up.y, rt, pc[e].x, dp.y, ap.y, am.y, P, rw[e]);
+          }
           const double2 rv = *reinterpret_cast<const double2 *>(&sm.r[so][r - 1][2 * t.lane]);
           double2 rn, xn;  // rn: the stored vector after the update (PC1: z, PC2: r)
           if (XM != XM_SKIP) {

@@ -268,7 +268,7 @@ constexpr int SV = 4;            // cells per thread along phi
 constexpr int SNR = 32;          // runs per tile row (one warp)
 constexpr int SWK = SV * SNR;    // 128 phi columns per tile
 #ifndef POT3D_SWJ
-#define POT3D_SWJ 8
+#define POT3D_SWJ 16
 #endif
 constexpr int SWJ = POT3D_SWJ;   // tile rows
 constexpr int SWT = SWJ * SNR;   // 256 threads
@@ -815,8 +815,14 @@ __device__ __forceinline__ void sweepS_body(const SweepArgs &A, int koff, int nt
 // A batch (A.nrhs > 1): ticket t is problem t % nrhs's ticket t / nrhs, so the
 // problems' wavefronts advance side by side and every wait is still on a tile of the
 // same problem taken earlier; a stopped problem's CTAs leave after their ticket.
+// CTAs per SM the row-scan sweeps are compiled for.  Measured (tools/gpu/sws2.sh): 16-row
+// tiles at one CTA per SM beat 8-row tiles at one or two (medium 1477 vs 1520 / 1619 us
+// per sweep pair, large 3665 vs 4399 / 3731 us, a 4-problem batch 1.80 vs 2.15 / 1.82 ms)
+#ifndef POT3D_SWS_MINB
+#define POT3D_SWS_MINB 1
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(SWT, 1) k_sweepS(SweepArgs A, int koff, int ntk4) {
+__global__ void __launch_bounds__(SWT, POT3D_SWS_MINB) k_sweepS(SweepArgs A, int koff, int ntk4) {
   if (A.nrhs <= 1 && A.predicated && A.S->stop) return;
   __shared__ int s_ticket;
   __shared__ double sred[SWT / 32];

@@ -32,15 +32,16 @@ static_assert(sizeof(SmemP) <= SMEM_P, "SMEM_P");
 __global__ void k_poly_init(PolyArgs A) {
   pdl_trigger();
   pdl_wait();
-  if (A.predicated && A.S->stop) return;
   const Grid &G = A.G;
   const Metrics &M = A.M;
+  const long long vo = (long long)blockIdx.y * (G.nr_loc + 2) * G.plane;  // a batch: problem blockIdx.y
+  if (A.predicated && A.S[blockIdx.y].stop) return;
   const long long per = (long long)G.nt * G.np, n = per * G.nr_loc;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
     const int il = (int)(c / per);
     const long long t = c - il * per;
     const int j = (int)(t / G.np), k = (int)(t - (long long)j * G.np);
-    const long long o = cidx(G, il, j, k);
+    const long long o = cidx(G, il, j, k) + vo;
     const DiagRow d = diag_row(plane_c(M, G.i0 + il), row_c(M, j));
     const double rv = jacobi(A.r[o], diag_at(__ldg(M.dp + k), d, __ldg(M.app + k), __ldg(M.apm + k)));
     const double dv = rv / A.theta;
@@ -57,7 +58,7 @@ template <bool LAST, bool FAST>
 __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs &A, int step, PassShared &sh) {
   const Grid &G = A.G;
   const Metrics &M = A.M;
-  Scalars *S = A.S;
+  Scalars *S = A.S + blockIdx.z;  // a batch: the problem of this block (pass_common.cuh)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemP &sm = *reinterpret_cast<SmemP *>(smem_raw);
   double *sred = sh.sred;
@@ -70,6 +71,8 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
   load_planes(pls, M, G.i0 + t.c0 - 1, L + 2);
   const int cs = 2 + 2 * t.lane;
   const long long PL = G.plane;
+  const int zp = rhs_planes(G);
+  const long long vo = zp * PL;
   const int src = (step - 1) & 1;  // d_{k-1} lives in d[(k-1) & 1]
   const void *map_d = &T.d_h[src];
   constexpr unsigned DB = TR * SROW * 8u, IB = TJ * TKB * 8u;
@@ -82,11 +85,11 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
       const int il = t.c0 - 1 + qi;
       const bool rown = (qi >= 1) && (qi <= L);
       mbar_arrive_expect_tx(&sm.bar[si], rown ? DB + (LAST ? 3 : 2) * IB : DB);
-      tma_load_3d(&sm.d[si][0][0], map_d, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, il + 1);
+      tma_load_3d(&sm.d[si][0][0], map_d, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, zp + il + 1);
       if (rown) {
-        tma_load_3d(&sm.res[si][0][0], &T.res_i, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
-        tma_load_3d(&sm.x[si][0][0], &T.x_i, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
-        if (LAST) tma_load_3d(&sm.r[si][0][0], &T.r_i, &sm.bar[si], t.k0 - 1 + COFF, t.j0, il + 1);
+        tma_load_3d(&sm.res[si][0][0], &T.res_i, &sm.bar[si], t.k0 - 1 + COFF, t.j0, zp + il + 1);
+        tma_load_3d(&sm.x[si][0][0], &T.x_i, &sm.bar[si], t.k0 - 1 + COFF, t.j0, zp + il + 1);
+        if (LAST) tma_load_3d(&sm.r[si][0][0], &T.r_i, &sm.bar[si], t.k0 - 1 + COFF, t.j0, zp + il + 1);
       }
     }
     ++qi;
@@ -108,9 +111,9 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
 #pragma unroll
   for (int e = 0; e < RPW; e++) dm[e] = dc[e] = dn[e] = Z2;
   double acc = 0.0;
-  double *g_d = A.d[src ^ 1] + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: plane c0
-  double *g_res = A.res + (long long)(t.c0 + 1) * PL;
-  double *g_x = (LAST ? A.z : A.x) + (long long)(t.c0 + 1) * PL;
+  double *g_d = A.d[src ^ 1] + vo + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: plane c0
+  double *g_res = A.res + vo + (long long)(t.c0 + 1) * PL;
+  double *g_x = (LAST ? A.z : A.x) + vo + (long long)(t.c0 + 1) * PL;
   int st = 0, so = NS_C - 1;
   unsigned ph = 0;
   auto st2 = [&](double *a, double2 v) {  // interior store (res, z_k: no ghost columns)
@@ -159,10 +162,10 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
         if (LAST) {
           const double2 rr = *reinterpret_cast<const double2 *>(&sm.r[so][r - 1][2 * t.lane]);
           acc += (m0 ? rr.x * xn.x : 0.0) + (m1 ? rr.y * xn.y : 0.0);
-          POT3D_CHK(S, in_range(g_x + o, A.z, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
+          POT3D_CHK(S, in_range(g_x + o, A.z + vo, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
           store_pair<FAST>(g_x + o, t, G.np, xn, true);  // z: pass A stages it (ghost columns)
         } else {
-          POT3D_CHK(S, in_range(g_d + o, A.d[src ^ 1], (G.nr_loc + 2) * PL), CHK_PASS_STORE);
+          POT3D_CHK(S, in_range(g_d + o, A.d[src ^ 1] + vo, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
           store_pair<FAST>(g_d + o, t, G.np, dnw, true);
           st2(g_res + o, resn);
           st2(g_x + o, xn);
@@ -183,7 +186,8 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
   }
   if (LAST) {
     double v[1] = {acc}, tot[1];
-    if (grid_sum<1>(v, A.partials, &S->counter[2], sred, tot, pass_bid(G), pass_nb(G)) && threadIdx.x == 0) {
+    if (grid_sum<1>(v, A.partials + blockIdx.z * A.pstride, &S->counter[2], sred, tot, pass_bid(G), pass_nb(G)) &&
+        threadIdx.x == 0) {
       if (A.finalize)
         finalize_rho(S, tot[0]);
       else

@@ -282,6 +282,7 @@ struct PolyArgs {
   double *partials, *local_sum;
   int finalize;          // LAST: 1 updates rho/beta, 0 writes local_sum
   int predicated;        // skip when the PCG loop has stopped
+  long long pstride;     // a batch (grid z / k_poly_init grid y = the problem): partials stride
 };
 
 // Arguments of the field kernels (a11).

@@ -156,6 +156,8 @@ CONFIGS = {
                          extra={"nrhs": 8}),
     "batchpc2": Config("batchpc2", 151, 301, 601, pc=2, note="SURVEY 8(f)-3 with PC2: 4 maps, interleaved sweeps",
                        extra={"nrhs": 4}),
+    "batchpc3": Config("batchpc3", 151, 301, 601, pc=3, note="SURVEY 8(f)-3 with PC3: 4 maps",
+                       extra={"nrhs": 4}),
 }
 
 

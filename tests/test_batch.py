@@ -150,8 +150,12 @@ def test_batch_medium_sampled_against_oracle():
     br = maps(tf, pf, [1, 2, 3, 4])
     with Pot3d(rf, tf, pf, br, nrhs=4) as s:
         res = s.solve(rtol=1e-9)
-    gold = json.loads((Path(__file__).parent / "golden" / "oracle_medium_pc1_b1.json").read_text())
-    assert res.status == 0 and abs(int(res.iters[0]) - gold["iters"]) <= 1, (res.iters, gold["iters"])
+    gdir = Path(__file__).parent / "golden"
+    gold = json.loads((gdir / "oracle_medium_pc1_b1.json").read_text())
+    # the oracle's iteration count and its evaluation-order spread (A24; 6567 / 6565)
+    its = [gold["iters"]] + [json.loads(q.read_text())["iters_variant"]
+                             for q in sorted(gdir.glob("oracle_medium_pc1_b1_spread_*.json"))]
+    assert res.status == 0 and min(its) - 1 <= int(res.iters[0]) <= max(its) + 1, (res.iters, its)
     got = res.phi[0].reshape(-1)[:: gold["stride"]]
     ref = np.asarray(gold["sample"])
     assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
@@ -187,8 +191,28 @@ def test_batch_pc2_equals_single_solves(blocks):
         assert np.linalg.norm(res.phi[q] - ref["x"]) <= 1e-9 * np.linalg.norm(ref["x"])
 
 
+@pytest.mark.gpu
+def test_batch_pc3_equals_single_solves():
+    """PC3 batches: the Chebyshev steps cover all problems per launch (grid z); each
+    problem equals its single PC3 solve bitwise and the oracle's PC3 solve."""
+    from paper_1709_01126_b200 import Pot3d
+
+    rf, tf, pf = synth.grid(30, 45, 90)
+    br = maps(tf, pf, [2, 3, 4], lmax=6)
+    with Pot3d(rf, tf, pf, br, pc=3, poly=(4, 100.0), nrhs=3) as s:
+        res = s.solve(rtol=1e-9)
+    assert res.status == 0
+    for q in range(3):
+        with Pot3d(rf, tf, pf, br[q], pc=3, poly=(4, 100.0)) as one:
+            r1 = one.solve(rtol=1e-9)
+        assert res.iters[q] == r1.iters and np.array_equal(res.phi[q], r1.phi), q
+        ref = oracle.solve(rf, tf, pf, br[q], pc=3, poly=(4, 100.0), rtol=1e-9)
+        assert abs(int(res.iters[q]) - ref["iters"]) <= 1, (q, res.iters[q], ref["iters"])
+        assert np.linalg.norm(res.phi[q] - ref["x"]) <= 1e-9 * np.linalg.norm(ref["x"])
+
+
 def test_batch_rejects_unsupported_combinations():
-    """nrhs > 1 is single-rank PC1 / PC2 standard PCG: other combinations are refused
+    """nrhs > 1 is single-rank standard PCG: other combinations are refused
     with POT3D_ERR_INVALID before any device work (runs without a GPU)."""
     from paper_1709_01126_b200 import pot3d as P
 
@@ -197,7 +221,7 @@ def test_batch_rejects_unsupported_combinations():
     br = np.zeros((2, 8, 6))
     dp = ctypes.POINTER(ctypes.c_double)
     g = P._Grid(4, 6, 8, rf.ctypes.data_as(dp), tf.ctypes.data_as(dp), pf.ctypes.data_as(dp))
-    for field, val, pc in (("variant", 1, 1), ("loopback_slabs", 2, 1), ("nranks", 2, 1), (None, 0, 3)):
+    for field, val, pc in (("variant", 1, 1), ("loopback_slabs", 2, 1), ("nranks", 2, 1), ("nranks", 2, 2)):
         rt = P._Runtime()
         rt.nranks, rt.nrhs, rt.device = 1, 2, -1
         if field:

@@ -391,7 +391,12 @@ def test_full_solve_matches_oracle_golden(gold):
         assert res.iters == fixed and res.status == 1
     else:
         assert res.status == 0 and g["status"] == 0
-        assert abs(res.iters - g["iters"]) <= 1, (res.iters, g["iters"])
+        # within 1 of the oracle's iteration count, or of its own evaluation-order spread
+        # where tools/oracle_spread.py recorded one (A24: medium PC1 stops at 6567 in the
+        # oracle's order and at 6565 with its dot products reversed)
+        its = [g["iters"]] + [json.loads(q.read_text())["iters_variant"]
+                              for q in sorted(GOLDEN.glob(f"{gold}_spread_*.json"))]
+        assert min(its) - 1 <= res.iters <= max(its) + 1, (res.iters, its)
     phi = np.asarray(res.phi).reshape(-1)
     ref = np.asarray(g["sample"])
     got = phi[:: g["stride"]]

@@ -9,6 +9,8 @@ VARIANTS = {
     "tj30": ["POT3D_TJ=30", "POT3D_MINB=1"],          # 512-thread tiles of 30 rows, 1 block/SM
     "tj22": ["POT3D_TJ=22", "POT3D_MINB=1"],          # 384 threads
     "tj30r4": ["POT3D_TJ=30", "POT3D_RPW=4", "POT3D_MINB=1"],  # 256 threads, 4 rows per lane
+    "sws1": ["POT3D_SWS_MINB=1"],                     # row-scan sweeps at one CTA per SM
+    "swj16m1": ["POT3D_SWJ=16", "POT3D_SWS_MINB=1"],
     "swj4": ["POT3D_SWJ=4"],
     "swj16": ["POT3D_SWJ=16"],
     "spd2": ["POT3D_SPD=2"],
