@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="large",
-                    choices=["tiny", "small", "medium", "large", "pc2", "pc3", "pc3large", "batch", "batchsmall", "batchpc2",
+                    choices=["tiny", "small", "medium", "large", "pc2", "pc3", "pc3large", "batch", "batchsmall", "batchpc2", "large8slab",
                              "batchpc3",
                              "weak"])
     ap.add_argument("--impl", default="own", choices=["own", "reference"])

@@ -40,10 +40,23 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
-    """Build libpot3d.so (or a tuning variant `out` with extra -D `defines`)."""
+    """Build libpot3d.so (or a tuning variant `out` with extra -D `defines`).  Processes
+    that build at once (the ranks of a torchrun job finding a stale library) take turns
+    on a file lock: the object files are shared, and the later ones find it fresh."""
+    import fcntl
+
     target = LIB if out is None else Path(out)
     if out is None and not force and not _stale():
         return LIB
+    (PKG / "build").mkdir(parents=True, exist_ok=True)
+    with open(PKG / "build" / ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if out is None and not force and not _stale():
+            return LIB
+        return _build_locked(target, verbose, defines, out)
+
+
+def _build_locked(target: Path, verbose: bool, defines, out) -> Path:
     nvcc = os.environ.get("NVCC", "nvcc")
     inc, libdir = nccl_dirs()
     objs = []

@@ -687,7 +687,8 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
     // at least 3 chunks, so an interior chunk runs while the halo travels (the two
     // chunks touching the ghost shells are scheduled last): 4 GPUs x 19 shells,
     // 84.9 us per iteration with 3 chunks vs 89.1 with the single-GPU choice of 1
-    if (ax.G.nchunks < 3 && G.nr_loc >= 6) ax.G.nchunks = 3;
+    static const int min_a = getenv("POT3D_MIN_CHUNKS_A") ? std::max(1, atoi(getenv("POT3D_MIN_CHUNKS_A"))) : 3;
+    if (ax.G.nchunks < min_a && G.nr_loc >= 2 * min_a) ax.G.nchunks = min_a;
     st.push_back([=]() -> int {
       CK(launch_pass(ctx->pdl, kern_a(ctx), dim3(0, ax.G.nchunks + 1), SMEM_A, ctx->stream, ctx->tmaps, ax,
                      parity));

@@ -150,6 +150,8 @@ CONFIGS = {
     "pc2": Config("pc2", 151, 301, 601, pc=2, note="BASELINE configs[3]: PC2 block ILU0"),
     "pc3": Config("pc3", 151, 301, 601, pc=3, note="SURVEY 8(f)-2: Chebyshev-accelerated Jacobi"),
     "pc3large": Config("pc3large", 301, 601, 1201, pc=3, note="SURVEY 8(f)-2 on the large grid"),
+    "large8slab": Config("large8slab", 152, 601, 1201,
+                         note="4 GPUs x 38 shells: the per-GPU slab of large on 8 GPUs (thin-slab tuning)"),
     "batch": Config("batch", 151, 301, 601, note="SURVEY 8(f)-3: 4 magnetograms (seeds 1-4) per solve",
                     extra={"nrhs": 4}),
     "batchsmall": Config("batchsmall", 42, 62, 122, note="SURVEY 8(f)-3 on a latency-bound grid: 8 maps",
