@@ -66,7 +66,7 @@ struct pot3d_ctx {
   double *poles = nullptr;
   Pc2 *pc2 = nullptr;
   TMaps tmaps{};
-  Cg1Maps cmaps{};          // CG1: U[0] = r, U[1] = P[1], p = P[0], s = s_cg
+  Cg1Maps cmaps{};          // CG1: U[0] = P[0], U[1] = P[1] (peer-mapped), p = r, s = s_cg
   double *s_cg = nullptr;
   // PC3 (poly.cu): Chebyshev steps, their coefficients and work vectors
   int poly_m = 4;
@@ -485,9 +485,9 @@ int make_maps(pot3d_ctx *ctx) {
     TRY(make_map(ctx, &ctx->pmaps.r_i, ctx->r, TKB, TJ));
   }
   if (ctx->variant == 1) {
-    TRY(make_map(ctx, &ctx->cmaps.u_h[0], ctx->r, SROW, TR));
+    TRY(make_map(ctx, &ctx->cmaps.u_h[0], ctx->P[0], SROW, TR));
     TRY(make_map(ctx, &ctx->cmaps.u_h[1], ctx->P[1], SROW, TR));
-    TRY(make_map(ctx, &ctx->cmaps.p_i, ctx->P[0], TKB, TJ));
+    TRY(make_map(ctx, &ctx->cmaps.p_i, ctx->r, TKB, TJ));
     TRY(make_map(ctx, &ctx->cmaps.s_i, ctx->s_cg, TKB, TJ));
     TRY(make_map(ctx, &ctx->cmaps.x_i, ctx->x, TKB, TJ));
   }
@@ -564,11 +564,13 @@ using Step = std::function<int()>;
 // ---------------------------------------------------------------------------
 // CG1 (single-reduction PCG, cg1.cu): per iteration K1 (vector update, u from
 // U[parity] into U[parity^1]), the halo of the new u, K2 (w = A u and the three
-// inner products), one reduction.  A loopback slab copies its edge shells into its
-// siblings' ghost shells and gathers their sums with device copies; a rank process
-// uses NCCL (send/recv, all-gather).
+// inner products), one reduction.  With peer memory (rank processes whose peers
+// are mapped, loopback slabs) K1 stores the halo into the neighbours' ghost shells
+// and K2 posts the sums to every mailbox (cg1.cu); otherwise NCCL send/recv and an
+// all-gather.  The u vectors live in P[0], P[1] (the peer-mapped buffers), p in r.
 // ---------------------------------------------------------------------------
-double *cg1_u(pot3d_ctx *c, int b) { return b ? c->P[1] : c->r; }
+double *cg1_u(pot3d_ctx *c, int b) { return c->P[b]; }
+bool cg1_peer(const pot3d_ctx *c) { return c->nranks > 1 && c->xfer && c->peers && !getenv("POT3D_CG1_NCCL"); }
 
 Cg1Args cg1_args(pot3d_ctx *ctx, int init) {
   Cg1Args a{};
@@ -577,7 +579,8 @@ Cg1Args cg1_args(pot3d_ctx *ctx, int init) {
   a.S = ctx->S;
   a.u[0] = cg1_u(ctx, 0);
   a.u[1] = cg1_u(ctx, 1);
-  a.p = ctx->P[0];
+  a.p = ctx->r;
+  a.peers = cg1_peer(ctx) ? ctx->peers : nullptr;
   a.s = ctx->s_cg;
   a.x = ctx->x;
   a.partials = ctx->partials;
@@ -605,7 +608,8 @@ std::vector<Step> cg1_steps(pot3d_ctx *ctx, int parity, bool init) {
       return 0;
     });
   }
-  if (ctx->nranks > 1) {  // the halo of the u the dots (and the next update) read
+  const bool peer = cg1_peer(ctx) && !init;  // the start's halo and sums go the copy way
+  if (ctx->nranks > 1 && !peer) {  // the halo of the u the dots (and the next update) read
     st.push_back([=]() -> int {
       if (!ctx->group) return halo_exchange(ctx, cg1_u(ctx, b));
       const std::vector<pot3d_ctx *> &M = *ctx->group;
@@ -628,7 +632,15 @@ std::vector<Step> cg1_steps(pot3d_ctx *ctx, int parity, bool init) {
     ctx->n_enq++;
     return 0;
   });
-  if (ctx->nranks > 1) {  // one reduction: every rank's (gamma, delta, ||r||^2) in rank order
+  if (peer) {  // one reduction through the mailboxes, summed in rank order
+    st.push_back([=]() -> int {
+      CK(launch_k(ctx->pdl, k_finalize_cg1_mail, dim3(1), dim3(1), 0, ctx->stream, ctx->S,
+                  (const PeerTab *)ctx->peers, ctx->hist));
+      MARK("cg1_finalize");
+      ctx->n_enq++;
+      return 0;
+    });
+  } else if (ctx->nranks > 1) {  // one reduction: every rank's (gamma, delta, ||r||^2) in rank order
     st.push_back([=]() -> int {
       if (!ctx->group) {
         NK(ncclAllGather(ctx->local_sum, ctx->gathered, 4, ncclDouble, ctx->comm, ctx->stream));
@@ -1150,6 +1162,8 @@ int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit) {
     CK(cudaGetLastError());
     ctx->n_launch++;
   }
+  // CG1 keeps u in P[0] / P[1] (the peer-mapped buffers) and p in r: u_0 = z_0
+  if (ctx->variant == 1) CK(cudaMemcpyAsync(ctx->P[0], ctx->r, cells * sizeof(double), cudaMemcpyDeviceToDevice, s));
   return 0;
 }
 
@@ -1415,7 +1429,10 @@ int pot3d_info(const pot3d_ctx *ctx, pot3d_info_t *info) {
   info->pc = ctx->pc;
   info->pc2_blocks_total = ctx->pc2_blocks * ctx->nranks;
   int64_t k = 2;
-  if (ctx->nranks > 1) k += (ctx->xfer && ctx->pc == 1) ? 2 : 3;
+  if (ctx->variant == 1)
+    k += ctx->nranks > 1 ? 1 : 0;  // CG1: update, dots (+ the finalisation across ranks)
+  else if (ctx->nranks > 1)
+    k += (ctx->xfer && ctx->pc == 1) ? 2 : 3;
   if (ctx->pc == 2 && ctx->pc2) k += pc2_kernels_per_apply(ctx->pc2) + (ctx->nranks > 1 ? 1 : 0);
   if (ctx->pc == 3) k += ctx->poly_m;
   info->graph_kernels_per_iter = k;
@@ -2044,7 +2061,7 @@ static int finish_solve(pot3d_ctx *ctx, std::vector<pot3d_ctx *> &M, double *phi
     // PC1 defers the x update of even iterations to the next (odd) pass B (A23): when the
     // last iteration K = iters - 1 was even, x += alpha_K p_K (p_K in P[1]) now
     if (m->pc == 1 && (hs.iter & 1)) {
-      k_x_finish<<<148 * 8, 256, 0, s>>>(m->G, m->S, m->x, m->variant == 1 ? m->P[0] : m->P[1]);
+      k_x_finish<<<148 * 8, 256, 0, s>>>(m->G, m->S, m->x, m->variant == 1 ? m->r : m->P[1]);
       CK(cudaGetLastError());
       m->n_launch++;
     }

@@ -18,6 +18,16 @@
 //       delta = sum w' u', ||r||^2 = sum (D u')^2 -> finalize (alpha, beta,
 //       convergence) in the last block.                                  [8 B/cell]
 // Per iteration 56 B/cell on average + 8 B/cell, one reduction (PCG: 56 B, two).
+//
+// Across ranks with peer memory (Cg1Args::peers): K1's blocks that own shell 0 or
+// nr_loc-1 also store those shells of u' into the neighbours' ghost shells (CUDA IPC /
+// loopback pointers, the p_lo / p_hi maps: U[b] is P[b]); the last of them raises the
+// neighbours' halo flags for this iteration.  K2's blocks whose chunk touches a ghost
+// shell wait for their flag before the TMA unit reads it, and the last block posts
+// (gamma, delta) and ||r||^2 into every rank's mailbox; k_finalize_cg1_mail sums them in
+// rank order.  Every wait is on a kernel of the previous phase on another GPU (no
+// co-residency assumption), and no rank can overwrite a ghost shell still being read:
+// its next K1 needs this iteration's alpha, which needs every rank's K2.
 #include "pass_common.cuh"
 
 namespace pot3d {
@@ -77,6 +87,25 @@ __device__ __forceinline__ void finalize_cg1(Scalars *S, double gamma, double de
   S->beta = beta;
   S->alpha = gamma / den;
   S->rho = gamma;
+}
+
+// sequence number of an iteration's CG1 exchange (the start's reduction: 0)
+__device__ __forceinline__ unsigned long long cg1_seq(const Scalars *S, int init) {
+  return mail_seq(S->epoch, init ? 0 : S->iter + 1);
+}
+
+__global__ void k_finalize_cg1_mail(Scalars *S, const PeerTab *peers, double *hist) {
+  pdl_trigger();
+  pdl_wait();
+  if (S->stop) return;
+  const unsigned long long seq = cg1_seq(S, 0);
+  double g, d, rr, unused;
+  if (!mail_collect(peers, MAIL_A, seq, S, g, d) || !mail_collect(peers, MAIL_B, seq, S, rr, unused)) {
+    S->status = -5;
+    S->stop = 1;
+    return;
+  }
+  finalize_cg1(S, g, d, rr, hist, false);
 }
 
 __global__ void k_finalize_cg1(Scalars *S, const double *gathered, int nranks, double *hist, int init) {
@@ -151,6 +180,13 @@ __device__ __forceinline__ void cg1_update_body(const Cg1Maps &T, const Cg1Args 
 #pragma unroll
   for (int e = 0; e < RPW; e++) um[e] = uc[e] = un[e] = Z2;
   double *g_u = A.u[parity ^ 1] + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: plane c0
+  // peer memory: u' of shell 0 / nr_loc-1 also lands in rank-1's top / rank+1's bottom
+  // ghost shell (the same [il+1][j][c] layout shifted by whole planes)
+  const PeerTab *pt = A.peers;
+  double *lo = pt ? pt->p_lo[parity ^ 1] : nullptr, *hi = pt ? pt->p_hi[parity ^ 1] : nullptr;
+  if (lo) lo += (long long)pt->nr_lo * PL;
+  if (hi) hi -= (long long)G.nr_loc * PL;
+  const bool edge_blk = pt && (t.c0 == 0 || t.c1 == G.nr_loc);
   double *g_p = A.p + (long long)(t.c0 + 1) * PL;
   double *g_s = A.s + (long long)(t.c0 + 1) * PL;
   double *g_x = A.x + (long long)(t.c0 + 1) * PL;
@@ -202,6 +238,16 @@ __device__ __forceinline__ void cg1_update_body(const Cg1Maps &T, const Cg1Args 
         POT3D_CHK(S, in_range(g_u + o, A.u[parity ^ 1], (G.nr_loc + 2) * PL) &&
                          in_range(g_p + o, A.p, (G.nr_loc + 2) * PL), CHK_CG1_STORE);
         store_pair<FAST>(g_u + o, t, G.np, unw, true);
+        if (edge_blk) {
+          const int il = t.c0 + q - 2;  // the shell of this store
+          double *rem = il == 0 ? lo : (il == G.nr_loc - 1 ? hi : nullptr);
+          // (lanes past the grid's last column store nothing: their row offset may leave the plane)
+          POT3D_CHK(S, !rem || !(FAST || t.st0 || t.st1) || (il == 0 ? in_range(rem + (g_u - A.u[parity ^ 1]) + o,
+                                                   pt->p_lo[parity ^ 1] + (long long)(pt->nr_lo + 1) * PL, PL)
+                                        : in_range(rem + (g_u - A.u[parity ^ 1]) + o, pt->p_hi[parity ^ 1], PL)),
+                    CHK_PEER_STORE);
+          if (rem) store_pair<FAST>(rem + (g_u - A.u[parity ^ 1]) + o, t, G.np, unw, false);
+        }
         st2(g_p + o, pn);
         st2(g_s + o, sn);
         if (XM == XM_PAIR) {
@@ -228,6 +274,17 @@ __device__ __forceinline__ void cg1_update_body(const Cg1Maps &T, const Cg1Args 
   }
   // end of the last block (the dots kernel's griddepcontrol.wait covers this grid's stores)
   if (threadIdx.x == 0) trace_max(S, TR_B1);
+  if (edge_blk) {  // every edge block's peer stores released, then the last raises the flags
+    const unsigned nedge = (unsigned)(gridDim.x * (G.nchunks > 1 ? 2 : 1));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      if (atomicAdd(&S->counter[4], 1u) == nedge - 1) {
+        S->counter[4] = 0u;
+        raise_halo_flags(pt, cg1_seq(S, 0));
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -255,8 +312,17 @@ __device__ __forceinline__ void cg1_dots_body(const Cg1Maps &T, const Cg1Args &A
 #pragma unroll
   for (int e = 0; e < RPW; e++) rw[e] = row_c(M, min(max(t.j0 - 1 + t.row[e], 0), G.nt - 1));
   int qi = 0, si = 0;
+  const PeerTab *pt = A.init ? nullptr : A.peers;  // the start's halo comes by copies
   auto issue = [&]() {
     if (qi <= L + 1) {
+      const int il = t.c0 - 1 + qi;
+      if (pt && (il < 0 || il >= G.nr_loc)) {  // a ghost shell: the neighbour's u' of this iteration
+        const int side = il < 0 ? 0 : 1;
+        if (side == 0 ? pt->rank > 0 : pt->rank < pt->nranks - 1) {
+          xfer_wait(&pt->mail[pt->rank]->halo[side], cg1_seq(S, 0), S);
+          fence_proxy_async_global();
+        }
+      }
       mbar_arrive_expect_tx(&sm.bar[si], UB);
       tma_load_3d(&sm.u[si][0][0], map_u, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, t.c0 + qi);
     }
@@ -325,6 +391,10 @@ __device__ __forceinline__ void cg1_dots_body(const Cg1Maps &T, const Cg1Args &A
     trace_mark(S, TR_A1);
     if (A.finalize) {
       finalize_cg1(S, tot[0], tot[1], tot[2], A.hist, A.init != 0);
+    } else if (pt) {
+      const unsigned long long seq = cg1_seq(S, 0);
+      mail_post(pt, MAIL_A, tot[0], tot[1], seq, S);
+      mail_post(pt, MAIL_B, tot[2], 0.0, seq, S);
     } else {
       A.local_sum[0] = tot[0];
       A.local_sum[1] = tot[1];

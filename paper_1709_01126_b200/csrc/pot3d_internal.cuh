@@ -264,6 +264,9 @@ struct Cg1Args {
   double *partials, *hist, *local_sum;
   int finalize;  // single rank: the last block of K2 updates the scalars
   int init;      // K2 of the start: gamma_0, delta_0 -> alpha_0
+  const PeerTab *peers;  // rank processes / loopback slabs with peer memory (cg1.cu): K1 stores
+                         // u's edge shells into the neighbours' ghost shells and raises their
+                         // halo flags, K2 waits for its own and posts its sums to every mailbox
 };
 
 // PC3 (poly.cu): TMA descriptors and arguments.  d ping-pongs between d[0], d[1].
@@ -356,6 +359,8 @@ __global__ void k_edge_p(Grid G, Metrics M, Scalars *S, const double *src, const
 // peer-memory finalisation: poll every rank's mailbox entry of `kind` for this
 // iteration, sum in rank order, update the scalars (what = 0 alpha, 1 beta, 2 rr, 3 rho)
 __global__ void k_finalize_mail(Scalars *S, const PeerTab *peers, int kind, int what, double *hist);
+// CG1 over peer memory: gamma, delta (MAIL_A) and ||r||^2 (MAIL_B) of every rank in rank order
+__global__ void k_finalize_cg1_mail(Scalars *S, const PeerTab *peers, double *hist);
 
 // pc2.cu -- PC2 (block ILU0 = D-ILU, A11) with tiled sync-free wavefront sweeps
 struct Pc2;

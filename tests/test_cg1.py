@@ -2,8 +2,10 @@
 PC1) against its own oracle (oracle/ orc_pcg variant CG1: Chronopoulos & Gear as
 stated by Ghysels & Vanroose 2014, Alg. 2, step by step): same seeded inputs,
 iteration count within 1, solution relative L2 <= 1e-9 (the north star's bar);
-fixed-iteration iterates element-wise; the loopback slab groups (one reduction
-per iteration through the slabs' gathered sums, halo of u by device copies)."""
+fixed-iteration iterates element-wise; the loopback slab groups run the peer-memory
+exchange of the rank processes (cg1.cu: K1 stores u's edge shells into the siblings'
+ghost shells and raises their halo flags, K2 waits for them and posts its three sums
+to every mailbox, k_finalize_cg1_mail sums them in rank order)."""
 import numpy as np
 import pytest
 
