@@ -1660,6 +1660,16 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   G.ntj = (nt + TJ - 1) / TJ;
   G.ntk = (np + 1 + TK - 1) / TK;  // tiles of columns 64t-1 .. 64t+62 cover -1 .. np-1
   {
+    // peer memory, PC1: pass A's first block row builds the edge shells only where a
+    // plane has fewer tiles than the resident pass blocks; on larger planes the separate
+    // edge-shell kernel is faster (large on 2 / 4 GPUs: 817.2 vs 805.0 / 1520.2 vs 1467.6
+    // iters/s; the 38-shell slab of 8 GPUs +4.8 %; medium on 4 GPUs: 7133 vs 7711,
+    // profiles/r02_edge_dispatch_n4.log) and needs no dispatch-order assumption (§8.2)
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    if (!getenv("POT3D_EDGE_IN_A") && (long long)G.ntj * G.ntk >= (long long)sms * PASS_MINB) ctx->edge_in_a = false;
+  }
+  {
     const void *fa[2] = {(const void *)k_pass_a, (const void *)k_pass_a_probe};
     const void *fb[3] = {(const void *)k_pass_b_pc1_even, (const void *)k_pass_b_pc1_odd,
                          (const void *)k_pass_b_pc2};

@@ -27,7 +27,11 @@
 // (gamma, delta) and ||r||^2 into every rank's mailbox; k_finalize_cg1_mail sums them in
 // rank order.  Every wait is on a kernel of the previous phase on another GPU (no
 // co-residency assumption), and no rank can overwrite a ghost shell still being read:
-// its next K1 needs this iteration's alpha, which needs every rank's K2.
+// its next K1 needs this iteration's alpha, which needs every rank's K2.  With one
+// reduction per iteration a fast rank can post iteration k+1 before a slow one has
+// read iteration k, so the mailbox slots alternate by iteration parity (MAIL_A/B on
+// even, MAIL_C/D on odd iterations): reaching k+2 needs every rank's k+1 posts, which
+// follow their reads of k.
 #include "pass_common.cuh"
 
 namespace pot3d {
@@ -99,8 +103,9 @@ __global__ void k_finalize_cg1_mail(Scalars *S, const PeerTab *peers, double *hi
   pdl_wait();
   if (S->stop) return;
   const unsigned long long seq = cg1_seq(S, 0);
+  const int k0 = (S->iter & 1) ? MAIL_C : MAIL_A;  // the slots of this iteration's parity
   double g, d, rr, unused;
-  if (!mail_collect(peers, MAIL_A, seq, S, g, d) || !mail_collect(peers, MAIL_B, seq, S, rr, unused)) {
+  if (!mail_collect(peers, k0, seq, S, g, d) || !mail_collect(peers, k0 + 1, seq, S, rr, unused)) {
     S->status = -5;
     S->stop = 1;
     return;
@@ -393,8 +398,9 @@ __device__ __forceinline__ void cg1_dots_body(const Cg1Maps &T, const Cg1Args &A
       finalize_cg1(S, tot[0], tot[1], tot[2], A.hist, A.init != 0);
     } else if (pt) {
       const unsigned long long seq = cg1_seq(S, 0);
-      mail_post(pt, MAIL_A, tot[0], tot[1], seq, S);
-      mail_post(pt, MAIL_B, tot[2], 0.0, seq, S);
+      const int k0 = (S->iter & 1) ? MAIL_C : MAIL_A;  // slots alternate by iteration parity
+      mail_post(pt, k0, tot[0], tot[1], seq, S);
+      mail_post(pt, k0 + 1, tot[2], 0.0, seq, S);
     } else {
       A.local_sum[0] = tot[0];
       A.local_sum[1] = tot[1];

@@ -145,11 +145,11 @@ struct MailEntry {          // one rank's contribution to a reduction
   unsigned long long seq;   // (epoch << 32) | iteration (1-based)
   unsigned long long pad;
 };
-enum MailKind { MAIL_A = 0, MAIL_B = 1, MAIL_C = 2 };
+enum MailKind { MAIL_A = 0, MAIL_B = 1, MAIL_C = 2, MAIL_D = 3 };  // CG1: (A, B) / (C, D) by iteration parity
 // slots of the per-iteration kernel timeline (Scalars::trace, [64][16] %globaltimer)
 enum TraceSlot { TR_EDGE0 = 0, TR_EDGE1, TR_A0, TR_AHALO, TR_A1, TR_F0, TR_F1, TR_B0, TR_B1, TR_EDGEM };
 struct Mailbox {
-  MailEntry e[3][MAXR];         // [kind][source rank]
+  MailEntry e[4][MAXR];         // [kind][source rank]
   unsigned long long halo[2];   // ghost shell filled: [0] from rank-1, [1] from rank+1
   unsigned long long pad[6];
 };
