@@ -604,14 +604,14 @@ static double dot(int64_t n, const double *x, const double *y) {
 int orc_pcg(int64_t N, orc_linop A, void *actx, orc_linop Minv, void *mctx, const double *b,
             double rtol, int64_t maxit, int variant, double *x, int64_t *iters,
             double *rel_res, double *hist) {
+  const int warm = (variant & ORC_PCG_X0) != 0;
+  variant &= ~ORC_PCG_X0;
   double *r = malloc(sizeof(double) * N);
   double *z = malloc(sizeof(double) * N);  /* z (standard) / u (CG1) */
   double *p = malloc(sizeof(double) * N);
   double *q = malloc(sizeof(double) * N);  /* q = A p (standard) / w = A u (CG1) */
   double *s = variant == ORC_PCG_CG1 ? malloc(sizeof(double) * N) : NULL;
   int status = 0, conv = 0;
-  const int warm = (variant & ORC_PCG_X0) != 0;
-  variant &= ~ORC_PCG_X0;
   if (warm) {                        /* r = b - A x0 */
     A(actx, x, r);
     for (int64_t m = 0; m < N; m++) r[m] = b[m] - r[m];

@@ -271,13 +271,16 @@ def test_pc3_symmetric_and_effective(oracle_lib):
 # ---------------------------------------------------------------------------
 # warm start (orc_pcg flag X0, SURVEY §8(f)-3 "repeated solves", A28)
 # ---------------------------------------------------------------------------
-def test_warm_start_from_zero_is_the_cold_loop(oracle_lib):
-    """x0 = 0 through the X0 path (r = b - A 0) gives the cold loop bitwise."""
+@pytest.mark.parametrize("variant", [0, 1])
+def test_warm_start_from_zero_is_the_cold_loop(oracle_lib, variant):
+    """x0 = 0 through the X0 path (r = b - A 0) gives the cold loop bitwise (standard
+    PCG and CG1)."""
     c = synth.CONFIGS["tiny"]
     rf, tf, pf = c.faces()
     br = synth.br0_map(tf, pf, 4, 3)
-    cold = oracle_lib.solve(rf, tf, pf, br, rtol=1e-9, history=True)
-    warm = oracle_lib.solve(rf, tf, pf, br, rtol=1e-9, history=True, x0=np.zeros_like(cold["x"]))
+    cold = oracle_lib.solve(rf, tf, pf, br, rtol=1e-9, history=True, variant=variant)
+    warm = oracle_lib.solve(rf, tf, pf, br, rtol=1e-9, history=True, x0=np.zeros_like(cold["x"]),
+                            variant=variant)
     assert warm["iters"] == cold["iters"] and np.array_equal(warm["x"], cold["x"])
     assert np.array_equal(warm["hist"], cold["hist"])
 
