@@ -176,9 +176,10 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
  * already meets it; hist[0] = ||r_0|| / ||b||).  x0: the layout of phi (a batch: nrhs
  * items), host or device, copied in; NULL = start from the context's last solution
  * (kept across pot3d_set_br0 and pot3d_field -- the time-series use: a new map, the
- * previous Phi; POT3D_ERR_STATE if a diagnostic call has run since).  One rank, no
- * loopback slabs (POT3D_ERR_INVALID otherwise); b = 0 still returns Phi = 0.
- * Outputs and status as pot3d_solve. */
+ * previous Phi; POT3D_ERR_STATE if a diagnostic call has run since).  Across ranks
+ * (collective) x0 is this rank's slab and the start takes two reductions (||b||,
+ * then r_0's sums) and the halo of x0; a loopback group takes the whole grid.  b = 0
+ * still returns Phi = 0.  Outputs and status as pot3d_solve. */
 int pot3d_solve_from(pot3d_ctx *ctx, const double *x0, double rtol, int64_t maxit, double *phi,
                      int64_t *iters, double *rel_residual, double *true_rel_residual);
 

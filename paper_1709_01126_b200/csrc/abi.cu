@@ -1098,49 +1098,60 @@ int build_graph_group(pot3d_ctx *h);
 
 // x0 = 0, r = b, p = 0 (A9), the device scalars, PC2: z0 = M^-1 b, local init sums.
 // Warm start (ctx->warm, pot3d_solve_from): x holds x0 (interior cells), r = b - A x0.
-int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit) {
+// phase 0: all of it; a warm start across ranks / slabs runs phase 1 (up to the local
+// sums of ||b||), then -- after the global ||b|| and x0's halo (solve_run) -- phase 2.
+int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit, int phase = 0) {
   const Grid &G = ctx->G;
   cudaStream_t s = ctx->stream;
   const size_t cells = (size_t)(G.nr_loc + 2) * G.plane;
   const bool warm = ctx->warm;
-  if (!warm) {
-    CK(cudaMemsetAsync(ctx->x, 0, cells * sizeof(double), s));
-  } else {  // the ghost shells of x0 are zero for the apply (the BCs are folded, A7)
-    CK(cudaMemsetAsync(ctx->x + sidx(G, -1), 0, G.plane * sizeof(double), s));
-    CK(cudaMemsetAsync(ctx->x + sidx(G, G.nr_loc), 0, G.plane * sizeof(double), s));
-  }
-  CK(cudaMemsetAsync(ctx->r, 0, cells * sizeof(double), s));
-  CK(cudaMemsetAsync(ctx->P[0], 0, cells * sizeof(double), s));
-  CK(cudaMemsetAsync(ctx->P[1], 0, cells * sizeof(double), s));
-  if (ctx->s_cg) CK(cudaMemsetAsync(ctx->s_cg, 0, cells * sizeof(double), s));
-  if (G.i0 == 0) {
-    CK(cudaMemcpyAsync(ctx->r + sidx(G, 0), ctx->bshell, G.plane * sizeof(double),
-                       cudaMemcpyDeviceToDevice, s));
-    k_fix_ghost_cols<<<(ctx->nt + 255) / 256, 256, 0, s>>>(G, ctx->r, 0, 1);
-    CK(cudaGetLastError());
-    ctx->n_launch++;
-  }
-  Scalars h0{};
-  h0.epoch = ++ctx->epoch;
-  if ((ctx->trace_on || getenv("POT3D_TRACE")) && !ctx->trace) {
-    TRY(dalloc(ctx, &ctx->trace, 64 * 16));
-  }
-  if (ctx->trace) CK(cudaMemsetAsync(ctx->trace, 0, 64 * 16 * sizeof(unsigned long long), s));
-  h0.trace = ctx->trace;
-  h0.rtol = rtol;
-  h0.maxit = (long long)maxit;  // the history keeps the first hist_len entries
-  h0.hist_len = ctx->hist_len;
-  CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+  if (phase != 2) {  // phase 2 starts at the residual of x0
+    if (!warm) {
+      CK(cudaMemsetAsync(ctx->x, 0, cells * sizeof(double), s));
+    } else {  // the ghost shells of x0 are zero for the apply (the BCs are folded, A7)
+      CK(cudaMemsetAsync(ctx->x + sidx(G, -1), 0, G.plane * sizeof(double), s));
+      CK(cudaMemsetAsync(ctx->x + sidx(G, G.nr_loc), 0, G.plane * sizeof(double), s));
+    }
+    CK(cudaMemsetAsync(ctx->r, 0, cells * sizeof(double), s));
+    CK(cudaMemsetAsync(ctx->P[0], 0, cells * sizeof(double), s));
+    CK(cudaMemsetAsync(ctx->P[1], 0, cells * sizeof(double), s));
+    if (ctx->s_cg) CK(cudaMemsetAsync(ctx->s_cg, 0, cells * sizeof(double), s));
+    if (G.i0 == 0) {
+      CK(cudaMemcpyAsync(ctx->r + sidx(G, 0), ctx->bshell, G.plane * sizeof(double),
+                         cudaMemcpyDeviceToDevice, s));
+      k_fix_ghost_cols<<<(ctx->nt + 255) / 256, 256, 0, s>>>(G, ctx->r, 0, 1);
+      CK(cudaGetLastError());
+      ctx->n_launch++;
+    }
+    Scalars h0{};
+    h0.epoch = ++ctx->epoch;
+    if ((ctx->trace_on || getenv("POT3D_TRACE")) && !ctx->trace) {
+      TRY(dalloc(ctx, &ctx->trace, 64 * 16));
+    }
+    if (ctx->trace) CK(cudaMemsetAsync(ctx->trace, 0, 64 * 16 * sizeof(unsigned long long), s));
+    h0.trace = ctx->trace;
+    h0.rtol = rtol;
+    h0.maxit = (long long)maxit;  // the history keeps the first hist_len entries
+    h0.hist_len = ctx->hist_len;
+    CK(cudaMemcpyAsync(ctx->S, &h0, sizeof(Scalars), cudaMemcpyHostToDevice, s));
+    if (warm) {
+      // ||b|| from r = b (the stopping test stays relative to b, A9); across ranks only
+      // this rank's sums here (phase 1)
+      k_init_dots<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, ctx->partials, phase == 1 ? 0 : 1,
+                                          ctx->local_sum, 0, nullptr, 0, nullptr);
+      CK(cudaGetLastError());
+      ctx->n_launch++;
+      if (phase == 1) return 0;
+    }
+  }  // phase != 2
   if (warm) {
-    // ||b|| from r = b (the stopping test stays relative to b, A9), then r = b - A x0
-    // over every cell and its periodic ghost columns (a stencil operand of pass A)
-    k_init_dots<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, ctx->partials, 1, ctx->local_sum, 0,
-                                        nullptr, 0, nullptr);
+    // r = b - A x0 over every cell and its periodic ghost columns (a stencil operand
+    // of pass A); x0's ghost shells hold the neighbours' edge shells (halo) or zero
     k_apply<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->x, ctx->r, ctx->bshell, G.i0 == 0 ? 0 : -1000, nullptr,
                                     nullptr, nullptr);
     k_fix_ghost_cols<<<(G.nr_loc * ctx->nt + 255) / 256, 256, 0, s>>>(G, ctx->r, 0, G.nr_loc);
     CK(cudaGetLastError());
-    ctx->n_launch += 3;
+    ctx->n_launch += 2;
   }
   // z0 = M^-1 r0, rho0 = r0.z0, ||b|| (a10 init)
   if (ctx->pc == 2) {
@@ -1171,7 +1182,8 @@ int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit) {
 int solve_init_end(pot3d_ctx *ctx) {
   cudaStream_t s = ctx->stream;
   if (ctx->nranks > 1) {
-    k_init_finalize<<<1, 1, 0, s>>>(ctx->S, ctx->gathered, ctx->nranks);
+    k_init_finalize<<<1, 1, 0, s>>>(ctx->S, ctx->gathered, ctx->nranks, ctx->warm ? 1 : 0,
+                                    ctx->warm ? ctx->hist : nullptr);
     CK(cudaGetLastError());
     ctx->n_launch++;
   }
@@ -1267,7 +1279,20 @@ int solve_run(pot3d_ctx *h, std::vector<pot3d_ctx *> &M, double rtol, int64_t ma
   else
     for (pot3d_ctx *m : M) TRY(ensure_hist(m, maxit, stale));
   if (stale) TRY(M.size() > 1 && !batch ? build_graph_group(h) : build_graph(h));  // graph captured the old hist
-  for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit));
+  if (!batch && M[0]->warm && (M.size() > 1 || M[0]->nranks > 1)) {
+    // a warm start across ranks / slabs: the global ||b|| first, then x0's halo and r_0
+    for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit, 1));
+    TRY(gather_all(M));
+    for (pot3d_ctx *m : M) {
+      k_init_finalize<<<1, 1, 0, m->stream>>>(m->S, m->gathered, m->nranks, 0, nullptr);
+      CK(cudaGetLastError());
+      m->n_launch++;
+    }
+    TRY(halo_all(M, [](pot3d_ctx *m) { return m->x; }));
+    for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit, 2));
+  } else {
+    for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit));
+  }
   if (!batch && (M.size() > 1 || M[0]->nranks > 1)) TRY(gather_all(M));
   for (pot3d_ctx *m : M) TRY(solve_init_end(m));
   if (M[0]->variant == 1) {  // CG1: w_0 = A u_0, delta_0 -> alpha_0 (the same steps, phase by phase)
@@ -2174,30 +2199,30 @@ int pot3d_solve(pot3d_ctx *ctx, double rtol, int64_t maxit, double *phi, int64_t
 int pot3d_solve_from(pot3d_ctx *ctx, const double *x0, double rtol, int64_t maxit, double *phi, int64_t *iters,
                      double *rel_residual, double *true_rel_residual) {
   if (!ctx) return POT3D_ERR_INVALID;
-  if (ctx->nranks > 1 || !ctx->slabs.empty()) {
-    ctx->err = "pot3d_solve_from runs on one rank (no loopback slabs)";
-    return POT3D_ERR_INVALID;
-  }
   if (!(rtol >= 0.0) || maxit < 1) {
     ctx->err = "rtol must be >= 0 and maxit >= 1";
     return POT3D_ERR_INVALID;
   }
   CK(cudaSetDevice(ctx->device));
-  std::vector<pot3d_ctx *> M = ctx->rhs.empty() ? std::vector<pot3d_ctx *>{ctx} : ctx->rhs;
-  const size_t ncell = (size_t)ctx->nr * ctx->nt * ctx->np;
-  for (size_t q = 0; q < M.size(); q++) {
-    pot3d_ctx *m = M[q];
-    if (x0) {
-      std::vector<pot3d_ctx *> one{m};
-      int rc = cells_in(m, one, x0 + q * ncell, [](pot3d_ctx *c) { return c->x + c->G.plane; });
-      if (rc) {
-        ctx->err = m->err;
-        return rc;
-      }
-    } else if (!m->has_x) {
+  // a batch: one x0 per problem; a loopback group: x0 is the whole grid; a rank: its slab
+  std::vector<pot3d_ctx *> M = ctx->rhs.empty() ? members(ctx) : ctx->rhs;
+  for (pot3d_ctx *m : M)
+    if (!x0 && !m->has_x) {
       ctx->err = "pot3d_solve_from(x0 = NULL): no solution in the context (a diagnostic call since the last solve)";
       return POT3D_ERR_STATE;
     }
+  if (x0 && !ctx->rhs.empty()) {
+    const size_t ncell = (size_t)ctx->nr * ctx->nt * ctx->np;
+    for (size_t q = 0; q < M.size(); q++) {
+      std::vector<pot3d_ctx *> one{M[q]};
+      int rc = cells_in(M[q], one, x0 + q * ncell, [](pot3d_ctx *c) { return c->x + c->G.plane; });
+      if (rc) {
+        ctx->err = M[q]->err;
+        return rc;
+      }
+    }
+  } else if (x0) {
+    TRY(cells_in(ctx, M, x0, [](pot3d_ctx *c) { return c->x + c->G.plane; }));
   }
   for (pot3d_ctx *m : M) m->warm = true;
   int rc = pot3d_solve(ctx, rtol, maxit, phi, iters, rel_residual, true_rel_residual);

@@ -333,21 +333,29 @@ __global__ void k_init_dots(Grid G, Metrics M, Scalars *S, const double *r, doub
   }
 }
 
-__global__ void k_init_finalize(Scalars *S, const double *gathered, int nranks) {
+// keep_b (a warm start across ranks): the sums are r_0's, ||b|| is already in S (as
+// k_init_dots' keep_b: the stopping test against ||b||, hist0[0] = ||r_0|| / ||b||)
+__global__ void k_init_finalize(Scalars *S, const double *gathered, int nranks, int keep_b, double *hist0) {
   double rz = 0.0, bb = 0.0;
   for (int r = 0; r < nranks; r++) {
     rz += gathered[r * 2 + 0];
     bb += gathered[r * 2 + 1];
   }
   S->rho = rz;
-  S->bnorm = sqrt(bb);
+  if (!keep_b) S->bnorm = sqrt(bb);
   S->rr = bb;
   S->iter = 0;
   S->beta = 0.0;
   S->alpha = 0.0;
   S->alpha_prev = 0.0;
   S->status = 0;
-  S->stop = (bb == 0.0) ? 1 : 0;
+  if (keep_b) {
+    const double bn = S->bnorm, rn = sqrt(bb);
+    S->stop = (bn == 0.0 || rn <= S->rtol * bn) ? 1 : 0;
+    if (hist0) hist0[0] = bn > 0.0 ? rn / bn : 0.0;
+  } else {
+    S->stop = (bb == 0.0) ? 1 : 0;
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -335,7 +335,7 @@ __global__ void k_finalize_rho(Scalars *S, const double *gathered, int nranks);
 __global__ void k_init_dots(Grid G, Metrics M, Scalars *S, const double *r, double *partials,
                             int finalize, double *local_sum, int use_z, const double *z, int keep_b,
                             double *hist0);
-__global__ void k_init_finalize(Scalars *S, const double *gathered, int nranks);
+__global__ void k_init_finalize(Scalars *S, const double *gathered, int nranks, int keep_b, double *hist0);
 __global__ void k_apply(Grid G, Metrics M, const double *x, double *y, const double *bshell,
                         int b_il, Scalars *S, double *partials, double *local_sum);
 __global__ void k_br_mean(Grid G, Metrics M, const double *br, double *out2);

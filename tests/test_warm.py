@@ -100,3 +100,22 @@ def test_warm_batch_per_problem_x0():
             r1 = one.solve(rtol=1e-9, x0=x0[q])
         assert res.iters[q] == r1.iters and np.array_equal(res.phi[q], r1.phi), q
     assert res.iters[1] < res.iters[0]
+
+
+@pytest.mark.parametrize("k,variant", [(2, 0), (3, 0), (2, 1)])
+def test_warm_loopback_slabs(k, variant):
+    """Warm starts across r-slabs (loopback groups run the ranks' exchange on one GPU):
+    x0 = 0 is the cold solve bitwise; from the previous Phi the oracle's warm start."""
+    c = synth.CONFIGS["small"]
+    rf, tf, pf = c.faces()
+    a = c.br0()
+    b = a + 0.02 * synth.br0_map(tf, pf, 4, 9)
+    with ctx(rf, tf, pf, a, loopback_slabs=k, variant=variant) as s:
+        cold = s.solve(rtol=1e-9)
+        zero = s.solve(rtol=1e-9, x0=np.zeros_like(cold.phi))
+        s.set_br0(b)
+        warm = s.solve(rtol=1e-9, warm=True)
+    assert zero.iters == cold.iters and np.array_equal(zero.phi, cold.phi)
+    ow = oracle.solve(rf, tf, pf, b, rtol=1e-9, variant=variant, x0=cold.phi)
+    assert warm.status == 0 and abs(warm.iters - ow["iters"]) <= 1, (warm.iters, ow["iters"])
+    assert np.linalg.norm(warm.phi - ow["x"]) <= 1e-9 * np.linalg.norm(ow["x"])

@@ -58,6 +58,33 @@ for name, pc, blocks, bc, variant in cases:
               f"{res.true_rel_residual:.2e} exchange {exch} repeat {'same' if same else 'DIFF'} "
               f"{'OK' if ok else 'FAIL'} ({time.time() - t0:.1f}s)",
               flush=True)
+# warm starts across ranks (pot3d_solve_from): x0 = 0 reproduces the cold
+# solve bitwise; a perturbed map from the previous Phi matches the oracle's warm start
+for name, variant in (("small", 0), ("small", 1), ("thin", 0)):
+    c = synth.Config("thin", 2 * world, 17, 33, lmax=4) if name == "thin" else synth.CONFIGS[name]
+    rf, tf, pf = c.faces()
+    a = c.br0()
+    b = a + 0.02 * synth.br0_map(tf, pf, 4, 9)
+    t0 = time.time()
+    with Pot3d(rf, tf, pf, a, rank=rank, nranks=world, variant=variant) as s:
+        cold = s.solve(rtol=1e-9)
+        zero = s.solve(rtol=1e-9, x0=np.zeros_like(cold.phi))
+        same = zero.iters == cold.iters and np.array_equal(zero.phi, cold.phi)
+        pa = gather_slabs(torch.from_numpy(cold.phi).cuda(), c.nr)
+        s.set_br0(b)
+        warm = s.solve(rtol=1e-9, warm=True)
+        pw = gather_slabs(torch.from_numpy(warm.phi).cuda(), c.nr)
+    if rank == 0:
+        import oracle
+
+        ow = oracle.solve(rf, tf, pf, b, rtol=1e-9, variant=variant, x0=pa.cpu().numpy())
+        oc = oracle.solve(rf, tf, pf, b, rtol=1e-9, variant=variant)
+        rel = np.linalg.norm(pw.cpu().numpy() - ow["x"]) / np.linalg.norm(ow["x"])
+        ok = same and abs(warm.iters - ow["iters"]) <= 1 and rel <= 1e-9 and warm.iters < oc["iters"]
+        fails += 0 if ok else 1
+        print(f"[{world} ranks] warm {name}{' cg1' if variant else ''}: x0=0 {'same' if same else 'DIFF'}, "
+              f"from the previous Phi {warm.iters} iterations (oracle warm {ow['iters']}, cold {oc['iters']}) "
+              f"rel {rel:.2e} {'OK' if ok else 'FAIL'} ({time.time() - t0:.1f}s)", flush=True)
 dist.barrier()
 dist.destroy_process_group()
 sys.exit(1 if fails else 0)
