@@ -256,6 +256,8 @@ def main():
     c = make_config(args, world)
     rf, tf, pf = c.faces()
     kb = c.extra.get("nrhs", 1)  # a multi-RHS batch: k problems per solve
+    if kb > 1 and world > 1:
+        raise SystemExit(f"--config {args.config}: batches run on one GPU (pot3d_runtime.nrhs, DESIGN.md §7.8)")
     br_np = synth.batch_maps(c, (rf, tf, pf)) if kb > 1 else c.br0((rf, tf, pf))
     s = Pot3d(rf, tf, pf, br_np, bc=c.bc, pc=c.pc, rank=rank, nranks=world,
               pc2_blocks=args.pc2_blocks, unroll=32, variant=args.variant, nrhs=kb)  # fresh NCCL id inside
