@@ -2,8 +2,10 @@
 process per GPU (torchrun), every case against the CPU oracle on the global grid.
 
 Runs tools/mgpu_check.py: PC1 source surface / closed wall, PC2 with 1 and 2
-ILU blocks per rank; iterations within 1 of the oracle's, rel L2 <= 1e-9, B
-within 1e-7, a repeated solve in the same context bitwise identical.  With two
+ILU blocks per rank, CG1; iterations within 1 of the oracle's, rel L2 <= 1e-9, B
+within 1e-7, a repeated solve in the same context bitwise identical; warm starts
+(x0 = 0 bitwise the cold solve, a perturbed map from the previous Phi against the
+oracle's warm start).  With two
 or more GPUs the peer-memory exchange (CUDA IPC over NVLink) is in use
 (exchange == 2 in pot3d_info); the NCCL fallback is run as well.
 Skipped on boxes with fewer than two GPUs.
@@ -44,4 +46,8 @@ def test_two_gpu_parity(xfer):
     lines = [ln for ln in out.splitlines() if ln.startswith("[2 ranks]")]
     assert rc == 0 and lines and all(ln.endswith(")") and " OK " in ln for ln in lines), out[-4000:]
     want = "exchange 2" if xfer == "1" else "exchange 1"
-    assert all(want in ln for ln in lines), out[-4000:]
+    solves = [ln for ln in lines if " warm " not in ln]
+    assert all(want in ln for ln in solves), out[-4000:]
+    # warm starts across the ranks (pot3d_solve_from): PCG and CG1, x0 = 0 bitwise the cold solve
+    warm = [ln for ln in lines if " warm " in ln]
+    assert len(warm) == 3 and all("x0=0 same" in ln for ln in warm), out[-4000:]
