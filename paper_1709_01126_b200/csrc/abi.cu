@@ -660,6 +660,9 @@ std::vector<Step> cg1_steps(pot3d_ctx *ctx, int parity, bool init) {
   return st;
 }
 
+std::vector<Step> poly_steps(pot3d_ctx *ctx, int finalize, bool iteration, int nz = 1,
+                             const PeerTab *peers = nullptr);
+
 std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
   if (ctx->variant == 1) return cg1_steps(ctx, parity, false);
   std::vector<Step> st;
@@ -670,6 +673,7 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
   ab.G.nchunks = ctx->nchunks_b;
   const dim3 grd(G.ntj * G.ntk, G.nchunks), grdb(G.ntj * G.ntk, ctx->nchunks_b);
   const bool pc2 = ctx->pc == 2;
+  const bool zs = ctx->pc >= 2;  // PC2 / PC3: z stored apart from r
   const PeerTab *pt = ctx->peers;
   auto fin = [ctx, pt](int kind, int what, double *hist, const char *nm) -> Step {
     return [=]() -> int {
@@ -687,7 +691,7 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
       return 0;
     };
   };
-  if (ctx->edge_in_a && !pc2) {
+  if (ctx->edge_in_a && !zs) {
     // pass A's first block row builds and sends the edge shells beside the interior
     // chunks; beta is finalised by its own kernel after pass B.  The halo waits of
     // the chunks next to a ghost shell (scheduled last in the grid) assume the
@@ -714,10 +718,10 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
     return st;
   }
   // PC1: the previous iteration's beta finalisation lives in edge_p (fold)
-  const int fold = pc2 ? 0 : 1;
+  const int fold = zs ? 0 : 1;
   st.push_back([=]() -> int {
     CK(launch_k(ctx->pdl, k_edge_p, dim3(ctx->edge_blocks), dim3(256), 0, ctx->stream, G, ctx->M, ctx->S,
-                (const double *)(pc2 ? ctx->z : ctx->r), (const double *)ctx->P[parity], ctx->P[parity ^ 1], 1,
+                (const double *)(zs ? ctx->z : ctx->r), (const double *)ctx->P[parity], ctx->P[parity ^ 1], 1,
                 pt, parity ^ 1, ctx->hist, fold));
     MARK("edge_p");
     ctx->n_enq++;
@@ -750,12 +754,40 @@ std::vector<Step> iteration_steps(pot3d_ctx *ctx, int parity) {
     });
     st.push_back(fin(MAIL_C, 3, nullptr, "finalize_rho"));
   }
+  if (ctx->pc == 3) {  // the Chebyshev steps (halo of d between them), r.z to every mailbox
+    st.push_back(fin(MAIL_B, 2, ctx->hist, "finalize_rr"));
+    for (Step &f : poly_steps(ctx, 0, true, 1, pt)) st.push_back(f);
+    st.push_back(fin(MAIL_C, 3, nullptr, "finalize_rho"));
+  }
   return st;
 }
 
-// PC3: z = M^-1 r (ctx->r -> ctx->z), the partial r.z to rho/beta (finalize) or local_sum.
+// halo of a cell array between r-slabs: NCCL send/recv (rank processes) or device copies
+// into the siblings' ghost shells (loopback slabs, which run it phase by phase)
+int halo_slab(pot3d_ctx *ctx, double *(*arr)(pot3d_ctx *)) {
+  if (!ctx->group) return halo_exchange(ctx, arr(ctx));
+  const std::vector<pot3d_ctx *> &M = *ctx->group;
+  const Grid &G = ctx->G;
+  const int q = ctx->rank;
+  const size_t bytes = (size_t)G.plane * sizeof(double);
+  if (q > 0)
+    CK(cudaMemcpyAsync(arr(M[q - 1]) + sidx(M[q - 1]->G, M[q - 1]->G.nr_loc), arr(ctx) + sidx(G, 0), bytes,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+  if (q + 1 < (int)M.size())
+    CK(cudaMemcpyAsync(arr(M[q + 1]) + sidx(M[q + 1]->G, -1), arr(ctx) + sidx(G, G.nr_loc - 1), bytes,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+  return 0;
+}
+
+// PC3: z = M^-1 r (ctx->r -> ctx->z), the partial r.z to rho/beta (finalize), every
+// mailbox (peers) or local_sum, as launch steps.  Across ranks the Chebyshev step k
+// reads d_{k-1} with the neighbours' edge shells: a halo step precedes it.
 // nz: problems covered (a batch leader's loop and profile: nrhs; the start of a solve: 1)
-int poly_apply(pot3d_ctx *ctx, int finalize, bool iteration, int nz = 1) {
+double *poly_d0(pot3d_ctx *c) { return c->p_d[0]; }
+double *poly_d1(pot3d_ctx *c) { return c->p_d[1]; }
+
+std::vector<Step> poly_steps(pot3d_ctx *ctx, int finalize, bool iteration, int nz, const PeerTab *peers) {
+  std::vector<Step> st;
   const Grid &G = ctx->G;
   PolyArgs a{};
   a.G = G;
@@ -777,18 +809,40 @@ int poly_apply(pot3d_ctx *ctx, int finalize, bool iteration, int nz = 1) {
   a.local_sum = ctx->local_sum;
   a.finalize = finalize;
   a.predicated = iteration ? 1 : 0;
-  const bool pdl = ctx->pdl && iteration;
-  CK(launch_k(pdl, k_poly_init, dim3(148 * 8, nz), dim3(256), 0, ctx->stream, a));
-  a.G.nchunks = ctx->nchunks_b;
+  a.peers = peers;
+  const bool pdl = ctx->pdl && iteration && ctx->nranks == 1;
+  auto count = [ctx, iteration]() {
+    if (iteration)
+      ctx->n_enq++;
+    else
+      ctx->n_launch++;
+  };
+  st.push_back([=]() -> int {
+    CK(launch_k(pdl, k_poly_init, dim3(148 * 8, nz), dim3(256), 0, ctx->stream, a));
+    count();
+    return 0;
+  });
+  PolyArgs ak = a;
+  ak.G.nchunks = ctx->nchunks_b;
   const dim3 grd(G.ntj * G.ntk, ctx->nchunks_b, nz);
-  for (int k = 1; k < ctx->poly_m; k++)
-    CK(launch_k(pdl, k + 1 == ctx->poly_m ? k_poly_last : k_poly_step, grd, dim3(NTHREADS), SMEM_P, ctx->stream,
-                ctx->pmaps, a, k));
-  if (iteration)
-    ctx->n_enq += ctx->poly_m;
-  else
-    ctx->n_launch += ctx->poly_m;
-  MARK("pc3");
+  for (int k = 1; k < ctx->poly_m; k++) {
+    if (ctx->nranks > 1) {
+      const int src = (k - 1) & 1;  // d_{k-1}
+      st.push_back([=]() -> int { return halo_slab(ctx, src ? poly_d1 : poly_d0); });
+    }
+    st.push_back([=]() -> int {
+      CK(launch_k(pdl, k + 1 == ctx->poly_m ? k_poly_last : k_poly_step, grd, dim3(NTHREADS), SMEM_P, ctx->stream,
+                  ctx->pmaps, ak, k));
+      count();
+      if (k + 1 == ctx->poly_m) MARK("pc3");
+      return 0;
+    });
+  }
+  return st;
+}
+
+int poly_apply(pot3d_ctx *ctx, int finalize, bool iteration, int nz = 1, const PeerTab *peers = nullptr) {
+  for (auto &f : poly_steps(ctx, finalize, iteration, nz, peers)) TRY(f());
   return 0;
 }
 
@@ -804,6 +858,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   ab.G.nchunks = ctx->nchunks_b;
   dim3 grdb(G.ntj * G.ntk, ctx->nchunks_b, ctx->nrhs);
   const bool pc2 = ctx->pc == 2;
+  const bool zs = ctx->pc >= 2;  // PC2 / PC3: z stored apart from r
   const bool multi = ctx->nranks > 1;
   if (ctx->xfer) {
     // peer memory: edge shells of p_k stored into the neighbours' ghost shells
@@ -816,7 +871,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   if (multi && G.nr_loc >= 3) {
     // edge shells first; their halo travels on the comm stream while pass A
     // covers the interior shells, then pass A finishes the two edge shells
-    k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
+    k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, zs ? ctx->z : ctx->r,
                                                 ctx->P[parity], ctx->P[parity ^ 1], 1,
                                                 nullptr, 0, nullptr, 0);
     CK(cudaGetLastError());
@@ -846,7 +901,7 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
     MARK("passA_edge");
   } else {
     if (multi) {
-      k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, pc2 ? ctx->z : ctx->r,
+      k_edge_p<<<148 * 4, 256, 0, ctx->stream>>>(G, ctx->M, ctx->S, zs ? ctx->z : ctx->r,
                                                   ctx->P[parity], ctx->P[parity ^ 1], 1,
                                                 nullptr, 0, nullptr, 0);
       CK(cudaGetLastError());
@@ -870,14 +925,22 @@ int enqueue_iteration(pot3d_ctx *ctx, int parity) {
   if (multi) {
     TRY(gather_sums(ctx, 2));
     MARK("allgather_rz_rr");
-    if (pc2)
+    if (zs)
       k_finalize_rr<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks, ctx->hist);
     else
       k_finalize_beta<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks, ctx->hist);
     CK(cudaGetLastError());
     ctx->n_enq++;
   }
-  if (ctx->pc == 3) TRY(poly_apply(ctx, 1, true, ctx->nrhs));
+  if (ctx->pc == 3) {
+    TRY(poly_apply(ctx, multi ? 0 : 1, true, ctx->nrhs));
+    if (multi) {  // r.z across the ranks, then rho / beta
+      TRY(gather_sums(ctx, 1));
+      k_finalize_rho<<<1, 1, 0, ctx->stream>>>(ctx->S, ctx->gathered, ctx->nranks);
+      CK(cudaGetLastError());
+      ctx->n_enq++;
+    }
+  }
   if (pc2) {
     // a batch leader: the sweeps of all nrhs problems in one launch per sweep
     const long long vst = ctx->nrhs > 1 ? (long long)(G.nr_loc + 2) * G.plane : 0;
@@ -1144,24 +1207,31 @@ int solve_begin(pot3d_ctx *ctx, double rtol, int64_t maxit, int phase = 0) {
       if (phase == 1) return 0;
     }
   }  // phase != 2
-  if (warm) {
-    // r = b - A x0 over every cell and its periodic ghost columns (a stencil operand
-    // of pass A); x0's ghost shells hold the neighbours' edge shells (halo) or zero
-    k_apply<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->x, ctx->r, ctx->bshell, G.i0 == 0 ? 0 : -1000, nullptr,
-                                    nullptr, nullptr);
-    k_fix_ghost_cols<<<(G.nr_loc * ctx->nt + 255) / 256, 256, 0, s>>>(G, ctx->r, 0, G.nr_loc);
-    CK(cudaGetLastError());
-    ctx->n_launch += 2;
+  if (phase != 3) {  // phase 3 starts at the init dots (loopback PC3, after the z0 steps)
+    if (warm) {
+      // r = b - A x0 over every cell and its periodic ghost columns (a stencil operand
+      // of pass A); x0's ghost shells hold the neighbours' edge shells (halo) or zero
+      k_apply<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->x, ctx->r, ctx->bshell, G.i0 == 0 ? 0 : -1000, nullptr,
+                                      nullptr, nullptr);
+      k_fix_ghost_cols<<<(G.nr_loc * ctx->nt + 255) / 256, 256, 0, s>>>(G, ctx->r, 0, G.nr_loc);
+      CK(cudaGetLastError());
+      ctx->n_launch += 2;
+    }
+    // z0 = M^-1 r0, rho0 = r0.z0, ||b|| (a10 init)
+    if (ctx->pc == 2) {
+      int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
+                         s, false);
+      TRY(nk);
+      CK(cudaGetLastError());
+      ctx->n_launch += nk;
+    }
+    if (ctx->pc == 3) {
+      // loopback slabs exchange d between the Chebyshev steps phase by phase: solve_run
+      // runs z0's steps for the whole group, then phase 3
+      if (ctx->group) return 0;
+      TRY(poly_apply(ctx, 0, false));  // z0 = M^-1 r0 (rank processes: NCCL halos)
+    }
   }
-  // z0 = M^-1 r0, rho0 = r0.z0, ||b|| (a10 init)
-  if (ctx->pc == 2) {
-    int nk = pc2_apply(ctx->pc2, ctx->M, ctx->S, ctx->r, ctx->z, ctx->partials, 0, ctx->local_sum,
-                       s, false);
-    TRY(nk);
-    CK(cudaGetLastError());
-    ctx->n_launch += nk;
-  }
-  if (ctx->pc == 3) TRY(poly_apply(ctx, 0, false));  // z0 = M^-1 b
   k_init_dots<<<148 * 4, 256, 0, s>>>(G, ctx->M, ctx->S, ctx->r, ctx->partials, ctx->nranks == 1,
                                       ctx->local_sum, ctx->pc >= 2, ctx->z, warm ? 1 : 0,
                                       warm ? ctx->hist : nullptr);
@@ -1292,6 +1362,19 @@ int solve_run(pot3d_ctx *h, std::vector<pot3d_ctx *> &M, double rtol, int64_t ma
     for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit, 2));
   } else {
     for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit));
+  }
+  if (!batch && M.size() > 1 && M[0]->pc == 3) {  // loopback PC3: z0's steps phase by phase
+    std::vector<std::vector<Step>> st;
+    for (pot3d_ctx *m : M) st.push_back(poly_steps(m, 0, false));
+    for (size_t q = 0; q < st[0].size(); q++)
+      for (size_t k = 0; k < st.size(); k++) {
+        int rc = st[k][q]();
+        if (rc) {
+          h->err = M[k]->err;
+          return rc;
+        }
+      }
+    for (pot3d_ctx *m : M) TRY(solve_begin(m, rtol, maxit, 3));
   }
   if (!batch && (M.size() > 1 || M[0]->nranks > 1)) TRY(gather_all(M));
   for (pot3d_ctx *m : M) TRY(solve_init_end(m));
@@ -1626,9 +1709,8 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
   ctx->variant = R.variant;
   ctx->poly_m = R.poly_degree > 0 ? R.poly_degree : 4;
   ctx->poly_ratio = R.poly_ratio > 0.0 ? R.poly_ratio : 100.0;
-  if (pc == POT3D_PC3 && (ctx->nranks > 1 || member || R.variant != 0 || ctx->poly_m < 2 ||
-                          ctx->poly_m > POLY_MMAX || !(ctx->poly_ratio > 1.0))) {
-    ctx->err = "PC3 runs on one rank (no loopback, standard PCG) with 2 <= poly_degree <= 8, poly_ratio > 1";
+  if (pc == POT3D_PC3 && (R.variant != 0 || ctx->poly_m < 2 || ctx->poly_m > POLY_MMAX || !(ctx->poly_ratio > 1.0))) {
+    ctx->err = "PC3 runs the standard PCG with 2 <= poly_degree <= 8, poly_ratio > 1";
     return fail(POT3D_ERR_INVALID);
   }
   if (ctx->variant != 0 && (ctx->variant != 1 || pc != POT3D_PC1)) {

@@ -190,6 +190,8 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
         threadIdx.x == 0) {
       if (A.finalize)
         finalize_rho(S, tot[0]);
+      else if (A.peers)  // the same slot and sequence as the PC2 sweeps' r.z
+        mail_post(A.peers, MAIL_C, tot[0], 0.0, mail_seq(S->epoch, S->iter), S);
       else
         A.local_sum[0] = tot[0];
     }

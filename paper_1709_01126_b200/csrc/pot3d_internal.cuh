@@ -286,6 +286,7 @@ struct PolyArgs {
   int finalize;          // LAST: 1 updates rho/beta, 0 writes local_sum
   int predicated;        // skip when the PCG loop has stopped
   long long pstride;     // a batch (grid z / k_poly_init grid y = the problem): partials stride
+  const PeerTab *peers;  // across ranks with peer memory: LAST posts r.z to every mailbox (MAIL_C)
 };
 
 // Arguments of the field kernels (a11).

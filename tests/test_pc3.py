@@ -10,6 +10,7 @@ import oracle
 import synth
 
 pytestmark = pytest.mark.gpu
+SS, CW = synth.SOURCE_SURFACE, synth.CLOSED_WALL
 
 
 def solver(rf, tf, pf, br, poly=(4, 100.0), **kw):
@@ -57,11 +58,28 @@ def test_pc3_closed_wall_and_fixed_iterations():
             assert np.abs(r.phi - o["x"]).max() <= 1e-12 * np.abs(o["x"]).max()
 
 
-def test_pc3_rejects_multi_rank_setups():
+def test_pc3_rejects_bad_parameters():
     from paper_1709_01126_b200.pot3d import Pot3dError
 
     c = synth.CONFIGS["tiny"]
     with pytest.raises(Pot3dError):
-        solver(*c.faces(), c.br0(), loopback_slabs=2)
+        solver(*c.faces(), c.br0(), variant=1)
     with pytest.raises(Pot3dError):
         solver(*c.faces(), c.br0(), poly=(1, 100.0))
+
+
+@pytest.mark.parametrize("k,bc", [(2, SS), (3, SS), (2, CW)])
+def test_pc3_loopback_slabs(k, bc):
+    """PC3 across r-slabs (loopback groups: the ranks' exchange on one GPU, a halo of d
+    between the Chebyshev steps, r.z through the mailboxes): the oracle's PC3 solve
+    (the polynomial acts on the global operator, so the slabs do not change it)."""
+    c = synth.CONFIGS["small"]
+    rf, tf, pf = c.faces()
+    br = c.br0()
+    ref = oracle.solve(rf, tf, pf, br, bc=bc, pc=3, poly=(4, 100.0), rtol=1e-9)
+    with solver(rf, tf, pf, br, bc=bc, loopback_slabs=k) as s:
+        res = s.solve(rtol=1e-9)
+        again = s.solve(rtol=1e-9)
+    assert res.status == 0 and abs(res.iters - ref["iters"]) <= 1, (res.iters, ref["iters"])
+    assert np.linalg.norm(res.phi - ref["x"]) <= 1e-9 * np.linalg.norm(ref["x"])
+    assert again.iters == res.iters and np.array_equal(again.phi, res.phi)

@@ -29,6 +29,9 @@ cases.append(("thin", 2, 1, synth.SOURCE_SURFACE, 0))
 # CG1 (single-reduction PCG) across ranks: NCCL halo + one all-gather
 cases += [("tiny", 1, 1, synth.SOURCE_SURFACE, 1), ("small", 1, 1, synth.CLOSED_WALL, 1),
           ("thin", 1, 1, synth.SOURCE_SURFACE, 1)]
+# PC3 (Chebyshev-accelerated Jacobi) across ranks: a halo of d between the steps
+cases += [("small", 3, 1, synth.SOURCE_SURFACE, 0), ("small", 3, 1, synth.CLOSED_WALL, 0),
+          ("thin", 3, 1, synth.SOURCE_SURFACE, 0)]
 for name, pc, blocks, bc, variant in cases:
     c = synth.Config("thin", 2 * world, 17, 33, lmax=4) if name == "thin" else synth.CONFIGS[name]
     rf, tf, pf = c.faces()
