@@ -80,7 +80,7 @@ typedef enum {
 
 typedef enum { POT3D_SOURCE_SURFACE = 0, POT3D_CLOSED_WALL = 1 } pot3d_outer_bc; /* P:54 */
 typedef enum { POT3D_PC1 = 1, POT3D_PC2 = 2,                                    /* P:88 */
-               POT3D_PC3 = 3 /* Chebyshev-accelerated Jacobi (SURVEY §8(f)-2; one rank) */ } pot3d_pc;
+               POT3D_PC3 = 3 /* Chebyshev-accelerated Jacobi (SURVEY §8(f)-2) */ } pot3d_pc;
 
 typedef struct {
   int32_t nr, nt, np;            /* cell counts (ghosts excluded, A12); each >= 2 */

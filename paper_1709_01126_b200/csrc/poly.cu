@@ -9,7 +9,8 @@
 //               z_{k+1} = z_k + d_k
 // i.e. a fixed SPD polynomial in D^-1 A times D^-1 (interval [2/ratio, 2] of
 // D^-1 A's spectrum, bounded by Gershgorin).  It replaces the PC2 sweeps in the
-// same PCG: pass A reads the stored z, pass B updates r.  Single rank.
+// same PCG: pass A reads the stored z, pass B updates r.  Across ranks a halo of d
+// precedes every step (abi.cu poly_steps) and the last step posts r.z to the mailboxes.
 //
 //   k_poly_init (K0): res, d_0 = z_1 from r, cell by cell          [8 + 24 B/cell]
 //   k_poly_step (K_k): the stencil of d_{k-1} from the staged, haloed box, then
