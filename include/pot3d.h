@@ -142,7 +142,9 @@ typedef struct {
   int32_t exchange;              /* inter-rank exchange of the PCG loop: 0 single rank,
                                     1 NCCL (send/recv halo + all-gather of the sums),
                                     2 peer memory (CUDA IPC over NVLink: the kernels store
-                                    halo shells and sums straight into the peers' buffers) */
+                                    halo shells and sums straight into the peers' buffers),
+                                    3 the same exchange between the slabs of a loopback
+                                    group on one device */
   int32_t chunks_a, chunks_b;    /* r-chunks per tile column of the two fused passes */
   int32_t nrhs;                  /* problems per solve (pot3d_runtime.nrhs; 1 unless a batch);
                                     bytes_per_iter then counts all of them */
