@@ -358,7 +358,7 @@ int halo_exchange(pot3d_ctx *ctx, double *a, cudaStream_t st = nullptr) {
 // arrays.  Enabled only when every rank succeeded (else the NCCL path stays).
 int setup_xfer(pot3d_ctx *ctx) {
   struct IpcInfo {
-    cudaIpcMemHandle_t h[3];
+    cudaIpcMemHandle_t h[5];  // P[0], P[1], the mailbox; PC3: the Chebyshev d[0], d[1]
     int32_t ok, nr_loc, pad0, pad1;
   };
   const int n = ctx->nranks, me = ctx->rank;
@@ -368,7 +368,9 @@ int setup_xfer(pot3d_ctx *ctx) {
   mine.nr_loc = ctx->G.nr_loc;
   if (mine.ok && (cudaIpcGetMemHandle(&mine.h[0], ctx->P[0]) != cudaSuccess ||
                   cudaIpcGetMemHandle(&mine.h[1], ctx->P[1]) != cudaSuccess ||
-                  cudaIpcGetMemHandle(&mine.h[2], ctx->mail) != cudaSuccess)) {
+                  cudaIpcGetMemHandle(&mine.h[2], ctx->mail) != cudaSuccess ||
+                  (ctx->pc == POT3D_PC3 && (cudaIpcGetMemHandle(&mine.h[3], ctx->p_d[0]) != cudaSuccess ||
+                                            cudaIpcGetMemHandle(&mine.h[4], ctx->p_d[1]) != cudaSuccess)))) {
     cudaGetLastError();
     mine.ok = 0;
   }
@@ -402,6 +404,10 @@ int setup_xfer(pot3d_ctx *ctx) {
     for (int q = 0; q < 2 && ok; q++) {
       if (me > 0) ok = ok && (T.p_lo[q] = static_cast<double *>(open(all[me - 1].h[q]))) != nullptr;
       if (me < n - 1) ok = ok && (T.p_hi[q] = static_cast<double *>(open(all[me + 1].h[q]))) != nullptr;
+    }
+    for (int q = 0; q < 2 && ok && ctx->pc == POT3D_PC3; q++) {
+      if (me > 0) ok = ok && (T.d_lo[q] = static_cast<double *>(open(all[me - 1].h[3 + q]))) != nullptr;
+      if (me < n - 1) ok = ok && (T.d_hi[q] = static_cast<double *>(open(all[me + 1].h[3 + q]))) != nullptr;
     }
   }
   // agreement: all ranks or none
@@ -810,7 +816,10 @@ std::vector<Step> poly_steps(pot3d_ctx *ctx, int finalize, bool iteration, int n
   a.finalize = finalize;
   a.predicated = iteration ? 1 : 0;
   a.peers = peers;
-  const bool pdl = ctx->pdl && iteration && ctx->nranks == 1;
+  // across ranks with peer memory the kernels exchange d's halo themselves (flags)
+  const bool peer_halo = ctx->nranks > 1 && ctx->xfer && ctx->peers && ctx->pc == POT3D_PC3;
+  a.hpeers = peer_halo ? ctx->peers : nullptr;
+  const bool pdl = ctx->pdl && iteration && (ctx->nranks == 1 || peer_halo);
   auto count = [ctx, iteration]() {
     if (iteration)
       ctx->n_enq++;
@@ -826,7 +835,7 @@ std::vector<Step> poly_steps(pot3d_ctx *ctx, int finalize, bool iteration, int n
   ak.G.nchunks = ctx->nchunks_b;
   const dim3 grd(G.ntj * G.ntk, ctx->nchunks_b, nz);
   for (int k = 1; k < ctx->poly_m; k++) {
-    if (ctx->nranks > 1) {
+    if (ctx->nranks > 1 && !peer_halo) {
       const int src = (k - 1) & 1;  // d_{k-1}
       st.push_back([=]() -> int { return halo_slab(ctx, src ? poly_d1 : poly_d0); });
     }
@@ -1861,7 +1870,12 @@ static int setup_one(const pot3d_grid *grid, const double *br0, int32_t outer_bc
       ctx->p_d[1] = slot->pd1;
       ctx->p_x = slot->px;
     } else {
-      DA(ctx->p_res, cells); DA(ctx->p_d[0], cells); DA(ctx->p_d[1], cells); DA(ctx->p_x, cells);
+      DA(ctx->p_res, cells); DA(ctx->p_x, cells);
+      if (ctx->xfer_want) {  // peer memory: the neighbours store d's halo straight into these
+        if ((rc = ipc_alloc(ctx, &ctx->p_d[0], cells)) || (rc = ipc_alloc(ctx, &ctx->p_d[1], cells))) return fail(rc);
+      } else {
+        DA(ctx->p_d[0], cells); DA(ctx->p_d[1], cells);
+      }
     }
     for (double *p : {ctx->p_res, ctx->p_d[0], ctx->p_d[1], ctx->p_x})
       if (cudaMemsetAsync(p, 0, cells * sizeof(double), ctx->stream)) { ctx->err = "memset"; return fail(POT3D_ERR_CUDA); }
@@ -2035,6 +2049,10 @@ static int setup_group(const pot3d_grid *grid, const double *br0, int32_t outer_
     for (int b = 0; b < 2; b++) {
       if (q > 0) T.p_lo[b] = h->slabs[q - 1]->P[b];
       if (q < k - 1) T.p_hi[b] = h->slabs[q + 1]->P[b];
+      if (pc == POT3D_PC3) {
+        if (q > 0) T.d_lo[b] = h->slabs[q - 1]->p_d[b];
+        if (q < k - 1) T.d_hi[b] = h->slabs[q + 1]->p_d[b];
+      }
     }
     if (int rc = dalloc(m, &m->peers, 1)) { h->err = m->err; return fail(rc); }
     if (cudaMemcpyAsync(m->peers, &T, sizeof(PeerTab), cudaMemcpyHostToDevice, h->stream) != cudaSuccess) {

@@ -407,6 +407,31 @@ __device__ __forceinline__ bool edge_shells(const Grid &G, const Metrics &M, Sca
   __syncthreads();
   return s_edge_last;
 }
+// spin until *flag >= seq (a sequence that only grows: PC3's d halo flags)
+__device__ __forceinline__ bool xfer_wait_ge(const unsigned long long *flag, unsigned long long seq,
+                                             Scalars *S) {
+  if (ld_acquire_sys(flag) >= seq) return true;
+  const unsigned long long t0 = global_ns();
+  volatile int *err = &S->xfer_error;
+  while (ld_acquire_sys(flag) < seq) {
+    if (*err || global_ns() - t0 > XFER_TIMEOUT_NS) {
+      *err = 1;
+      return false;
+    }
+  }
+  return true;
+}
+// PC3: the neighbours' d-halo flags (caller: the last edge block, one thread)
+__device__ __forceinline__ void raise_dhalo_flags(const PeerTab *peers, unsigned long long seq) {
+  __threadfence_system();
+  if (peers->rank > 0) st_relaxed_sys(&peers->mail[peers->rank - 1]->dhalo[1], seq);
+  if (peers->rank < peers->nranks - 1) st_relaxed_sys(&peers->mail[peers->rank + 1]->dhalo[0], seq);
+}
+// the d-halo sequence of Chebyshev vector d_s of iteration S->iter: grows with both
+__device__ __forceinline__ unsigned long long dhalo_seq(const Scalars *S, int s) {
+  return mail_seq(S->epoch, S->iter * 8 + s + 1);
+}
+
 // neighbours' halo flags for seq (caller: the last block of edge_shells, one thread)
 __device__ __forceinline__ void raise_halo_flags(const PeerTab *peers, unsigned long long seq) {
   __threadfence_system();  // + relaxed stores = release of every block's ghost stores

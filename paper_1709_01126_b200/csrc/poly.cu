@@ -38,6 +38,11 @@ __global__ void k_poly_init(PolyArgs A) {
   const long long vo = (long long)blockIdx.y * (G.nr_loc + 2) * G.plane;  // a batch: problem blockIdx.y
   if (A.predicated && A.S[blockIdx.y].stop) return;
   const long long per = (long long)G.nt * G.np, n = per * G.nr_loc;
+  // peer memory: d_0's edge shells also into the neighbours' ghost shells of their d[0]
+  const PeerTab *hp = A.hpeers;
+  double *rlo = hp ? hp->d_lo[0] : nullptr, *rhi = hp ? hp->d_hi[0] : nullptr;
+  if (rlo) rlo += (long long)hp->nr_lo * G.plane;
+  if (rhi) rhi -= (long long)G.nr_loc * G.plane;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
     const int il = (int)(c / per);
     const long long t = c - il * per;
@@ -52,6 +57,22 @@ __global__ void k_poly_init(PolyArgs A) {
     d0[o] = dv;
     if (k == 0) d0[o + G.np] = dv;  // periodic ghost columns: d is a stencil operand
     if (k == G.np - 1) d0[o - G.np] = dv;
+    double *rem = il == 0 ? rlo : (il == G.nr_loc - 1 ? rhi : nullptr);
+    if (rem) {
+      rem[o] = dv;
+      if (k == 0) rem[o + G.np] = dv;
+      if (k == G.np - 1) rem[o - G.np] = dv;
+    }
+  }
+  if (hp) {  // every block's peer stores released, then the last raises the flags
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      if (atomicAdd(&A.S->counter[4], 1u) == gridDim.x * gridDim.y - 1) {
+        A.S->counter[4] = 0u;
+        raise_dhalo_flags(hp, dhalo_seq(A.S, 0));
+      }
+    }
   }
 }
 
@@ -76,6 +97,7 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
   const long long vo = zp * PL;
   const int src = (step - 1) & 1;  // d_{k-1} lives in d[(k-1) & 1]
   const void *map_d = &T.d_h[src];
+  const PeerTab *hp = A.hpeers;  // peer memory: the d halo (flags) instead of host-side copies
   constexpr unsigned DB = TR * SROW * 8u, IB = TJ * TKB * 8u;
   RowC rw[RPW];
 #pragma unroll
@@ -85,6 +107,13 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
     if (qi <= L + 1) {
       const int il = t.c0 - 1 + qi;
       const bool rown = (qi >= 1) && (qi <= L);
+      if (hp && (il < 0 || il >= G.nr_loc)) {  // a ghost shell: the neighbour's d_{k-1}
+        const int side = il < 0 ? 0 : 1;
+        if (side == 0 ? hp->rank > 0 : hp->rank < hp->nranks - 1) {
+          xfer_wait_ge(&hp->mail[hp->rank]->dhalo[side], dhalo_seq(S, step - 1), S);
+          fence_proxy_async_global();
+        }
+      }
       mbar_arrive_expect_tx(&sm.bar[si], rown ? DB + (LAST ? 3 : 2) * IB : DB);
       tma_load_3d(&sm.d[si][0][0], map_d, &sm.bar[si], t.k0 - 3 + COFF, t.j0 - 1, zp + il + 1);
       if (rown) {
@@ -113,6 +142,10 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
   for (int e = 0; e < RPW; e++) dm[e] = dc[e] = dn[e] = Z2;
   double acc = 0.0;
   double *g_d = A.d[src ^ 1] + vo + (long long)(t.c0 + 1) * PL;  // + rowoff[e]: plane c0
+  double *dlo = (hp && !LAST) ? hp->d_lo[src ^ 1] : nullptr, *dhi = (hp && !LAST) ? hp->d_hi[src ^ 1] : nullptr;
+  if (dlo) dlo += (long long)hp->nr_lo * PL;
+  if (dhi) dhi -= (long long)G.nr_loc * PL;
+  const bool edge_blk = hp && !LAST && (t.c0 == 0 || t.c1 == G.nr_loc);
   double *g_res = A.res + vo + (long long)(t.c0 + 1) * PL;
   double *g_x = (LAST ? A.z : A.x) + vo + (long long)(t.c0 + 1) * PL;
   int st = 0, so = NS_C - 1;
@@ -168,6 +201,11 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
         } else {
           POT3D_CHK(S, in_range(g_d + o, A.d[src ^ 1] + vo, (G.nr_loc + 2) * PL), CHK_PASS_STORE);
           store_pair<FAST>(g_d + o, t, G.np, dnw, true);
+          if (edge_blk) {
+            const int il = t.c0 + q - 2;  // the shell of this store
+            double *rem = il == 0 ? dlo : (il == G.nr_loc - 1 ? dhi : nullptr);
+            if (rem) store_pair<FAST>(rem + (g_d - (A.d[src ^ 1] + vo)) + o, t, G.np, dnw, false);
+          }
           st2(g_res + o, resn);
           st2(g_x + o, xn);
         }
@@ -184,6 +222,17 @@ __device__ __forceinline__ void poly_step_body(const PolyMaps &T, const PolyArgs
     so = st;
     st = wrap_inc(st, NS_C);
     ph ^= (st == 0);
+  }
+  if (edge_blk) {  // every edge block's peer stores released, then the last raises the flags
+    const unsigned nedge = (unsigned)(gridDim.x * (G.nchunks > 1 ? 2 : 1));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      if (atomicAdd(&S->counter[4], 1u) == nedge - 1) {
+        S->counter[4] = 0u;
+        raise_dhalo_flags(hp, dhalo_seq(S, step));
+      }
+    }
   }
   if (LAST) {
     double v[1] = {acc}, tot[1];

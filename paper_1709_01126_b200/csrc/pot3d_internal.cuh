@@ -151,11 +151,13 @@ enum TraceSlot { TR_EDGE0 = 0, TR_EDGE1, TR_A0, TR_AHALO, TR_A1, TR_F0, TR_F1, T
 struct Mailbox {
   MailEntry e[4][MAXR];         // [kind][source rank]
   unsigned long long halo[2];   // ghost shell filled: [0] from rank-1, [1] from rank+1
-  unsigned long long pad[6];
+  unsigned long long dhalo[2];  // PC3: the Chebyshev d's ghost shell filled (sequence grows)
+  unsigned long long pad[4];
 };
 struct PeerTab {
   Mailbox *mail[MAXR];          // every rank's mailbox (own included)
   double *p_lo[2], *p_hi[2];    // P[0], P[1] of rank-1 / rank+1 (nullptr at the ends)
+  double *d_lo[2], *d_hi[2];    // PC3: the Chebyshev d buffers of rank-1 / rank+1 (or nullptr)
   int rank, nranks, nr_lo, pad; // nr_lo: nr_loc of rank-1 (its top ghost shell index)
 };
 __host__ __device__ inline unsigned long long mail_seq(unsigned long long epoch, long long iter1) {
@@ -287,6 +289,8 @@ struct PolyArgs {
   int predicated;        // skip when the PCG loop has stopped
   long long pstride;     // a batch (grid z / k_poly_init grid y = the problem): partials stride
   const PeerTab *peers;  // across ranks with peer memory: LAST posts r.z to every mailbox (MAIL_C)
+  const PeerTab *hpeers; // ... and the d halo: init / step k store d's edge shells into the
+                         // neighbours' ghost shells and raise dhalo; step k waits for d_{k-1}'s
 };
 
 // Arguments of the field kernels (a11).

@@ -28,4 +28,4 @@ def test_checked_build_runs_every_protocol_clean():
     r = subprocess.run([sys.executable, str(ROOT / "tools" / "sanitize_cases.py")], cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert r.stdout.count(" OK") == 7, r.stdout
+    assert r.stdout.count(" OK") == 10, r.stdout

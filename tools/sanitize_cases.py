@@ -17,14 +17,19 @@ from paper_1709_01126_b200 import Pot3d  # noqa: E402
 rf, tf, pf = synth.grid(10, 17, 70)
 br = synth.br0_map(tf, pf, lmax=3, seed=1)
 cases = [dict(pc=1), dict(pc=2), dict(pc=2, pc2_blocks=2), dict(pc=1, loopback_slabs=2),
-         dict(pc=2, loopback_slabs=2), dict(pc=1, variant=1), dict(pc=1, variant=1, loopback_slabs=2)]
+         dict(pc=2, loopback_slabs=2), dict(pc=1, variant=1), dict(pc=1, variant=1, loopback_slabs=2),
+         dict(pc=3), dict(pc=3, loopback_slabs=2), dict(pc=1, nrhs=2)]
 ok = True
 for kw in cases:
     blocks = kw.get("pc2_blocks", 1) * max(1, kw.get("loopback_slabs", 1))
     ref = oracle.solve(rf, tf, pf, br, pc=kw["pc"], pc2_blocks=blocks, rtol=1e-9,
                        variant=kw.get("variant", 0))
-    with Pot3d(rf, tf, pf, br, **kw) as s:
+    nrhs = kw.get("nrhs", 1)
+    with Pot3d(rf, tf, pf, np.stack([br] * nrhs) if nrhs > 1 else br, **kw) as s:
         res = s.solve(rtol=1e-9)
+        if nrhs > 1:  # a batch of the same map twice: both problems are this solve
+            assert np.array_equal(res.phi[0], res.phi[1])
+            res.phi, res.iters = res.phi[0], int(res.iters[0])
         if kw == cases[0]:
             s.field()
             x = synth.random_vector(10 * 17 * 70, 1).reshape(70, 17, 10)
