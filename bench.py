@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--pc2-blocks", type=int, default=1)
     ap.add_argument("--variant", type=int, default=0, choices=[0, 1],
                     help="0 standard PCG, 1 single-reduction CG1 (PC1; SURVEY 8(f)-1)")
+    ap.add_argument("--poly", default="4,100",
+                    help="PC3: Chebyshev steps m and the interval ratio (pot3d_runtime.poly_degree, poly_ratio)")
     ap.add_argument("--weak-iters", type=int, default=300)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=20)
@@ -73,8 +75,10 @@ def workload_desc(c, args):
     mp = "dipole" if c.lmax == 0 else f"dipole + l<={c.lmax} multipoles seed {c.seed} (A14)"
     if k > 1:
         mp = f"a batch of {k} maps: dipole + l<={c.lmax} multipoles seeds {c.seed}-{c.seed + k - 1} (A14)"
+    poly = getattr(args, "poly", "4,100")
     return (f"{c.name} {c.nr}x{c.nt}x{c.np} {law}, {mp}, "
             f"{'source surface' if c.bc == 0 else 'closed wall'}, PC{c.pc}"
+            f"{f' (m, ratio = {poly})' if c.pc == 3 else ''}"
             f"{', CG1 single-reduction PCG' if getattr(args, 'variant', 0) else ''}")
 
 
@@ -260,7 +264,8 @@ def main():
         raise SystemExit(f"--config {args.config}: batches run on one GPU (pot3d_runtime.nrhs, DESIGN.md §7.8)")
     br_np = synth.batch_maps(c, (rf, tf, pf)) if kb > 1 else c.br0((rf, tf, pf))
     s = Pot3d(rf, tf, pf, br_np, bc=c.bc, pc=c.pc, rank=rank, nranks=world,
-              pc2_blocks=args.pc2_blocks, unroll=32, variant=args.variant, nrhs=kb)  # fresh NCCL id inside
+              pc2_blocks=args.pc2_blocks, unroll=32, variant=args.variant, nrhs=kb,
+              poly=(int(args.poly.split(",")[0]), float(args.poly.split(",")[1])))  # fresh NCCL id inside
     lead = (kb,) if kb > 1 else ()
     s.trace(True)  # in-situ pass durations of the timed solves (%globaltimer, no extra launches)
     info = s.info()
@@ -378,9 +383,10 @@ def main():
     elif info["pc"] == 2:
         kern += [("k_pass_b_pc2", 40 * cells_loc, 1.0, ms_b),
                  ("k_sweepS (forward + backward)", 56 * cells_loc, 1.0, ms_pc)]
-    else:  # PC3: the Chebyshev steps (48 m - 24 B/cell per apply, m = 4)
+    else:  # PC3: the Chebyshev steps (48 m - 24 B/cell per apply)
+        pm = int(args.poly.split(",")[0])
         kern += [("k_pass_b_pc2", 40 * cells_loc, 1.0, ms_b),
-                 ("k_poly_init + k_poly_step/last", (48 * 4 - 24) * cells_loc, 1.0, ms_pc)]
+                 ("k_poly_init + k_poly_step/last", (48 * pm - 24) * cells_loc, 1.0, ms_pc)]
     table = {k: {"bytes_per_launch": by, "launches_per_iter": lp, "ms": t, "gbs": by / (t * 1e-3) / 1e9,
                  "frac": by / (t * 1e-3) / 1e9 / peak} for k, by, lp, t in kern}
     dom, dom_bytes, _, dom_ms = max(kern, key=lambda k: k[2] * k[3])
